@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""CSK hot-path benchmark (BASELINE.json metric): time-to-1e-6 (sketch + iterate),
+iterations/s and sketch HBM GB/s on B200, plus the CPU oracle beside it.
+
+One "step" = one pass of the whole hot path over one synthetic problem resident in
+HBM: plan (S1/S2) + sketch with fused norms (S3/S4) + the persistent Algorithm 1
+loop (S5-S8) until RES <= 1e-6 or the iteration cap.
+Default workload: config C3 (see DESIGN.md §7 for why C3).  Between timed steps L2
+is flushed by writing a 256 MiB buffer (untimed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+N > 1 (torchrun): each rank solves its own independent C-config problem (weak
+scaling, no data-path collective) -- the sharded single-problem path is measured
+separately.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from csk_synth import CONFIGS, make_config  # noqa: E402
+
+METRIC = "CSK time-to-1e-6 rel err (sketch+iterate); iterations/s; sketch HBM GB/s"
+SMEM_BYTES_PER_CLK_PER_SM = 128  # B300_MICROARCH.md "smem crossbar BW 128/N B/cyc/SM"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 20 ms while running."""
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        return (time.perf_counter(), sm, mx, r)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._sample())
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self._nvml:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self, t0, t1):
+        if not self._nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        if not inside:  # timed region shorter than the sampling period: sample right at its end
+            try:
+                inside = [self._sample()]
+            except Exception:
+                inside = self.samples[-1:]
+        nv = self._nvml
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            "display_clock_setting": 0x100,
+        }
+        mask = 0
+        for s in inside:
+            mask |= int(s[3])
+        reasons = [k for k, v in names.items() if mask & v and k != "gpu_idle"]
+        return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": inside[-1][2],
+                "reasons": reasons, "samples": len(inside)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        rank = int(os.environ["RANK"])
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist, rank, ws, local
+    return None, 0, 1, 0
+
+
+def _barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def _max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def alg_bytes_sketch(cfg) -> int:
+    """8mn + 8m + 8dn + 8d (A, b read; A~, b~ written) + 8d (nsq)."""
+    return 8 * cfg.m * cfg.n + 8 * cfg.m + 8 * cfg.d * cfg.n + 16 * cfg.d
+
+
+def alg_bytes_iter(cfg) -> int:
+    """8dn + 16d per iteration (A~ + b~ + nsq)."""
+    return 8 * cfg.d * cfg.n + 16 * cfg.d
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, dist, rank, ws):
+    import paper_2004_02480_b200 as csk
+
+    cfg = CONFIGS[args.config]
+    hbm_peak, sm_max_mhz, peak_src = _peaks()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p = make_config(cfg, dev)
+    ctx = csk.Context()
+    d, n = cfg.d, cfg.n
+    At = torch.empty(d, n, dtype=torch.float64, device=dev)
+    bt = torch.empty(d, dtype=torch.float64, device=dev)
+    nsq = torch.empty(d, dtype=torch.float64, device=dev)
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        x.zero_()
+        if ev:
+            ev[0].record(stream)
+        csk.csk_sketch(p.A, p.b, d, seed=cfg.sketch_seed, ctx=ctx, out=(At, bt, nsq))
+        if ev:
+            ev[1].record(stream)
+        csk.csk_solve_async(At, bt, nsq, x, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters, ctx=ctx)
+        if ev:
+            ev[2].record(stream)
+        return csk.csk_solve_wait(ctx)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    reps = []
+    _barrier(dist)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(1.0)  # untimed: outside the events of step k
+        reps.append(step(evs[k]))
+    torch.cuda.synchronize()
+    _barrier(dist)
+    t1 = time.perf_counter()
+    sampler.stop()
+    clocks = sampler.summary(t0, t1)
+
+    sk = [e[0].elapsed_time(e[1]) for e in evs]
+    sv = [e[1].elapsed_time(e[2]) for e in evs]
+    tot = [a + b for a, b in zip(sk, sv)]
+    ms_step = _max_over_ranks(dist, sum(tot) / len(tot))
+    sk_ms = sum(sk) / len(sk)
+    sv_ms = sum(sv) / len(sv)
+    it = reps[-1].iterations
+    assert all(r.iterations == it for r in reps), "non-deterministic iteration count"
+
+    # roofline: the dominant kernel is the solve loop (A~ resident in SMEM at C1-C3)
+    loop_bytes = alg_bytes_iter(cfg) * it
+    loop_gbs = loop_bytes / (sv_ms * 1e-3) / 1e9
+    smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
+    sketch_gbs = alg_bytes_sketch(cfg) / (sk_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC,
+        "value": round(ms_step, 4),
+        "unit": "ms",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (torch Philox, PAPER.md:180 recipe; csk_synth.py)",
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "kind": cfg.kind,
+                   "tol": cfg.tol, "max_iters": cfg.max_iters, "sketch_seed": cfg.sketch_seed,
+                   "per_rank": "independent problem per rank" if ws > 1 else "single problem",
+                   "l2": "flushed between steps (256 MiB write, untimed); A (%.0f MB) > L2" % (cfg.bytes_A / 1e6)},
+        "iterations": it,
+        "final_res": reps[-1].final_res,
+        "termination": ["converged", "max_iters", "stagnated"][reps[-1].termination],
+        "iterations_per_s": round(it / (sv_ms * 1e-3), 1),
+        "sketch_ms": round(sk_ms, 5),
+        "solve_ms": round(sv_ms, 5),
+        "sketch_hbm_gbs": round(sketch_gbs, 1),
+        "us_per_iteration": round(sv_ms * 1e3 / max(it, 1), 4),
+        "roofline": {"kernel": "k_solve (persistent loop)", "bound": "smem",
+                     "achieved": round(loop_gbs, 1),
+                     "peak": round(smem_peak, 1), "unit": "GB/s", "frac": round(loop_gbs / smem_peak, 4),
+                     "traffic": None,
+                     "peak_source": f"derived: 148 SM x {SMEM_BYTES_PER_CLK_PER_SM} B/clk x {sm_max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                     "alg_bytes_per_iteration": alg_bytes_iter(cfg)},
+        "roofline_sketch": {"kernel": "plan + k_sketch_dense", "bound": "hbm",
+                            "achieved": round(sketch_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                            "frac": round(sketch_gbs / hbm_peak, 4), "peak_source": peak_src,
+                            "alg_bytes": alg_bytes_sketch(cfg)},
+        "clocks": clocks,
+        "gpu_launches": 4 * args.steps,
+        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_solve (+ CUB onesweep radix-sort kernels and one memset)",
+    }
+
+    # ---- e2e: the public API with HOST buffers, copies inside the timed region
+    if not args.no_e2e:
+        Ah = p.A.cpu().pin_memory()
+        bh = p.b.cpu().pin_memory()
+        xsh = p.x_star.cpu().pin_memory()
+        for _ in range(1):
+            csk.csk_run_host(Ah, bh, d, seed=cfg.sketch_seed, x_star=xsh, tol=cfg.tol, max_iters=cfg.max_iters, ctx=ctx)
+        times = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            ta = time.perf_counter()
+            xh, rep = csk.csk_run_host(Ah, bh, d, seed=cfg.sketch_seed, x_star=xsh, tol=cfg.tol,
+                                       max_iters=cfg.max_iters, ctx=ctx)
+            times.append((time.perf_counter() - ta) * 1e3)
+        e2e_ms = _max_over_ranks(dist, sum(times) / len(times))
+        out["e2e"] = {"value": round(e2e_ms, 4), "unit": "ms",
+                      "h2d_bytes_per_step": 8 * cfg.m * cfg.n + 8 * cfg.m + 16 * cfg.n,
+                      "d2h_bytes_per_step": 8 * cfg.n + 32,
+                      "api": "csk_run_host (C ABI, pinned host buffers)"}
+        del Ah, bh
+
+    # ---- CPU oracle beside it (rank 0, N = 1 only)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(cfg, p)
+
+    # ---- other configs (rank 0, N = 1): evidence for every §8(a) regime
+    if rank == 0 and ws == 1 and not args.no_extras:
+        out["per_config"] = extras(csk, ctx, [c for c in ("C1", "C2", "C4") if c != cfg.name], flush)
+    return out
+
+
+def extras(csk, ctx, names, flush):
+    res = {}
+    for nm in names:
+        cfg = CONFIGS[nm]
+        p = make_config(cfg, "cuda")
+        d, n = cfg.d, cfg.n
+        At = torch.empty(d, n, dtype=torch.float64, device="cuda")
+        bt = torch.empty(d, dtype=torch.float64, device="cuda")
+        nsq = torch.empty(d, dtype=torch.float64, device="cuda")
+        x = torch.zeros(n, dtype=torch.float64, device="cuda")
+        st = torch.cuda.current_stream()
+        rows = []
+        for k in range(4):
+            flush.fill_(1.0)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            x.zero_()
+            e[0].record(st)
+            csk.csk_sketch(p.A, p.b, d, seed=cfg.sketch_seed, ctx=ctx, out=(At, bt, nsq))
+            e[1].record(st)
+            csk.csk_solve_async(At, bt, nsq, x, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters, ctx=ctx)
+            e[2].record(st)
+            rep = csk.csk_solve_wait(ctx)
+            if k:
+                rows.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), rep))
+        sk = statistics.median(r[0] for r in rows)
+        sv = statistics.median(r[1] for r in rows)
+        rep = rows[-1][2]
+        res[nm] = {"ms_per_step": round(sk + sv, 4), "sketch_ms": round(sk, 5), "solve_ms": round(sv, 4),
+                   "iterations": rep.iterations, "final_res": rep.final_res,
+                   "termination": ["converged", "max_iters", "stagnated"][rep.termination],
+                   "iterations_per_s": round(rep.iterations / (sv * 1e-3), 1),
+                   "us_per_iteration": round(sv * 1e3 / max(rep.iterations, 1), 4),
+                   "sketch_hbm_gbs": round(alg_bytes_sketch(cfg) / (sk * 1e-3) / 1e9, 1),
+                   "loop_gbs": round(alg_bytes_iter(cfg) * rep.iterations / (sv * 1e-3) / 1e9, 1)}
+        del p, At
+        torch.cuda.empty_cache()
+    return res
+
+
+# ------------------------------------------------------------------ oracle arm
+def _oracle_sample(cfg, A, b, xs, budget_s=20.0):
+    """Time the oracle (1 core) on the workload: sketch + norms + loop.  Small configs run
+    whole; if the full loop would exceed ``budget_s`` the loop is run for a bounded number
+    of iterations and the per-iteration time is extrapolated to the GPU's iteration count."""
+    import oracle
+    t0 = time.perf_counter()
+    At, bt = oracle.sketch_dense(A, b, cfg.d, seed=cfg.sketch_seed)
+    nsq = oracle.row_norms(At)
+    t_sketch = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    probe = oracle.solve(At, bt, nsq, x_star=xs, tol=cfg.tol, max_iters=20)
+    t_probe = (time.perf_counter() - t1) / max(probe.iterations, 1)
+    cap = max(1, int((budget_s - t_sketch) / max(t_probe, 1e-9)))
+    t2 = time.perf_counter()
+    r = oracle.solve(At, bt, nsq, x_star=xs, tol=cfg.tol, max_iters=min(cfg.max_iters, cap))
+    t_loop = time.perf_counter() - t2
+    complete = r.termination == 0 or r.iterations >= cfg.max_iters
+    per_it = t_loop / max(r.iterations, 1)
+    return t_sketch, t_loop, per_it, r, complete
+
+
+def cpu_baseline(cfg, p):
+    A = p.A.cpu().numpy()
+    b = p.b.cpu().numpy()
+    xs = p.x_star.cpu().numpy()
+    t_sketch, t_loop, per_it, r, complete = _oracle_sample(cfg, A, b, xs)
+    if complete:
+        val = (t_sketch + t_loop) * 1e3
+        sample = f"whole {cfg.name} solve (sketch + {r.iterations} iterations)"
+    else:
+        val = (t_sketch + per_it * cfg.max_iters) * 1e3
+        sample = (f"{cfg.name}: sketch + {r.iterations} iterations timed, loop extrapolated "
+                  f"to {cfg.max_iters} at {per_it * 1e3:.2f} ms/iteration")
+    return {"value": round(val, 3), "unit": "ms", "cores": 1, "kind": "oracle", "sample": sample,
+            "iterations": r.iterations, "sketch_ms": round(t_sketch * 1e3, 3),
+            "loop_ms_per_iteration": round(per_it * 1e3, 4)}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (plain C, 1 thread) on our arm's config/metric."""
+    import oracle
+    cfg = CONFIGS[args.config]
+    p = make_config(cfg, "cpu")
+    A, b, xs = p.A.numpy(), p.b.numpy(), p.x_star.numpy()
+    oracle.build()
+    for _ in range(args.warmup):
+        _oracle_sample(cfg, A, b, xs, budget_s=5.0)
+    times = []
+    last = None
+    for _ in range(args.steps):
+        t_sketch, t_loop, per_it, r, complete = _oracle_sample(cfg, A, b, xs, budget_s=20.0)
+        times.append((t_sketch + (t_loop if complete else per_it * cfg.max_iters)) * 1e3)
+        last = (r, complete, per_it)
+    v = sum(times) / len(times)
+    r, complete, per_it = last
+    sample = (f"whole {cfg.name} solve ({r.iterations} iterations)" if complete else
+              f"{cfg.name}: {r.iterations} iterations timed, extrapolated to {cfg.max_iters}")
+    return {"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3),
+            "higher_is_better": False, "impl": "reference", "dtype": "f64",
+            "data": "synthetic (torch Philox CPU stream, csk_synth.py)",
+            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d},
+            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "iterations": r.iterations, "vs_baseline": None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args)))
+        return
+    dist, rank, ws, _ = _dist()
+    out = run_ours(args, dist, rank, ws)
+    if rank == 0:
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * csk.h -- C ABI of the B200-native Count-Sketch Kaczmarz (CSK) hot path.
+ *
+ * Method: Zhang & Li, "A Count Sketch Kaczmarz Method for Solving Large
+ * Overdetermined Linear Systems", arXiv 2004.02480 (/root/reference/PAPER.md,
+ * cited as P:<line>).  The library computes, on an sm_100a GPU:
+ *   (1) the count sketch  A~ = S A,  b~ = S b,  S = Phi D   (Def. 1);
+ *   (2) the row norms     nsq_j = ||A~^(j)||_2^2             (P:62 denominator);
+ *   (3) the Algorithm 1 loop  i_k = argmax r_i^2/nsq_i,  x += (r_ik/nsq_ik) A~^(ik)T
+ *       with r = b~ - A~ x_k, stopped by RES <= tol or an iteration cap
+ *       (P:180).
+ *
+ * Conventions for every entry point:
+ *   - Every array argument is a DEVICE pointer unless the name ends in _host.
+ *     Floating point is IEEE fp64; matrices are row-major with the given leading
+ *     dimension; indices are 0-based (the paper's [m], [d] are 1-based).
+ *   - Ownership: the caller allocates and frees every input and output; the
+ *     library owns only the scratch workspaces inside a csk_ctx_t.
+ *   - Ordering: calls are asynchronous on `stream` (a cudaStream_t passed as
+ *     void*) unless stated otherwise; csk_solve* and *_host block until done
+ *     because they return a termination reason.
+ *   - Errors: every call returns a csk_status_t; no exception crosses the ABI.
+ *     csk_last_error(ctx) returns a human-readable reason for the last failure
+ *     on that context.  There is no CPU fallback: a call that cannot run on the
+ *     GPU fails.
+ *   - Alignment: A and A~ must be 16-byte aligned and `lda` even (128-bit
+ *     vector and TMA bulk-copy path); violations return CSK_E_ARG.
+ *   - Sizes: 1 <= d < m (Algorithm 1, "with d < m"), m < 2^31, n >= 1,
+ *     n <= CSK_MAX_N for csk_solve*.
+ */
+#ifndef CSK_H_
+#define CSK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CSK_API __attribute__((visibility("default")))
+#else
+#define CSK_API
+#endif
+
+#define CSK_ABI_VERSION 1
+#define CSK_MAX_N 2048 /* solve keeps x in registers: 64 columns per lane-pair group */
+
+typedef enum {
+    CSK_OK = 0,
+    CSK_E_ARG = 1,          /* bad size, null/misaligned pointer, d >= m, tol <= 0, ... */
+    CSK_E_ZERO_SKETCH = 2,  /* every row of A~ is zero: nothing to select */
+    CSK_E_UNSUPPORTED = 3,  /* valid input outside what this build implements */
+    CSK_E_CUDA = 4,         /* a CUDA runtime error; csk_last_error has the text */
+    CSK_E_NCCL = 5,         /* an NCCL error in a sharded call */
+    CSK_E_NOMEM = 6         /* workspace allocation failed */
+} csk_status_t;
+
+/* Termination of the Algorithm 1 loop. */
+typedef enum {
+    CSK_CONVERGED = 0,  /* stop quantity <= tol */
+    CSK_MAX_ITERS = 1,  /* k reached max_iters ("exceeds 20000"; configs: 50k) */
+    CSK_STAGNATED = 2   /* every unmasked residual is exactly 0 while not converged */
+} csk_term_t;
+
+/* Stop quantity: RES = ||x_k - x*||^2/||x*||^2 when x_star != NULL,
+ * else the solution-free relative residual ||b~ - A~ x_k||^2/||b~||^2. */
+typedef enum { CSK_STOP_RES = 0, CSK_STOP_RESIDUAL = 1 } csk_stop_mode_t;
+
+typedef struct {
+    int64_t iterations;   /* IT = number of projections applied */
+    double final_res;     /* stop quantity at the returned iterate */
+    int32_t termination;  /* csk_term_t */
+    int32_t stop_mode;    /* csk_stop_mode_t */
+    int64_t last_index;   /* i_{IT-1}, or -1 if no step was taken */
+} csk_report_t;
+
+/* Optional knobs and debug traces for csk_solve_ex.  Zero-initialise for defaults. */
+#define CSK_SOLVE_ASYNC 1 /* opts->flags: return right after the launch; csk_solve_wait fills the report */
+
+typedef struct {
+    int32_t num_ctas;      /* persistent CTAs (<= co-resident limit); 0 = auto */
+    int32_t smem_rows;     /* rows of A~ kept in shared memory per CTA: 0 = auto (max),
+                              -1 = none (every row re-read from L2/HBM), k > 0 = at most k */
+    int32_t flags;         /* CSK_SOLVE_ASYNC */
+    int32_t reserved;
+    int64_t trace_cap;     /* capacity of the traces below (iterations) */
+    int64_t *idx_trace;    /* device int64[trace_cap]: i_k, or NULL */
+    double *res_trace;     /* device double[trace_cap]: stop quantity at x_k, or NULL */
+    double *x_trace;       /* device double[trace_cap * n]: x_k row by row, or NULL */
+} csk_solve_opts_t;
+
+typedef struct csk_ctx_s *csk_ctx_t;
+
+/* ---- context --------------------------------------------------------------- */
+/* Binds the calling thread's CUDA device `device` and allocates nothing yet;
+ * workspaces grow on demand and are reused.  Not thread-safe: one ctx per thread. */
+CSK_API csk_status_t csk_ctx_create(int device, csk_ctx_t *out);
+CSK_API csk_status_t csk_ctx_destroy(csk_ctx_t ctx);
+CSK_API const char *csk_last_error(csk_ctx_t ctx);
+CSK_API const char *csk_status_string(csk_status_t status);
+CSK_API int csk_abi_version(void);
+
+/* ---- S1/S2: the count-sketch plan ------------------------------------------- */
+/* csk_hash: h[i] = floor(z_h * d / 2^64), sign[i] = (z_s >> 63) ? -1 : +1 with
+ *   z_h = SM64(seed, 2c), z_s = SM64(seed, 2c+1), c = row_offset + i and
+ *   SM64(seed, c) = splitmix64_mix(seed + (c+1) * 0x9E3779B97F4A7C15)  -- the
+ *   counter form of the SplitMix64 stream (reading R-1 of DESIGN.md), realising
+ *   Definition 1: h uniform on [d], D_ii = +-1 with probability 1/2.
+ *   `row_offset` lets a row shard hash with GLOBAL row indices.
+ *   h: int32[m], sign: int8[m] (device, caller-owned).  Requires d >= 1. */
+CSK_API csk_status_t csk_hash(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_t m, int64_t d,
+                      int32_t *h, int8_t *sign, void *stream);
+
+/* csk_plan: the stable bucketing of rows by h ("source-row order"):
+ *   perm[t] (int32[m]) lists the row indices grouped by bucket, ascending row
+ *   index inside each bucket, with bit 31 set when sign = -1;
+ *   offsets[j] (int32[d+1]) = first position of bucket j in perm, offsets[d] = m.
+ *   h/sign are taken from the seed (h_in == NULL) or from explicit device arrays
+ *   h_in int32[m] / sign_in int8[m] (the csk_sketch_with_map test hook; values
+ *   outside [0,d) or not +-1 return CSK_E_ARG after a stream sync). */
+CSK_API csk_status_t csk_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_t m, int64_t d,
+                      const int32_t *h_in, const int8_t *sign_in,
+                      int32_t *perm, int32_t *offsets, void *stream);
+
+/* ---- S3/S4: the sketch ------------------------------------------------------- */
+/* csk_sketch: A~ = S A (d x n, ld = n), b~ = S b (d), with S = Phi D drawn from
+ *   `seed` (Algorithm 1 "Initialize").  A~[j,:] = sum over rows i with
+ *   h(i) = j, in ascending i, of sign_i * A[i,:], starting from +0.0 -- the same
+ *   fp64 adds in the same order as the dense product Phi D A, so A~ and b~ are
+ *   bit-reproducible and equal to the oracle bit for bit.  If nsq != NULL the
+ *   row norms (S4) are fused into the epilogue (same arithmetic as csk_row_norms).
+ *   A: m x n, leading dimension lda >= n (even), 16-byte aligned.  1 <= d < m. */
+CSK_API csk_status_t csk_sketch(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
+                        int64_t m, int64_t n, int64_t d, uint64_t seed,
+                        double *A_tilde, double *b_tilde, double *nsq, void *stream);
+
+/* Test hook (Remark 1): explicit map h/sign (device int32[m] / int8[m]);
+ * allows d == m, e.g. h = identity, which turns CSK into MWRK. */
+CSK_API csk_status_t csk_sketch_with_map(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
+                                 int64_t m, int64_t n, int64_t d,
+                                 const int32_t *h, const int8_t *sign,
+                                 double *A_tilde, double *b_tilde, double *nsq, void *stream);
+
+/* CSR input (config C5): row_ptr int64[m+1], col int32[nnz] (distinct within a
+ * row, any order; the stored order is the accumulation order), val fp64[nnz]. */
+CSK_API csk_status_t csk_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col,
+                            const double *val, const double *b,
+                            int64_t m, int64_t n, int64_t d, uint64_t seed,
+                            double *A_tilde, double *b_tilde, double *nsq, void *stream);
+
+/* nsq[j] = ||A~^(j)||_2^2 for j < d (P:62 / P:122).  Fixed summation order:
+ * thread t of a row's team sums columns {2t, 2t+1} + 2T*q with fma, then a
+ * fixed-shape tree -- bit-identical to the fused sketch epilogue.  A~: ld = n. */
+CSK_API csk_status_t csk_row_norms(csk_ctx_t ctx, const double *A_tilde, int64_t d, int64_t n,
+                           double *nsq, void *stream);
+
+/* ---- S5-S8: the Algorithm 1 loop ---------------------------------------------- */
+/* csk_solve: x is x_0 on entry and the final iterate on exit.  One
+ *   persistent cooperative kernel runs every iteration: GEMV r = b~ - A~ x_k,
+ *   score r_i^2/nsq_i (rows with nsq_i = 0 masked), argmax with lowest-index
+ *   ties, x_{k+1} = x_k + (r_ik/nsq_ik) A~^(ik)T, stop test; A~ rows stay
+ *   resident in shared memory (the remainder is re-read from L2/HBM).
+ *   x_star != NULL: stop when RES <= tol; NULL: residual mode.
+ *   Stops at max_iters (>= 0).  Blocks; fills *report (host pointer).
+ *   Returns CSK_E_ZERO_SKETCH if every nsq is 0. */
+CSK_API csk_status_t csk_solve(csk_ctx_t ctx, const double *A_tilde, const double *b_tilde,
+                       const double *nsq, int64_t d, int64_t n, double *x,
+                       const double *x_star, double tol, int64_t max_iters,
+                       csk_report_t *report, void *stream);
+
+CSK_API csk_status_t csk_solve_ex(csk_ctx_t ctx, const double *A_tilde, const double *b_tilde,
+                          const double *nsq, int64_t d, int64_t n, double *x,
+                          const double *x_star, double tol, int64_t max_iters,
+                          const csk_solve_opts_t *opts, csk_report_t *report, void *stream);
+
+/* After csk_solve_ex(..., flags = CSK_SOLVE_ASYNC): synchronise the stream of the last
+ * solve on this ctx and fill *report (host).  Returns that solve's status
+ * (e.g. CSK_E_ZERO_SKETCH).  x is valid only after this returns. */
+CSK_API csk_status_t csk_solve_wait(csk_ctx_t ctx, csk_report_t *report);
+
+/* ---- Whole Algorithm 1 (INPUT A, b, d, x0 -> OUTPUT x) ---------------- */
+/* Plan + sketch + norms + loop on device buffers (workspace for A~, b~, nsq owned
+ * by ctx).  Blocks; fills *report. */
+CSK_API csk_status_t csk_run(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
+                     int64_t m, int64_t n, int64_t d, uint64_t seed, double *x,
+                     const double *x_star, double tol, int64_t max_iters,
+                     csk_report_t *report, void *stream);
+
+/* Same with HOST buffers (A_host: m x lda, b_host: m, x_host: n in/out,
+ * x_star_host: n or NULL).  Copies in, runs csk_run, copies x back; pinned host
+ * memory gives full PCIe bandwidth.  Blocks. */
+CSK_API csk_status_t csk_run_host(csk_ctx_t ctx, const double *A_host, int64_t lda, const double *b_host,
+                          int64_t m, int64_t n, int64_t d, uint64_t seed, double *x_host,
+                          const double *x_star_host, double tol, int64_t max_iters,
+                          csk_report_t *report, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSK_H_ */

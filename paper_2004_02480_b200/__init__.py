@@ -1,0 +1,360 @@
+"""B200-native Count-Sketch Kaczmarz (CSK) hot path -- thin Python binding of libcsk.
+
+Every function here is argument marshalling around the C ABI in ``include/csk.h``
+(same names): it checks dtypes/devices, passes ``data_ptr()``s and the current CUDA
+stream, and raises on a non-OK status.  All arithmetic runs in the CUDA kernels of
+``csrc/`` (sm_100a).  There is no CPU fallback: importing this package without the
+built ``libcsk.so`` raises, and every call needs CUDA tensors.
+
+Method: Zhang & Li, arXiv 2004.02480 -- Algorithm 1: sketch once
+(A~ = S A, b~ = S b, S = Phi D of Definition 1), then the maximal-weighted-
+residual Kaczmarz loop on (A~, b~) until RES <= tol.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcsk.so")
+
+CSK_OK, CSK_E_ARG, CSK_E_ZERO_SKETCH, CSK_E_UNSUPPORTED, CSK_E_CUDA, CSK_E_NCCL, CSK_E_NOMEM = range(7)
+CONVERGED, MAX_ITERS, STAGNATED = 0, 1, 2
+STOP_RES, STOP_RESIDUAL = 0, 1
+MAX_N = 2048
+SOLVE_ASYNC = 1
+
+
+class CskError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "CSK_OK", 1: "CSK_E_ARG", 2: "CSK_E_ZERO_SKETCH", 3: "CSK_E_UNSUPPORTED",
+           4: "CSK_E_CUDA", 5: "CSK_E_NCCL", 6: "CSK_E_NOMEM"}
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("final_res", ctypes.c_double),
+                ("termination", ctypes.c_int32), ("stop_mode", ctypes.c_int32),
+                ("last_index", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("num_ctas", ctypes.c_int32), ("smem_rows", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("trace_cap", ctypes.c_int64), ("idx_trace", ctypes.c_void_p),
+                ("res_trace", ctypes.c_void_p), ("x_trace", ctypes.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i64, u64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+    sigs = {
+        "csk_abi_version": ([], ctypes.c_int),
+        "csk_ctx_create": ([i32, ctypes.POINTER(P)], i32),
+        "csk_ctx_destroy": ([P], i32),
+        "csk_last_error": ([P], ctypes.c_char_p),
+        "csk_status_string": ([i32], ctypes.c_char_p),
+        "csk_hash": ([P, u64, i64, i64, i64, P, P, P], i32),
+        "csk_plan": ([P, u64, i64, i64, i64, P, P, P, P, P], i32),
+        "csk_sketch": ([P, P, i64, P, i64, i64, i64, u64, P, P, P, P], i32),
+        "csk_sketch_with_map": ([P, P, i64, P, i64, i64, i64, P, P, P, P, P, P], i32),
+        "csk_sketch_csr": ([P, P, P, P, P, i64, i64, i64, u64, P, P, P, P], i32),
+        "csk_row_norms": ([P, P, i64, i64, P, P], i32),
+        "csk_solve": ([P, P, P, P, i64, i64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
+        "csk_solve_ex": ([P, P, P, P, i64, i64, P, P, dbl, i64, ctypes.POINTER(SolveOpts),
+                          ctypes.POINTER(Report), P], i32),
+        "csk_solve_wait": ([P, ctypes.POINTER(Report)], i32),
+        "csk_run": ([P, P, i64, P, i64, i64, i64, u64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
+        "csk_run_host": ([P, P, i64, P, i64, i64, i64, u64, P, P, dbl, i64,
+                          ctypes.POINTER(Report), P], i32),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _extend_sharded(lib)
+    return lib
+
+
+def _extend_sharded(lib):
+    P, i64, u64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+    extra = {
+        "csk_comm_unique_id": ([P], i32),
+        "csk_comm_create": ([P, P, i32, i32], i32),
+        "csk_comm_destroy": ([P], i32),
+        "csk_shard_range": ([i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "csk_sketch_sharded": ([P, P, i64, P, i64, i64, i64, i64, i64, u64, P, P, P,
+                                ctypes.POINTER(i64), ctypes.POINTER(i64), P], i32),
+        "csk_solve_sharded": ([P, P, P, P, i64, i64, i64, i64, P, P, dbl, i64,
+                               ctypes.POINTER(Report), P], i32),
+        "csk_solve_virtual_ranks": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P,
+                                     ctypes.POINTER(Report), P], i32),
+    }
+    for name, (args, res) in extra.items():
+        if hasattr(lib, name):
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+
+
+lib = _load()
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need(t: torch.Tensor, dtype, name, dims=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if dims is not None and t.dim() != dims:
+        raise ValueError(f"{name} must be {dims}-D")
+
+
+class Context:
+    """Owns a ``csk_ctx_t`` (workspaces, plan scratch, optional NCCL communicator)."""
+
+    def __init__(self, device: int | None = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        h = ctypes.c_void_p()
+        st = lib.csk_ctx_create(device, ctypes.byref(h))
+        if st != CSK_OK:
+            raise CskError(st, "csk_ctx_create failed (needs an sm_100 GPU)")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib.csk_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int):
+        if st != CSK_OK:
+            raise CskError(st, lib.csk_last_error(self.handle).decode())
+
+
+_default: Context | None = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None or _default.device != torch.cuda.current_device():
+        _default = Context()
+    return _default
+
+
+# ------------------------------------------------------------------ S1/S2 plan
+def csk_hash(m: int, d: int, seed: int = 0, row_offset: int = 0, ctx: Context | None = None):
+    """(h int32[m], sign int8[m]) of Definition 1, counter-form SplitMix64."""
+    ctx = ctx or default_context()
+    h = torch.empty(m, dtype=torch.int32, device="cuda")
+    s = torch.empty(m, dtype=torch.int8, device="cuda")
+    ctx.check(lib.csk_hash(ctx.handle, seed & (2**64 - 1), row_offset, m, d, _ptr(h), _ptr(s), _stream()))
+    return h, s
+
+
+def csk_plan(m: int, d: int, seed: int = 0, row_offset: int = 0, h=None, sign=None,
+             ctx: Context | None = None):
+    """(perm int32[m] with sign in bit 31, offsets int32[d+1]) -- stable bucketing by h."""
+    ctx = ctx or default_context()
+    perm = torch.empty(m, dtype=torch.int32, device="cuda")
+    offsets = torch.empty(d + 1, dtype=torch.int32, device="cuda")
+    if h is not None:
+        _need(h, torch.int32, "h", 1)
+        _need(sign, torch.int8, "sign", 1)
+    ctx.check(lib.csk_plan(ctx.handle, seed & (2**64 - 1), row_offset, m, d, _ptr(h), _ptr(sign),
+                           _ptr(perm), _ptr(offsets), _stream()))
+    return perm, offsets
+
+
+# ------------------------------------------------------------------ S3/S4 sketch
+def csk_sketch(A: torch.Tensor, b: torch.Tensor, d: int, seed: int = 0, with_norms: bool = True,
+               ctx: Context | None = None, out=None):
+    """(A~, b~, nsq) = (S A, S b, row norms of A~) (Algorithm 1 "Initialize")."""
+    ctx = ctx or default_context()
+    _need(A, torch.float64, "A", 2)
+    _need(b, torch.float64, "b", 1)
+    if A.stride(1) != 1:
+        raise ValueError("A must be row-major (stride(1) == 1)")
+    m, n = A.shape
+    if out is None:
+        At = torch.empty(d, n, dtype=torch.float64, device=A.device)
+        bt = torch.empty(d, dtype=torch.float64, device=A.device)
+        nsq = torch.empty(d, dtype=torch.float64, device=A.device) if with_norms else None
+    else:
+        At, bt, nsq = out
+    ctx.check(lib.csk_sketch(ctx.handle, _ptr(A), A.stride(0), _ptr(b.contiguous()), m, n, d,
+                             seed & (2**64 - 1), _ptr(At), _ptr(bt), _ptr(nsq), _stream()))
+    return At, bt, nsq
+
+
+def csk_sketch_with_map(A, b, d: int, h, sign, with_norms: bool = True, ctx: Context | None = None):
+    """Sketch with an explicit map (test hook; d == m allowed, Remark 1 P:69)."""
+    ctx = ctx or default_context()
+    _need(A, torch.float64, "A", 2)
+    _need(h, torch.int32, "h", 1)
+    _need(sign, torch.int8, "sign", 1)
+    m, n = A.shape
+    At = torch.empty(d, n, dtype=torch.float64, device=A.device)
+    bt = torch.empty(d, dtype=torch.float64, device=A.device)
+    nsq = torch.empty(d, dtype=torch.float64, device=A.device) if with_norms else None
+    ctx.check(lib.csk_sketch_with_map(ctx.handle, _ptr(A), A.stride(0), _ptr(b.contiguous()), m, n, d,
+                                      _ptr(h), _ptr(sign), _ptr(At), _ptr(bt), _ptr(nsq), _stream()))
+    return At, bt, nsq
+
+
+def csk_sketch_csr(row_ptr, col, val, b, n: int, d: int, seed: int = 0, with_norms: bool = True,
+                   ctx: Context | None = None):
+    """CSR-input sketch (config C5)."""
+    ctx = ctx or default_context()
+    _need(row_ptr, torch.int64, "row_ptr", 1)
+    _need(col, torch.int32, "col", 1)
+    _need(val, torch.float64, "val", 1)
+    _need(b, torch.float64, "b", 1)
+    m = row_ptr.shape[0] - 1
+    At = torch.empty(d, n, dtype=torch.float64, device=val.device)
+    bt = torch.empty(d, dtype=torch.float64, device=val.device)
+    nsq = torch.empty(d, dtype=torch.float64, device=val.device) if with_norms else None
+    ctx.check(lib.csk_sketch_csr(ctx.handle, _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(b), m, n, d,
+                                 seed & (2**64 - 1), _ptr(At), _ptr(bt), _ptr(nsq), _stream()))
+    return At, bt, nsq
+
+
+def csk_row_norms(At: torch.Tensor, ctx: Context | None = None):
+    """nsq_j = ||A~^(j)||^2."""
+    ctx = ctx or default_context()
+    _need(At, torch.float64, "A_tilde", 2)
+    At = At.contiguous()
+    d, n = At.shape
+    nsq = torch.empty(d, dtype=torch.float64, device=At.device)
+    ctx.check(lib.csk_row_norms(ctx.handle, _ptr(At), d, n, _ptr(nsq), _stream()))
+    return nsq
+
+
+# ------------------------------------------------------------------ S5-S8 loop
+@dataclass
+class SolveResult:
+    x: torch.Tensor
+    iterations: int
+    final_res: float
+    termination: int
+    stop_mode: int
+    last_index: int
+    idx_trace: torch.Tensor | None = None
+    res_trace: torch.Tensor | None = None
+    x_trace: torch.Tensor | None = None
+
+
+def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
+              num_ctas: int = 0, smem_rows: int = 0, trace: int = 0, trace_x: bool = False,
+              ctx: Context | None = None) -> SolveResult:
+    """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel."""
+    ctx = ctx or default_context()
+    _need(At, torch.float64, "A_tilde", 2)
+    _need(bt, torch.float64, "b_tilde", 1)
+    _need(nsq, torch.float64, "nsq", 1)
+    At = At.contiguous()
+    d, n = At.shape
+    x = torch.zeros(n, dtype=torch.float64, device=At.device) if x0 is None else x0.clone().contiguous()
+    xs = None if x_star is None else x_star.contiguous()
+    opts = SolveOpts()
+    opts.num_ctas = num_ctas
+    opts.smem_rows = smem_rows
+    idx_t = res_t = x_t = None
+    if trace:
+        idx_t = torch.full((trace,), -1, dtype=torch.int64, device=At.device)
+        res_t = torch.full((trace,), float("nan"), dtype=torch.float64, device=At.device)
+        if trace_x:
+            x_t = torch.full((trace, n), float("nan"), dtype=torch.float64, device=At.device)
+        opts.trace_cap = trace
+        opts.idx_trace = idx_t.data_ptr()
+        opts.res_trace = res_t.data_ptr()
+        opts.x_trace = None if x_t is None else x_t.data_ptr()
+    rep = Report()
+    ctx.check(lib.csk_solve_ex(ctx.handle, _ptr(At), _ptr(bt.contiguous()), _ptr(nsq.contiguous()),
+                               d, n, _ptr(x), _ptr(xs), float(tol), int(max_iters),
+                               ctypes.byref(opts), ctypes.byref(rep), _stream()))
+    k = rep.iterations
+    return SolveResult(x=x, iterations=k, final_res=rep.final_res, termination=rep.termination,
+                       stop_mode=rep.stop_mode, last_index=rep.last_index,
+                       idx_trace=None if idx_t is None else idx_t[:min(k, trace)],
+                       res_trace=None if res_t is None else res_t[:min(k + 1, trace)],
+                       x_trace=None if x_t is None else x_t[:min(k + 1, trace)])
+
+
+def csk_solve_async(At, bt, nsq, x, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
+                    num_ctas: int = 0, smem_rows: int = 0, ctx: Context | None = None):
+    """Launch the loop without waiting (CSK_SOLVE_ASYNC); x (in/out) is updated in place.
+    Call ``csk_solve_wait(ctx)`` for the report."""
+    ctx = ctx or default_context()
+    d, n = At.shape
+    opts = SolveOpts()
+    opts.num_ctas = num_ctas
+    opts.smem_rows = smem_rows
+    opts.flags = SOLVE_ASYNC
+    ctx.check(lib.csk_solve_ex(ctx.handle, _ptr(At), _ptr(bt), _ptr(nsq), d, n, _ptr(x), _ptr(x_star),
+                               float(tol), int(max_iters), ctypes.byref(opts), None, _stream()))
+
+
+def csk_solve_wait(ctx: Context | None = None) -> Report:
+    ctx = ctx or default_context()
+    rep = Report()
+    ctx.check(lib.csk_solve_wait(ctx.handle, ctypes.byref(rep)))
+    return rep
+
+
+def csk_run(A, b, d: int, seed: int = 0, x0=None, x_star=None, tol: float = 1e-6,
+            max_iters: int = 50_000, ctx: Context | None = None):
+    """Whole Algorithm 1 on device buffers: plan + sketch + norms + loop."""
+    ctx = ctx or default_context()
+    _need(A, torch.float64, "A", 2)
+    _need(b, torch.float64, "b", 1)
+    m, n = A.shape
+    x = torch.zeros(n, dtype=torch.float64, device=A.device) if x0 is None else x0.clone().contiguous()
+    rep = Report()
+    ctx.check(lib.csk_run(ctx.handle, _ptr(A), A.stride(0), _ptr(b.contiguous()), m, n, d,
+                          seed & (2**64 - 1), _ptr(x), _ptr(x_star), float(tol), int(max_iters),
+                          ctypes.byref(rep), _stream()))
+    return x, rep
+
+
+def csk_run_host(A, b, d: int, seed: int = 0, x0=None, x_star=None, tol: float = 1e-6,
+                 max_iters: int = 50_000, ctx: Context | None = None):
+    """Whole Algorithm 1 from HOST (CPU, ideally pinned) tensors; copies in and out."""
+    ctx = ctx or default_context()
+    for t, nm in ((A, "A"), (b, "b")):
+        if t.is_cuda or t.dtype != torch.float64:
+            raise TypeError(f"{nm} must be a host fp64 tensor")
+    m, n = A.shape
+    x = torch.zeros(n, dtype=torch.float64) if x0 is None else x0.clone().contiguous()
+    rep = Report()
+    ctx.check(lib.csk_run_host(ctx.handle, _ptr(A), A.stride(0), _ptr(b.contiguous()), m, n, d,
+                               seed & (2**64 - 1), _ptr(x), _ptr(x_star), float(tol), int(max_iters),
+                               ctypes.byref(rep), _stream()))
+    return x, rep

@@ -1,0 +1,178 @@
+// csk_internal.cuh -- shared internals of libcsk (context, error plumbing, PTX helpers).
+// Product code only: nothing here is shared with oracle/ (the CPU oracle is independent).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/csk.h"
+
+namespace csk {
+
+// ---------------------------------------------------------------- context
+struct Workspace {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+struct Comm;  // sharded path (comm.cu)
+
+}  // namespace csk
+
+struct csk_ctx_s {
+    int device = 0;
+    int num_sms = 148;
+    int max_smem_optin = 227 * 1024;
+    std::string last_error;
+    // plan workspaces
+    csk::Workspace keys_in, keys_out, vals_in, vals_out, cub_tmp, offsets, flag;
+    // csk_run workspaces
+    csk::Workspace a_tilde, b_tilde, nsq, x_dev, xs_dev, a_dev, b_dev;
+    // solve workspaces
+    csk::Workspace slots, report, scalars;
+    csk::Comm *comm = nullptr;
+    // in-flight solve (CSK_SOLVE_ASYNC)
+    int64_t *report_host = nullptr;  // pinned
+    cudaStream_t pending_stream = nullptr;
+    bool pending = false;
+    bool pending_resmode = false;
+};
+
+namespace csk {
+
+csk_status_t fail(csk_ctx_t ctx, csk_status_t st, const std::string &msg);
+csk_status_t cuda_fail(csk_ctx_t ctx, cudaError_t e, const char *what);
+// Grow-only device workspace.
+csk_status_t ensure(csk_ctx_t ctx, Workspace &w, size_t bytes);
+
+#define CSK_CUDA(ctx, call)                                   \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return csk::cuda_fail((ctx), _e, #call); \
+    } while (0)
+
+#define CSK_CHECK(call)                        \
+    do {                                       \
+        csk_status_t _s = (call);              \
+        if (_s != CSK_OK) return _s;           \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------- plan
+// Internal plan build used by every sketch entry point.  perm/offsets may point
+// into the ctx workspace.  See plan.cu.
+csk_status_t build_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_t m, int64_t d,
+                        const int32_t *h_in, const int8_t *sign_in, int32_t **perm_out,
+                        int32_t **offsets_out, cudaStream_t stream);
+
+// ---------------------------------------------------------------- sketch (sketch.cu)
+csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
+                                 int64_t m, int64_t n, int64_t d, const int32_t *perm,
+                                 const int32_t *offsets, double *At, double *bt, double *nsq,
+                                 cudaStream_t stream);
+csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col,
+                               const double *val, const double *b, int64_t m, int64_t n,
+                               int64_t d, const int32_t *perm, const int32_t *offsets,
+                               double *At, double *bt, double *nsq, cudaStream_t stream);
+csk_status_t launch_row_norms(csk_ctx_t ctx, const double *At, int64_t d, int64_t n,
+                              double *nsq, cudaStream_t stream);
+// Team size used by the row-norm arithmetic (shared by fused and standalone paths).
+int norm_team_threads(int64_t n);
+
+// ---------------------------------------------------------------- solve (solve.cu)
+csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq,
+                       int64_t d, int64_t n, double *x, const double *x_star, double tol,
+                       int64_t max_iters, const csk_solve_opts_t *opts, csk_report_t *report,
+                       cudaStream_t stream);
+csk_status_t ensure_host_report(csk_ctx_t ctx);
+csk_status_t finish_solve(csk_ctx_t ctx, csk_report_t *report);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+// Counter form of SplitMix64: output number c (0-based) of the stream seeded with `seed`.
+__device__ __forceinline__ uint64_t sm64(uint64_t seed, uint64_t c) {
+    return splitmix64_mix(seed + (c + 1ULL) * 0x9E3779B97F4A7C15ULL);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Streaming read-only 16-byte load that does not allocate in L1.
+__device__ __forceinline__ double2 ldg_stream2(const double *p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldg_stream1(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// Relaxed gpu-scope 16-byte accesses used by the cross-CTA candidate exchange.
+__device__ __forceinline__ void st_relaxed_v2u64(uint64_t *p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v2u64(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(a), "=l"(b)
+                 : "l"(p)
+                 : "memory");
+}
+
+}  // namespace csk

@@ -1,0 +1,429 @@
+// sketch.cu -- S3 count-sketch application A~ = S A, b~ = S b and S4 row norms.
+//
+// Algorithm 1 "Initialize": A~ = S A, b~ = S b with S = Phi D (Def. 1,
+// P:50).  Row j of A~ is the signed sum of the rows of A hashed to bucket j, added in
+// ascending row order from +0.0, i.e. exactly the fp64 adds of the dense
+// product Phi D A -- so every A~ / b~ entry is bit-identical to the CPU oracle.
+//
+// Dense kernel (B200 design):
+//   * persistent grid, one CTA per SM; CTA c owns the buckets whose first row falls in
+//     rows [c m/G, (c+1) m/G) of the bucket-sorted order, so the work per CTA is a
+//     contiguous range of `perm` (balanced by rows, not by buckets);
+//   * a producer warp streams the gathered rows of A into a shared-memory ring with
+//     1-D TMA bulk copies (cp.async.bulk, completion on an mbarrier per slot);
+//     each row of A is read from HBM exactly once, as one contiguous 8n-byte burst;
+//   * consumer warps own column pairs (16-byte lanes) and fold the ring rows into
+//     fp64 register accumulators in ring (= row) order; at a bucket boundary they
+//     store the row of A~ (coalesced) and reduce its squared norm (S4, fused);
+//   * a b-warp folds b~ for the same buckets, one bucket per lane, row order.
+// CSR kernel (config C5): warp per bucket, dense shared-memory accumulator row.
+#include "csk_internal.cuh"
+
+namespace csk {
+
+namespace {
+
+constexpr int kPmax = 4;               // column pairs per consumer thread (template max)
+constexpr int kMaxConsumers = 256;     // consumer threads per CTA
+constexpr int kMaxSlots = 64;          // ring depth cap
+constexpr int kRingBudget = 192 * 1024;
+
+struct DenseGeom {
+    int tc;          // consumer threads (multiple of 32)
+    int p;           // pairs per consumer thread (1, 2 or 4)
+    int chunk_cols;  // columns per chunk (even), = 2 * tc * p
+    int chunks;      // ceil(n / chunk_cols)
+    int slot_bytes;  // ring slot stride (multiple of 128)
+    int slots;       // ring depth
+    size_t smem;     // dynamic shared memory
+};
+
+DenseGeom dense_geom(int64_t n) {
+    DenseGeom g{};
+    const int64_t pairs = (n + 1) / 2;
+    int64_t tc = ((pairs + 31) / 32) * 32;
+    if (tc > kMaxConsumers) tc = kMaxConsumers;
+    int64_t p = (pairs + tc - 1) / tc;
+    if (p > kPmax) p = kPmax;
+    if (p == 3) p = 4;
+    g.tc = static_cast<int>(tc);
+    g.p = static_cast<int>(p);
+    g.chunk_cols = 2 * g.tc * g.p;
+    g.chunks = static_cast<int>((n + g.chunk_cols - 1) / g.chunk_cols);
+    const int64_t cols0 = n < g.chunk_cols ? n : g.chunk_cols;
+    g.slot_bytes = static_cast<int>(((cols0 * 8 + 127) / 128) * 128);
+    int slots = kRingBudget / g.slot_bytes;
+    if (slots > kMaxSlots) slots = kMaxSlots;
+    if (slots < 2) slots = 2;
+    g.slots = slots;
+    // header: full[slots], empty[slots] (8 B each), sign/row[slots] (4 B each), red[2][8] doubles
+    size_t header = static_cast<size_t>(slots) * 16 + static_cast<size_t>(slots) * 8 + 2 * 8 * 8;
+    header = (header + 127) / 128 * 128;
+    g.smem = header + static_cast<size_t>(slots) * g.slot_bytes;
+    return g;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t len, int64_t v) {
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (static_cast<int64_t>(a[mid]) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Bucket range [j0, j1) of CTA `c` out of G: buckets whose first row lies in
+// [c m / G, (c+1) m / G) of the sorted order.
+__device__ __forceinline__ void cta_buckets(const int32_t *offsets, int64_t m, int64_t d, int c,
+                                            int G, int64_t &j0, int64_t &j1) {
+    const int64_t r0 = m * c / G;
+    const int64_t r1 = m * (c + 1) / G;
+    j0 = lower_bound_i32(offsets, d, r0);
+    j1 = (c == G - 1) ? d : lower_bound_i32(offsets, d, r1);
+}
+
+// Warp-level butterfly sum: every lane ends with the same bits (IEEE + is commutative).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kMaxConsumers + 64, 1)
+k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m,
+               int64_t n, int64_t d, const int32_t *__restrict__ perm,
+               const int32_t *__restrict__ offsets, double *__restrict__ At,
+               double *__restrict__ bt, double *__restrict__ nsq, int tc, int chunk_cols,
+               int chunks, int slot_bytes, int slots) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + slots;
+    int32_t *slot_row = reinterpret_cast<int32_t *>(empty + slots);  // row | sign bit
+    double *red = reinterpret_cast<double *>(slot_row + slots + (slots & 1));  // [2][8]
+    size_t header = static_cast<size_t>(slots) * 16 + static_cast<size_t>(slots) * 8 + 2 * 8 * 8;
+    header = (header + 127) / 128 * 128;
+    unsigned char *ring = smem + header;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int wc = tc >> 5;  // consumer warps
+
+    __shared__ int64_t s_j0, s_j1;
+    if (tid == 0) {
+        int64_t j0, j1;
+        cta_buckets(offsets, m, d, blockIdx.x, gridDim.x, j0, j1);
+        s_j0 = j0;
+        s_j1 = j1;
+        for (int s = 0; s < slots; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], wc);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t j0 = s_j0, j1 = s_j1;
+    if (j0 >= j1) return;
+    const int64_t t0 = offsets[j0];
+    const int64_t t1 = offsets[j1];
+
+    if (warp == wc) {
+        // ------------------------------------------------ producer warp (TMA)
+        int64_t u = 0;
+        for (int c = 0; c < chunks; ++c) {
+            const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
+            const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
+            const uint32_t bytes = static_cast<uint32_t>(((c1 - c0) & ~int64_t(1)) * 8);
+            for (int64_t tb = t0; tb < t1; tb += 32) {
+                const int64_t tl = tb + lane;
+                const int32_t mine = tl < t1 ? __ldg(perm + tl) : 0;
+                const int cnt = static_cast<int>((t1 - tb) < 32 ? (t1 - tb) : 32);
+                for (int k = 0; k < cnt; ++k, ++u) {
+                    const int32_t pr = __shfl_sync(0xffffffffu, mine, k);
+                    if (lane == 0) {
+                        const int s = static_cast<int>(u % slots);
+                        const int64_t use = u / slots;
+                        if (use > 0) mbar_wait(&empty[s], static_cast<uint32_t>((use - 1) & 1));
+                        slot_row[s] = pr;
+                        mbar_arrive_expect_tx(&full[s], bytes);
+                        if (bytes) {
+                            const int64_t row = pr & 0x7fffffff;
+                            bulk_g2s(ring + static_cast<size_t>(s) * slot_bytes,
+                                     A + row * lda + c0, bytes, &full[s]);
+                        }
+                    }
+                }
+            }
+        }
+        return;
+    }
+    if (warp == wc + 1) {
+        // ------------------------------------------------ b~ warp: one bucket per lane
+        for (int64_t j = j0 + lane; j < j1; j += 32) {
+            const int64_t a = offsets[j], e = offsets[j + 1];
+            double acc = 0.0;
+            int64_t t = a;
+            for (; t + 4 <= e; t += 4) {
+                int32_t p4[4];
+                double v4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) p4[q] = __ldg(perm + t + q);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v4[q] = __ldg(b + (p4[q] & 0x7fffffff));
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc = acc + (p4[q] < 0 ? -v4[q] : v4[q]);
+            }
+            for (; t < e; ++t) {
+                const int32_t pr = __ldg(perm + t);
+                const double v = __ldg(b + (pr & 0x7fffffff));
+                acc = acc + (pr < 0 ? -v : v);
+            }
+            bt[j] = acc;
+        }
+        return;
+    }
+
+    // ---------------------------------------------------- consumer warps
+    int64_t u = 0;
+    int red_parity = 0;
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
+        const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
+        const int64_t ce = c0 + ((c1 - c0) & ~int64_t(1));  // end of the TMA-copied columns
+        for (int64_t j = j0; j < j1; ++j) {
+            double2 acc[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) acc[p] = make_double2(0.0, 0.0);
+            const int64_t e = offsets[j + 1];
+            for (int64_t t = offsets[j]; t < e; ++t, ++u) {
+                const int s = static_cast<int>(u % slots);
+                mbar_wait(&full[s], static_cast<uint32_t>((u / slots) & 1));
+                const int32_t pr = slot_row[s];
+                const bool neg = pr < 0;
+                const double2 *srow =
+                    reinterpret_cast<const double2 *>(ring + static_cast<size_t>(s) * slot_bytes);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int q = tid + tc * p;
+                    const int64_t col = c0 + 2 * static_cast<int64_t>(q);
+                    if (col + 1 < ce) {
+                        double2 v = srow[q];
+                        if (neg) { v.x = -v.x; v.y = -v.y; }
+                        acc[p].x = acc[p].x + v.x;
+                        acc[p].y = acc[p].y + v.y;
+                    } else if (col < c1) {  // odd-n tail column, not in the bulk copy
+                        double v = A[static_cast<int64_t>(pr & 0x7fffffff) * lda + col];
+                        if (neg) v = -v;
+                        acc[p].x = acc[p].x + v;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            // epilogue: store the row of A~, fused squared norm (S4)
+            double part = 0.0;
+            double *dst = At + j * n;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int q = tid + tc * p;
+                const int64_t col = c0 + 2 * static_cast<int64_t>(q);
+                if (col + 1 < c1) {
+                    if ((n & 1) == 0) {
+                        *reinterpret_cast<double2 *>(dst + col) = acc[p];
+                    } else {
+                        dst[col] = acc[p].x;
+                        dst[col + 1] = acc[p].y;
+                    }
+                    part = __fma_rn(acc[p].x, acc[p].x, part);
+                    part = __fma_rn(acc[p].y, acc[p].y, part);
+                } else if (col < c1) {
+                    dst[col] = acc[p].x;
+                    part = __fma_rn(acc[p].x, acc[p].x, part);
+                }
+            }
+            if (nsq != nullptr) {
+                part = warp_sum(part);
+                if (lane == 0) red[red_parity * 8 + warp] = part;
+                asm volatile("bar.sync 1, %0;" ::"r"(tc) : "memory");
+                if (tid == 0) {
+                    double tot = red[red_parity * 8];
+                    for (int w = 1; w < wc; ++w) tot = tot + red[red_parity * 8 + w];
+                    nsq[j] = (c == 0) ? tot : nsq[j] + tot;
+                }
+                red_parity ^= 1;
+            }
+        }
+    }
+}
+
+// Standalone S4: the same per-row arithmetic as the fused epilogue above
+// (thread t sums pairs t + tc*p, p ascending, then warp butterfly, then warps in
+// order, then chunks in order), one CTA of `tc` threads per row.
+template <int P>
+__global__ void __launch_bounds__(kMaxConsumers)
+k_row_norms(const double *__restrict__ At, int64_t d, int64_t n, double *__restrict__ nsq,
+            int chunk_cols, int chunks) {
+    __shared__ double red[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tc = blockDim.x;
+    for (int64_t j = blockIdx.x; j < d; j += gridDim.x) {
+        double total = 0.0;
+        for (int c = 0; c < chunks; ++c) {
+            const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
+            const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
+            double part = 0.0;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int64_t col = c0 + 2 * static_cast<int64_t>(tid + tc * p);
+                if (col + 1 < c1) {
+                    const double a0 = At[j * n + col], a1 = At[j * n + col + 1];
+                    part = __fma_rn(a0, a0, part);
+                    part = __fma_rn(a1, a1, part);
+                } else if (col < c1) {
+                    const double a0 = At[j * n + col];
+                    part = __fma_rn(a0, a0, part);
+                }
+            }
+            part = warp_sum(part);
+            if (lane == 0) red[warp] = part;
+            __syncthreads();
+            if (tid == 0) {
+                double tot = red[0];
+                for (int w = 1; w < (tc >> 5); ++w) tot = tot + red[w];
+                total = (c == 0) ? tot : total + tot;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) nsq[j] = total;
+    }
+}
+
+// CSR sketch: one warp per bucket; a dense fp64 accumulator row of n in shared
+// memory per warp; rows of the bucket in ascending order, each row's stored
+// (col, val) pairs spread over lanes (columns are distinct within a row, so
+// per-column adds keep row order).  Row norms fused as in the dense epilogue
+// but with the warp-only team (documented in DESIGN.md; checked to tolerance).
+__global__ void k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                             const double *__restrict__ val, const double *__restrict__ b,
+                             int64_t n, int64_t d, const int32_t *__restrict__ perm,
+                             const int32_t *__restrict__ offsets, double *__restrict__ At,
+                             double *__restrict__ bt, double *__restrict__ nsq, int64_t acc_stride) {
+    extern __shared__ __align__(16) double acc_all[];
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5;
+    double *acc = acc_all + static_cast<int64_t>(warp) * acc_stride;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * wpb + warp; j < d;
+         j += static_cast<int64_t>(gridDim.x) * wpb) {
+        for (int64_t k = lane; k < n; k += 32) acc[k] = 0.0;
+        __syncwarp();
+        const int64_t a = offsets[j], e = offsets[j + 1];
+        double bacc = 0.0;
+        for (int64_t t = a; t < e; ++t) {
+            const int32_t pr = __ldg(perm + t);
+            const int64_t row = pr & 0x7fffffff;
+            const bool neg = pr < 0;
+            const int64_t s0 = __ldg(row_ptr + row), s1 = __ldg(row_ptr + row + 1);
+            for (int64_t q = s0 + lane; q < s1; q += 32) {
+                const int32_t cc = __ldg(col + q);
+                double v = __ldg(val + q);
+                if (neg) v = -v;
+                acc[cc] = acc[cc] + v;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const double bv = __ldg(b + row);
+                bacc = bacc + (neg ? -bv : bv);
+            }
+        }
+        double part = 0.0;
+        double *dst = At + j * n;
+        for (int64_t k = 2 * lane; k < n; k += 64) {
+            const double a0 = acc[k];
+            dst[k] = a0;
+            part = __fma_rn(a0, a0, part);
+            if (k + 1 < n) {
+                const double a1 = acc[k + 1];
+                dst[k + 1] = a1;
+                part = __fma_rn(a1, a1, part);
+            }
+        }
+        part = warp_sum(part);
+        if (lane == 0) {
+            bt[j] = bacc;
+            if (nsq) nsq[j] = part;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+int norm_team_threads(int64_t n) { return dense_geom(n).tc; }
+
+csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
+                                 int64_t m, int64_t n, int64_t d, const int32_t *perm,
+                                 const int32_t *offsets, double *At, double *bt, double *nsq,
+                                 cudaStream_t stream) {
+    const DenseGeom g = dense_geom(n);
+    int grid = ctx->num_sms;
+    if (grid > d) grid = static_cast<int>(d);
+    const int threads = g.tc + 64;
+    cudaError_t e = cudaSuccess;
+#define CSK_LAUNCH_DENSE(PP)                                                                    \
+    case PP: {                                                                                  \
+        e = cudaFuncSetAttribute(k_sketch_dense<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 static_cast<int>(g.smem));                                     \
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(k_sketch_dense)");  \
+        k_sketch_dense<PP><<<grid, threads, g.smem, stream>>>(A, lda, b, m, n, d, perm, offsets, \
+                                                              At, bt, nsq, g.tc, g.chunk_cols,  \
+                                                              g.chunks, g.slot_bytes, g.slots); \
+        break;                                                                                  \
+    }
+    switch (g.p) {
+        CSK_LAUNCH_DENSE(1)
+        CSK_LAUNCH_DENSE(2)
+        CSK_LAUNCH_DENSE(4)
+        default: return fail(ctx, CSK_E_UNSUPPORTED, "sketch geometry");
+    }
+#undef CSK_LAUNCH_DENSE
+    CSK_CUDA(ctx, cudaGetLastError());
+    return CSK_OK;
+}
+
+csk_status_t launch_row_norms(csk_ctx_t ctx, const double *At, int64_t d, int64_t n, double *nsq,
+                              cudaStream_t stream) {
+    const DenseGeom g = dense_geom(n);
+    int64_t grid = d < int64_t(ctx->num_sms) * 8 ? d : int64_t(ctx->num_sms) * 8;
+    switch (g.p) {
+        case 1: k_row_norms<1><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
+        case 2: k_row_norms<2><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
+        case 4: k_row_norms<4><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
+        default: return fail(ctx, CSK_E_UNSUPPORTED, "row-norm geometry");
+    }
+    CSK_CUDA(ctx, cudaGetLastError());
+    return CSK_OK;
+}
+
+csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col,
+                               const double *val, const double *b, int64_t m, int64_t n,
+                               int64_t d, const int32_t *perm, const int32_t *offsets,
+                               double *At, double *bt, double *nsq, cudaStream_t stream) {
+    (void)m;
+    const int64_t stride = (n + 1) & ~int64_t(1);
+    int wpb = static_cast<int>((ctx->max_smem_optin - 1024) / (stride * 8));
+    if (wpb > 16) wpb = 16;
+    if (wpb < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
+    const size_t smem = static_cast<size_t>(wpb) * stride * 8;
+    CSK_CUDA(ctx, cudaFuncSetAttribute(k_sketch_csr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    int64_t grid = (d + wpb - 1) / wpb;
+    const int64_t cap = int64_t(ctx->num_sms) * 4;
+    if (grid > cap) grid = cap;
+    k_sketch_csr<<<static_cast<int>(grid), wpb * 32, smem, stream>>>(
+        row_ptr, col, val, b, n, d, perm, offsets, At, bt, nsq, stride);
+    CSK_CUDA(ctx, cudaGetLastError());
+    return CSK_OK;
+}
+
+}  // namespace csk

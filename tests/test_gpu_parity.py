@@ -1,0 +1,284 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE north_star):
+  * h, D, perm, offsets, A~, b~: bit-exact at P = 1 (the sketch is a fixed-order
+    fold of exactly representable +-A values);
+  * nsq: fixed but different summation order -> |d nsq| <= 2 n u nsq (gamma_n bound
+    for a sum of n non-negative terms, u = 2^-53);
+  * loop: lockstep -- given the GPU's x_k the oracle's residual picks the same i_k
+    (or a near-tie within 4e-10 relative), the oracle's step from (x_k, i_k) lands on
+    the GPU's x_{k+1} within 1e-12 relative; free-running -- RES <= tol for both and
+    |IT_gpu - IT_orc| <= max(1, 5 % IT_orc).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from csk_synth import CONFIGS, make_config, make_dense
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0**-53
+
+
+@pytest.fixture(scope="module")
+def csk():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2004_02480_b200 as m
+    return m
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _check_sketch(csk, A, b, d, seed, **kw):
+    At, bt, nsq = csk.csk_sketch(A, b, d, seed=seed, **kw)
+    torch.cuda.synchronize()
+    An = _np(A)
+    At_o, bt_o = oracle.sketch_dense(An, _np(b), d, seed=seed)
+    assert np.array_equal(_np(At), At_o), "A~ not bit-exact"
+    assert np.array_equal(_np(bt), bt_o), "b~ not bit-exact"
+    nsq_o = oracle.row_norms(At_o)
+    n = A.shape[1]
+    assert np.all(np.abs(_np(nsq) - nsq_o) <= 2 * n * U * nsq_o)
+    nsq2 = csk.csk_row_norms(At)
+    assert torch.equal(nsq, nsq2), "fused and standalone row norms differ"
+    return At, bt, nsq
+
+
+# ---------------------------------------------------------------- S1/S2
+@pytest.mark.parametrize("seed,m,d,off", [(0, 1000, 500, 0), (0, 20000, 2000, 0),
+                                          (2**63 + 5, 123457, 40000, 0), (7, 5000, 3, 1234)])
+def test_hash_bitexact(csk, seed, m, d, off):
+    h, s = csk.csk_hash(m, d, seed=seed, row_offset=off)
+    ho, so = oracle.hash_map(seed, m + off, d)
+    assert np.array_equal(_np(h), ho[off:])
+    assert np.array_equal(_np(s), so[off:])
+
+
+@pytest.mark.parametrize("m,d", [(1000, 500), (100000, 5000), (77777, 1), (4096, 4095)])
+def test_plan_bitexact(csk, m, d):
+    perm, offs = csk.csk_plan(m, d, seed=11)
+    h, s = oracle.hash_map(11, m, d)
+    order = np.argsort(h, kind="stable")
+    want = order.astype(np.int64) | np.where(s[order] < 0, 1 << 31, 0)
+    got = _np(perm).astype(np.int64) & 0xFFFFFFFF
+    assert np.array_equal(got, want)
+    assert np.array_equal(_np(offs), np.searchsorted(h[order], np.arange(d + 1), side="left"))
+
+
+# ---------------------------------------------------------------- S3/S4
+@pytest.mark.parametrize("m,n,d", [(1000, 50, 500), (20000, 200, 2000), (3001, 17, 700),
+                                   (999, 1, 10), (4000, 2500, 300), (5000, 64, 4999),
+                                   (2000, 333, 1), (6000, 1000, 100)])
+def test_sketch_bitexact_shapes(csk, m, n, d):
+    p = make_dense(m, n, "lognormal_rows", 77, "cuda")
+    _check_sketch(csk, p.A, p.b, d, seed=3)
+
+
+def test_sketch_padded_lda(csk):
+    p = make_dense(3000, 130, "gauss", 5, "cuda")
+    Ab = torch.zeros(3000, 136, dtype=torch.float64, device="cuda")
+    Ab[:, :130] = p.A
+    At, bt, _ = csk.csk_sketch(Ab[:, :130], p.b, 400, seed=9)
+    At_o, bt_o = oracle.sketch_dense(_np(p.A), _np(p.b), 400, seed=9)
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+
+
+def test_sketch_identity_map_signed_rows(csk):
+    """Remark 1: h = identity, d = m -> A~ = D A exactly."""
+    p = make_dense(500, 40, "gauss", 8, "cuda")
+    h = torch.arange(500, dtype=torch.int32, device="cuda")
+    s = (torch.randint(0, 2, (500,), device="cuda", dtype=torch.int8) * 2 - 1).to(torch.int8)
+    At, bt, _ = csk.csk_sketch_with_map(p.A, p.b, 500, h, s)
+    sd = s.to(torch.float64)
+    assert torch.equal(At, p.A * sd[:, None]) and torch.equal(bt, p.b * sd)
+
+
+def test_sketch_argument_errors(csk):
+    p = make_dense(100, 8, "gauss", 1, "cuda")
+    with pytest.raises(csk.CskError) as e:
+        csk.csk_sketch(p.A, p.b, 100)           # d == m violates d < m
+    assert e.value.status == csk.CSK_E_ARG
+    with pytest.raises(csk.CskError):
+        csk.csk_sketch(p.A, p.b, 0)
+    with pytest.raises(csk.CskError):           # odd leading dimension -> no vector path
+        Ab = torch.zeros(100, 9, dtype=torch.float64, device="cuda")
+        csk.csk_sketch(Ab[:, :8], p.b, 10)
+
+
+# ---------------------------------------------------------------- S5-S8 loop
+def _lockstep(At, bt, nsq, xtr, itr, k_max):
+    At, bt, nsq = _np(At), _np(bt), _np(nsq)
+    xtr, itr = _np(xtr), _np(itr)
+    for k in range(min(k_max, len(itr))):
+        r = oracle.residual(At, bt, xtr[k])
+        mask = nsq > 0
+        sc = np.where(mask, r * r / np.where(mask, nsq, 1), -1.0)
+        io = int(np.argmax(sc))
+        ig = int(itr[k])
+        assert ig == io or sc[ig] >= (1 - 4e-10) * sc[io], (k, ig, io)
+        lam = r[ig] / nsq[ig]
+        x1 = xtr[k] + lam * At[ig]
+        assert np.linalg.norm(x1 - xtr[k + 1]) <= 1e-12 * max(np.linalg.norm(x1), 1e-300) + 1e-14 * np.linalg.norm(lam * At[ig]), k
+
+
+def _free_running(res_g, res_o):
+    assert res_g.final_res <= 1e-6 and res_o.final_res <= 1e-6
+    assert abs(res_g.iterations - res_o.iterations) <= max(1, 0.05 * res_o.iterations)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_solve_parity_small_configs(csk, name):
+    cfg = CONFIGS[name]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = _check_sketch(csk, p.A, p.b, cfg.d, cfg.sketch_seed)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters,
+                      trace=4000, trace_x=True)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star),
+                     tol=cfg.tol, max_iters=cfg.max_iters, trace=4000)
+    assert g.termination == csk.CONVERGED
+    _free_running(g, o)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000)
+    n_same = min(len(g.idx_trace), len(o.idx_trace))
+    assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
+    assert abs(g.final_res - oracle.solve(_np(At), _np(bt), _np(nsq), x0=_np(g.x), x_star=_np(p.x_star), max_iters=0).final_res) <= 1e-12
+
+
+@pytest.mark.parametrize("num_ctas,smem_rows", [(1, 0), (7, 0), (148, -1), (37, 3), (2, -1)])
+def test_solve_launch_shapes_and_streamed_rows(csk, num_ctas, smem_rows):
+    """The L2/HBM-streamed GEMV path (smem_rows = -1: no resident rows) and odd grids."""
+    p = make_dense(8000, 300, "lognormal_rows", 91, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, 1500, seed=4)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, num_ctas=num_ctas, smem_rows=smem_rows,
+                      trace=300, trace_x=True)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), trace=300)
+    _free_running(g, o)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 300)
+
+
+@pytest.mark.parametrize("n", [1, 3, 63, 64, 65, 129, 1023, 2047, 2048])
+def test_solve_ragged_n(csk, n):
+    m = max(4 * n + 50, 400)
+    d = max(2 * n + 10, 50)
+    p = make_dense(m, n, "gauss", 1000 + n, "cuda")
+    At, bt, nsq = _check_sketch(csk, p.A, p.b, d, seed=n)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=20000, trace=50, trace_x=True)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), max_iters=20000)
+    _free_running(g, o)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 50)
+
+
+def test_solve_residual_mode(csk):
+    p = make_dense(6000, 40, "gauss", 12, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, 400, seed=2)
+    g = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-10)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=None, tol=1e-10)
+    assert g.stop_mode == csk.STOP_RESIDUAL and g.termination == csk.CONVERGED
+    assert abs(g.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
+    r = _np(bt) - _np(At) @ _np(g.x)
+    assert float(r @ r) / float(_np(bt) @ _np(bt)) <= 1e-10 * (1 + 1e-6)
+
+
+def test_solve_edge_cases(csk):
+    dev = "cuda"
+    # A = I4, b = (4,3,2,1): exactly 4 steps, indices 0..3
+    At = torch.eye(4, dtype=torch.float64, device=dev)
+    b = torch.tensor([4.0, 3.0, 2.0, 1.0], dtype=torch.float64, device=dev)
+    g = csk.csk_solve(At, b, torch.ones(4, dtype=torch.float64, device=dev), x_star=b,
+                      tol=1e-30, trace=10)
+    assert g.iterations == 4 and _np(g.idx_trace).tolist() == [0, 1, 2, 3]
+    assert torch.equal(g.x, b)
+    # x0 = x* -> 0 iterations
+    p = make_dense(300, 6, "gauss", 3, dev)
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, 40)
+    g = csk.csk_solve(At, bt, nsq, x0=p.x_star, x_star=p.x_star)
+    assert g.iterations == 0 and g.termination == csk.CONVERGED
+    # max_iters = 0 and the cap
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=0)
+    assert g.iterations == 0 and g.termination == csk.MAX_ITERS
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=3, tol=1e-30)
+    assert g.iterations == 3 and g.termination == csk.MAX_ITERS
+    # stagnation: consistent-looking zero residual, RES > tol
+    g = csk.csk_solve(torch.tensor([[1.0, 0.0]], dtype=torch.float64, device=dev),
+                      torch.zeros(1, dtype=torch.float64, device=dev),
+                      torch.ones(1, dtype=torch.float64, device=dev),
+                      x_star=torch.tensor([0.0, 1.0], dtype=torch.float64, device=dev))
+    assert g.termination == csk.STAGNATED and g.iterations == 0
+    # masked zero rows never selected
+    At = torch.tensor([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]], dtype=torch.float64, device=dev)
+    bt = torch.tensor([100.0, 1.0, 2.0], dtype=torch.float64, device=dev)
+    g = csk.csk_solve(At, bt, csk.csk_row_norms(At), x_star=torch.tensor([1.0, 2.0], dtype=torch.float64, device=dev),
+                      tol=1e-30, trace=10)
+    assert 0 not in _np(g.idx_trace).tolist()
+    # zero sketch -> CSK_E_ZERO_SKETCH
+    with pytest.raises(csk.CskError) as e:
+        z = torch.zeros(3, 2, dtype=torch.float64, device=dev)
+        csk.csk_solve(z, torch.ones(3, dtype=torch.float64, device=dev),
+                      torch.zeros(3, dtype=torch.float64, device=dev),
+                      x_star=torch.ones(2, dtype=torch.float64, device=dev))
+    assert e.value.status == csk.CSK_E_ZERO_SKETCH
+
+
+def test_identity_map_solve_is_mwrk(csk):
+    """CSK with d = m, h = id equals MWRK on (A, b) (Remark 1): same i_k sequence."""
+    p = make_dense(400, 12, "gauss", 4, "cuda")
+    h = torch.arange(400, dtype=torch.int32, device="cuda")
+    s = torch.ones(400, dtype=torch.int8, device="cuda")
+    s[::3] = -1
+    At, bt, nsq = csk.csk_sketch_with_map(p.A, p.b, 400, h, s)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=1e-12, trace=2000)
+    o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), tol=1e-12, trace=2000)
+    n_same = min(len(g.idx_trace), len(o.idx_trace)) - 2
+    assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
+
+
+def test_run_and_run_host(csk):
+    cfg = CONFIGS["C2"]
+    p = make_config(cfg, "cuda")
+    x, rep = csk.csk_run(p.A, p.b, cfg.d, x_star=p.x_star)
+    assert rep.termination == csk.CONVERGED and rep.final_res <= 1e-6
+    xh, reph = csk.csk_run_host(p.A.cpu().pin_memory(), p.b.cpu(), cfg.d, x_star=p.x_star.cpu())
+    assert reph.iterations == rep.iterations and torch.equal(xh, x.cpu())
+
+
+# ---------------------------------------------------------------- full-size configs
+def test_C3_full_parity(csk):
+    cfg = CONFIGS["C3"]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = _check_sketch(csk, p.A, p.b, cfg.d, cfg.sketch_seed)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cfg.max_iters, trace=200, trace_x=True)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star),
+                     max_iters=cfg.max_iters)
+    _free_running(g, o)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 40)
+
+
+def test_C4_full_size_sampled(csk):
+    """8 GB A: sampled buckets against the oracle's fold of exactly those rows, lockstep on the
+    first iterations, and properties over the whole 50k-iteration run (monotone RES, eq:A)."""
+    cfg = CONFIGS["C4"]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
+    torch.cuda.synchronize()
+    h, s = oracle.hash_map(cfg.sketch_seed, cfg.m, cfg.d)
+    rng = np.random.default_rng(0)
+    for j in rng.choice(cfg.d, 24, replace=False).tolist() + [0, cfg.d - 1]:
+        rows = np.nonzero(h == j)[0]
+        sub = _np(p.A[torch.as_tensor(rows, device="cuda")]) if len(rows) else np.zeros((0, cfg.n))
+        bsub = _np(p.b[torch.as_tensor(rows, device="cuda")]) if len(rows) else np.zeros(0)
+        if len(rows):
+            a1, b1 = oracle.sketch_dense(sub, bsub, 1, h=np.zeros(len(rows), np.int32), s=s[rows])
+        else:
+            a1, b1 = np.zeros((1, cfg.n)), np.zeros(1)
+        assert np.array_equal(_np(At[j]), a1[0]) and _np(bt[j]) == b1[0]
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cfg.max_iters, trace=cfg.max_iters + 1)
+    assert g.termination in (csk.CONVERGED, csk.MAX_ITERS)
+    res = _np(g.res_trace)
+    assert np.all(np.diff(res) <= 1e-12 * res[:-1])
+    g20 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=12, tol=1e-30, trace=13, trace_x=True)
+    _lockstep(At, bt, nsq, g20.x_trace, g20.idx_trace, 12)
+    assert np.array_equal(_np(g20.idx_trace), _np(g.idx_trace)[:12])
