@@ -23,8 +23,9 @@
  *     csk_last_error(ctx) returns a human-readable reason for the last failure
  *     on that context.  There is no CPU fallback: a call that cannot run on the
  *     GPU fails.
- *   - Alignment: A and A~ must be 16-byte aligned and `lda` even (128-bit
- *     vector and TMA bulk-copy path); violations return CSK_E_ARG.
+ *   - Alignment: A~ must be 16-byte aligned, A 8-byte aligned.  The sketch
+ *     streams rows of A with TMA bulk copies when A is 16-byte aligned and lda is
+ *     even (the fast path); otherwise the same kernel reads rows with plain loads.
  *   - Sizes: 1 <= d < m (Algorithm 1, "with d < m"), m < 2^31, n >= 1,
  *     n <= CSK_MAX_N for csk_solve*.
  */
@@ -130,7 +131,7 @@ CSK_API csk_status_t csk_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, 
  *   fp64 adds in the same order as the dense product Phi D A, so A~ and b~ are
  *   bit-reproducible and equal to the oracle bit for bit.  If nsq != NULL the
  *   row norms (S4) are fused into the epilogue (same arithmetic as csk_row_norms).
- *   A: m x n, leading dimension lda >= n (even), 16-byte aligned.  1 <= d < m. */
+ *   A: m x n, leading dimension lda >= n.  1 <= d < m. */
 CSK_API csk_status_t csk_sketch(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
                         int64_t m, int64_t n, int64_t d, uint64_t seed,
                         double *A_tilde, double *b_tilde, double *nsq, void *stream);

@@ -58,8 +58,8 @@ static csk_status_t check_dense(csk_ctx_t ctx, const char *fn, const double *A, 
                  fn, allow_d_eq_m ? "<=" : "<", (long long)m, (long long)n, (long long)d);
         return fail(ctx, CSK_E_ARG, buf);
     }
-    if (lda < n || (lda & 1) || !aligned16(A) || !aligned16(At)) {
-        snprintf(buf, sizeof buf, "%s: need lda >= n, lda even, A and A~ 16-byte aligned", fn);
+    if (lda < n || (reinterpret_cast<uintptr_t>(A) & 7) || !aligned16(At)) {
+        snprintf(buf, sizeof buf, "%s: need lda >= n, A 8-byte and A~ 16-byte aligned", fn);
         return fail(ctx, CSK_E_ARG, buf);
     }
     return CSK_OK;

@@ -89,7 +89,10 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int P>
+// TMA = true: rows staged by 1-D bulk copies (A 16-byte aligned, lda even).
+// TMA = false: any alignment; the producer only publishes the row order and the
+// consumers read their columns straight from global memory (same adds, same order).
+template <int P, bool TMA>
 __global__ void __launch_bounds__(kMaxConsumers + 64, 1)
 k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m,
                int64_t n, int64_t d, const int32_t *__restrict__ perm,
@@ -134,7 +137,7 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
         for (int c = 0; c < chunks; ++c) {
             const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
             const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
-            const uint32_t bytes = static_cast<uint32_t>(((c1 - c0) & ~int64_t(1)) * 8);
+            const uint32_t bytes = TMA ? static_cast<uint32_t>(((c1 - c0) & ~int64_t(1)) * 8) : 0u;
             for (int64_t tb = t0; tb < t1; tb += 32) {
                 const int64_t tl = tb + lane;
                 const int32_t mine = tl < t1 ? __ldg(perm + tl) : 0;
@@ -190,7 +193,7 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
     for (int c = 0; c < chunks; ++c) {
         const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
         const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
-        const int64_t ce = c0 + ((c1 - c0) & ~int64_t(1));  // end of the TMA-copied columns
+        const int64_t ce = TMA ? c0 + ((c1 - c0) & ~int64_t(1)) : c0;  // end of the TMA-copied columns
         for (int64_t j = j0; j < j1; ++j) {
             double2 acc[P];
 #pragma unroll
@@ -212,10 +215,16 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
                         if (neg) { v.x = -v.x; v.y = -v.y; }
                         acc[p].x = acc[p].x + v.x;
                         acc[p].y = acc[p].y + v.y;
-                    } else if (col < c1) {  // odd-n tail column, not in the bulk copy
-                        double v = A[static_cast<int64_t>(pr & 0x7fffffff) * lda + col];
+                    } else if (col < c1) {  // columns not in the bulk copy: read directly
+                        const double *src = A + static_cast<int64_t>(pr & 0x7fffffff) * lda + col;
+                        double v = src[0];
                         if (neg) v = -v;
                         acc[p].x = acc[p].x + v;
+                        if (col + 1 < c1) {
+                            double w = src[1];
+                            if (neg) w = -w;
+                            acc[p].y = acc[p].y + w;
+                        }
                     }
                 }
                 __syncwarp();
@@ -365,25 +374,34 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
                                  int64_t m, int64_t n, int64_t d, const int32_t *perm,
                                  const int32_t *offsets, double *At, double *bt, double *nsq,
                                  cudaStream_t stream) {
-    const DenseGeom g = dense_geom(n);
+    DenseGeom g = dense_geom(n);
     int grid = ctx->num_sms;
     if (grid > d) grid = static_cast<int>(d);
     const int threads = g.tc + 64;
-    cudaError_t e = cudaSuccess;
-#define CSK_LAUNCH_DENSE(PP)                                                                    \
-    case PP: {                                                                                  \
-        e = cudaFuncSetAttribute(k_sketch_dense<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 static_cast<int>(g.smem));                                     \
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(k_sketch_dense)");  \
-        k_sketch_dense<PP><<<grid, threads, g.smem, stream>>>(A, lda, b, m, n, d, perm, offsets, \
-                                                              At, bt, nsq, g.tc, g.chunk_cols,  \
-                                                              g.chunks, g.slot_bytes, g.slots); \
-        break;                                                                                  \
+    const bool tma = aligned16(A) && (lda % 2 == 0);
+    if (!tma) {  // no ring payload: only the slot metadata
+        g.slots = kMaxSlots;
+        g.slot_bytes = 0;
+        size_t header = static_cast<size_t>(g.slots) * 16 + static_cast<size_t>(g.slots) * 8 + 2 * 8 * 8;
+        g.smem = (header + 127) / 128 * 128;
     }
-    switch (g.p) {
-        CSK_LAUNCH_DENSE(1)
-        CSK_LAUNCH_DENSE(2)
-        CSK_LAUNCH_DENSE(4)
+    cudaError_t e = cudaSuccess;
+#define CSK_LAUNCH_DENSE(PP, T)                                                                      \
+    {                                                                                                \
+        e = cudaFuncSetAttribute(k_sketch_dense<PP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 static_cast<int>(g.smem));                                          \
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(k_sketch_dense)");       \
+        k_sketch_dense<PP, T><<<grid, threads, g.smem, stream>>>(A, lda, b, m, n, d, perm, offsets,  \
+                                                                 At, bt, nsq, g.tc, g.chunk_cols,    \
+                                                                 g.chunks, g.slot_bytes, g.slots);   \
+    }
+    switch (g.p * 2 + (tma ? 1 : 0)) {
+        case 3: CSK_LAUNCH_DENSE(1, true) break;
+        case 2: CSK_LAUNCH_DENSE(1, false) break;
+        case 5: CSK_LAUNCH_DENSE(2, true) break;
+        case 4: CSK_LAUNCH_DENSE(2, false) break;
+        case 9: CSK_LAUNCH_DENSE(4, true) break;
+        case 8: CSK_LAUNCH_DENSE(4, false) break;
         default: return fail(ctx, CSK_E_UNSUPPORTED, "sketch geometry");
     }
 #undef CSK_LAUNCH_DENSE
