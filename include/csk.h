@@ -89,6 +89,7 @@ typedef struct {
     int64_t *idx_trace;    /* device int64[trace_cap]: i_k, or NULL */
     double *res_trace;     /* device double[trace_cap]: stop quantity at x_k, or NULL */
     double *x_trace;       /* device double[trace_cap * n]: x_k row by row, or NULL */
+    int64_t *phase_cycles; /* debug: device int64[16] per-phase SM-cycle totals of CTA 0, or NULL */
 } csk_solve_opts_t;
 
 typedef struct csk_ctx_s *csk_ctx_t;

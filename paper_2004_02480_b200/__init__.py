@@ -51,7 +51,8 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("num_ctas", ctypes.c_int32), ("smem_rows", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("trace_cap", ctypes.c_int64), ("idx_trace", ctypes.c_void_p),
-                ("res_trace", ctypes.c_void_p), ("x_trace", ctypes.c_void_p)]
+                ("res_trace", ctypes.c_void_p), ("x_trace", ctypes.c_void_p),
+                ("phase_cycles", ctypes.c_void_p)]
 
 
 def _load():
@@ -273,7 +274,7 @@ class SolveResult:
 
 def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
               num_ctas: int = 0, smem_rows: int = 0, trace: int = 0, trace_x: bool = False,
-              ctx: Context | None = None) -> SolveResult:
+              phase_cycles: torch.Tensor | None = None, ctx: Context | None = None) -> SolveResult:
     """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel."""
     ctx = ctx or default_context()
     _need(At, torch.float64, "A_tilde", 2)
@@ -296,6 +297,8 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
         opts.idx_trace = idx_t.data_ptr()
         opts.res_trace = res_t.data_ptr()
         opts.x_trace = None if x_t is None else x_t.data_ptr()
+    if phase_cycles is not None:
+        opts.phase_cycles = phase_cycles.data_ptr()
     rep = Report()
     ctx.check(lib.csk_solve_ex(ctx.handle, _ptr(At), _ptr(bt.contiguous()), _ptr(nsq.contiguous()),
                                d, n, _ptr(x), _ptr(xs), float(tol), int(max_iters),

@@ -149,17 +149,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
         : "memory");
 }
 
-// Streaming read-only 16-byte load that does not allocate in L1.
+// Streaming read-only 16-byte load that does not allocate in L1.  Deliberately not
+// `volatile`: the data is immutable for the kernel's lifetime, and a volatile asm
+// would pin the loads in program order and serialise them.
 __device__ __forceinline__ double2 ldg_stream2(const double *p) {
     double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-                 : "=d"(v.x), "=d"(v.y)
-                 : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
     return v;
 }
 __device__ __forceinline__ double ldg_stream1(const double *p) {
     double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
 

@@ -1,26 +1,31 @@
 // solve.cu -- S5..S8: the Algorithm 1 loop as ONE persistent kernel.
 //
+// Grid: G cooperative CTAs (<= 1 per SM), CTA c owns the contiguous rows
+// [d c/G, d (c+1)/G) of A~; as many of them as fit stay resident in shared memory for
+// the whole solve, the rest are re-read from L2/HBM every iteration.
+//
+// Thread layout (8 warps): warps form a Wr x Wc grid.  Column-warp cw owns the column
+// pairs cw*32P + lane + 32p (p < P), and keeps those entries of x and x* in registers;
+// row-team t processes the 32-row groups g = t, t + Wr, ...
+//
 // Every iteration k (all steps fused, no per-iteration launch):
-//   S6  r_i = b~_i - A~^(i) x_k for the CTA's rows (P:62 numerator).  Each warp keeps
-//       a private copy of x in registers (lane l holds column pairs l + 32v), so the
-//       GEMV streams only A~: from shared memory for the rows resident there, from
-//       L2/HBM (ld.global.nc, no L1 allocate) for the rest.
-//   S7  score_i = r_i^2 / nsq_i (squared form), masked rows score -1;
-//       warp argmax -> CTA argmax (smem) -> grid argmax through a one-round-trip
-//       exchange: every CTA publishes (score, lambda, idx, sum r^2) as eight 64-bit
-//       words each carrying the iteration tag in its low half (LL-style: every
-//       8-byte store is single-copy atomic, so a reader that sees the tag in all
-//       words has consistent data), double-buffered by iteration parity; one warp
-//       per CTA polls all G slots.  Ties -> lowest row index (north_star).
-//   S8  lambda = r_ik / nsq_ik (computed by the owning CTA); every warp of every CTA
-//       applies x += lambda * A~^(ik) to its register copy with the same fma in the
-//       same order, so all copies stay bit-identical and every CTA takes the same
-//       stop decision without further communication.
-//   S5  RES_{k+1} = ||x - x*||^2/||x*||^2 per warp (butterfly), or in
-//       residual mode ||r||^2/||b~||^2 from the exchanged partial sums.
-// Launch: cooperative (all CTAs co-resident, required by the spin exchange).
-#include <cooperative_groups.h>
-
+//   S6  GEMV r = b~ - A~ x_k (P:62 numerator).  For a 32-row group each lane folds its
+//       pairs into 32 row accumulators (fma, pair order), a transposed shuffle reduction
+//       leaves row l's warp partial in lane l, partials of the Wc column-warps are added
+//       in column order.  Fixed order => identical bits in every run.
+//   S7  score_i = r_i^2 / nsq_i (squared form; masked rows -1), one division per
+//       lane in parallel; warp argmax -> CTA argmax -> grid argmax through a PUSH
+//       exchange: each CTA writes (score, lambda, idx, sum r^2) into every CTA's private
+//       inbox slot (eight 64-bit words, each carrying the iteration tag in its low half:
+//       8-byte stores are single-copy atomic, so a reader that sees the tag in all words
+//       has a consistent slot), double-buffered by iteration parity; each CTA polls only
+//       its own inbox, so no L2 line is hammered by more than one reader.
+//       Ties -> lowest row index (north_star).
+//   S8  lambda = r_ik / nsq_ik (computed by the owning CTA); every CTA applies
+//       x += lambda * A~^(ik) with the same fma in the same order, so all copies of x
+//       stay bit-identical and every CTA takes the same stop decision locally.
+//   S5  RES_k = ||x_k - x*||^2/||x*||^2 from register partials, or in residual
+//       mode ||r||^2/||b~||^2 from the exchanged partial sums.
 #include <string.h>
 
 #include "csk_internal.cuh"
@@ -29,6 +34,8 @@ namespace csk {
 
 namespace {
 
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
 constexpr int kMaxSlotsPerLane = 5;  // G <= 160 CTAs
 constexpr int kMaxG = 32 * kMaxSlotsPerLane;
 constexpr int kSlotWords = 8;        // 64-byte slot
@@ -42,19 +49,21 @@ struct SolveParams {
     const double *x_star;
     double tol;
     int64_t max_iters;
-    uint64_t *slots;        // [2][G][8] words
+    uint64_t *slots;        // [2][G readers][G writers][8] words
     int64_t *report;        // [0]=iterations, [1]=final_res bits, [2]=termination, [3]=last idx
     const double *bb;       // residual mode: ||b~||^2 (device scalar)
-    int smem_rows_cap;      // rows per CTA kept in shared memory
+    int smem_rows_cap;      // rows per CTA kept in shared memory (multiple of 32 unless all)
+    int wc;                 // column warps (1, 2, 4, 8)
     int64_t trace_cap;
     int64_t *idx_trace;
     double *res_trace;
     double *x_trace;
+    int64_t *phase_cycles;  // debug: per-phase clock64 totals of CTA 0, warps 0 and 1
 };
 
 struct Cand {
     double score;
-    double lambda;
+    double r;
     double rr;
     int64_t idx;
 };
@@ -70,16 +79,16 @@ __device__ __forceinline__ bool better(double sa, int64_t ia, double sb, int64_t
     return sa > sb || (sa == sb && ia < ib);
 }
 
-__device__ __forceinline__ void warp_argmax(double &score, int64_t &idx, double &lambda) {
+__device__ __forceinline__ void warp_argmax(double &score, int64_t &idx, double &v1) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const double os = __shfl_xor_sync(0xffffffffu, score, o);
         const int64_t oi = __shfl_xor_sync(0xffffffffu, idx, o);
-        const double ol = __shfl_xor_sync(0xffffffffu, lambda, o);
+        const double o1 = __shfl_xor_sync(0xffffffffu, v1, o);
         if (better(os, oi, score, idx)) {
             score = os;
             idx = oi;
-            lambda = ol;
+            v1 = o1;
         }
     }
 }
@@ -97,29 +106,48 @@ __device__ __forceinline__ double2 load_pair_global(const double *row, int64_t q
     return v;
 }
 
-template <int NV, int R, int W, bool EVEN, bool RESMODE>
-__global__ void __launch_bounds__(W * 32, 1) k_solve(const SolveParams p) {
+// 32 row partials per lane -> lane l holds the sum over lanes of row l (fixed tree).
+__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < o; ++j) {
+            const double send = upper ? v[j] : v[j + o];
+            const double keep = upper ? v[j + o] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+template <int P, bool EVEN, bool RESMODE>
+__global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
     const int64_t d = p.d, n = p.n;
     const int64_t npairs = (n + 1) >> 1;
-    const int64_t npairs_pad = 32 * NV;
     const int64_t r0 = d * cta / G, r1 = d * (cta + 1) / G;
     const int rows = static_cast<int>(r1 - r0);
     const int srows = rows < p.smem_rows_cap ? rows : p.smem_rows_cap;
+    const int ngroups = (rows + 31) >> 5;
+    const int Wc = p.wc, Wr = kWarps / Wc;
+    const int cw = warp % Wc, team = warp / Wc;
+    const int64_t npairs_pad = static_cast<int64_t>(Wc) * 32 * P;
 
-    // shared-memory carve-up
-    double2 *xs2 = reinterpret_cast<double2 *>(smem);            // x* pairs   [npairs_pad]
-    double2 *wrow = xs2 + npairs_pad;                             // winner row [npairs_pad]
-    double *bt_loc = reinterpret_cast<double *>(wrow + npairs_pad);  // [rows]
-    double *nsq_loc = bt_loc + rows;                              // [rows]
-    Cand *cand = reinterpret_cast<Cand *>(nsq_loc + rows);                     // [W]
-    volatile int64_t *win_i = reinterpret_cast<int64_t *>(cand + W);        // [4]
-    double2 *arows = reinterpret_cast<double2 *>(cand + W) + 2;  // [srows][npairs]
+    // ---- shared-memory carve-up (16-byte aligned pieces) ----
+    double2 *wrow = reinterpret_cast<double2 *>(smem);                 // winner row [npairs_pad]
+    double *part = reinterpret_cast<double *>(wrow + npairs_pad);      // [ngroups][Wc][32]
+    double *bt_loc = part + static_cast<size_t>(ngroups) * Wc * 32;    // [rows]
+    double *nsq_loc = bt_loc + rows;                                   // [rows]
+    double *res_w = nsq_loc + rows;                                    // [8]
+    Cand *cand = reinterpret_cast<Cand *>(res_w + 8);                  // [8]
+    volatile int64_t *win = reinterpret_cast<volatile int64_t *>(cand + kWarps);  // [8]
+    double2 *arows = reinterpret_cast<double2 *>(cand + kWarps) + 4;   // [srows][npairs]
 
-    // ---- prologue: stage resident rows, b~, nsq, x* ----
-    for (int64_t e = tid; e < static_cast<int64_t>(srows) * npairs; e += blockDim.x) {
+    // ---- prologue: stage resident rows, b~, nsq; x, x* pairs into registers ----
+    for (int64_t e = tid; e < static_cast<int64_t>(srows) * npairs; e += kThreads) {
         const int64_t l = e / npairs, q = e - l * npairs;
         const double *src = p.At + (r0 + l) * n;
         double2 v;
@@ -131,263 +159,318 @@ __global__ void __launch_bounds__(W * 32, 1) k_solve(const SolveParams p) {
         }
         arows[e] = v;
     }
-    for (int l = tid; l < rows; l += blockDim.x) {
+    for (int l = tid; l < rows; l += kThreads) {
         bt_loc[l] = p.bt[r0 + l];
         nsq_loc[l] = p.nsq[r0 + l];
     }
-    for (int64_t q = tid; q < npairs_pad; q += blockDim.x) {
-        double2 v = make_double2(0.0, 0.0);
-        if (!RESMODE && q < npairs) {
-            v.x = p.x_star[2 * q];
-            if (2 * q + 1 < n) v.y = p.x_star[2 * q + 1];
-        }
-        xs2[q] = v;
-    }
-    // x_0 into registers (every warp holds the whole vector, lane-strided pairs)
-    double2 xr[NV];
+    double2 xr[P], xs[P];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        const int64_t q = lane + 32 * v;
-        xr[v] = make_double2(0.0, 0.0);
+    for (int j = 0; j < P; ++j) {
+        const int64_t q = static_cast<int64_t>(cw) * 32 * P + lane + 32 * j;
+        xr[j] = make_double2(0.0, 0.0);
+        xs[j] = make_double2(0.0, 0.0);
         if (q < npairs) {
-            xr[v].x = p.x[2 * q];
-            if (2 * q + 1 < n) xr[v].y = p.x[2 * q + 1];
+            xr[j].x = p.x[2 * q];
+            if (2 * q + 1 < n) xr[j].y = p.x[2 * q + 1];
+            if (!RESMODE) {
+                xs[j].x = p.x_star[2 * q];
+                if (2 * q + 1 < n) xs[j].y = p.x_star[2 * q + 1];
+            }
         }
+    }
+    // ||x*||^2 (team 0 partials; summed in column-warp order by every thread below)
+    if (!RESMODE && team == 0) {
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            a = __fma_rn(xs[j].x, xs[j].x, a);
+            a = __fma_rn(xs[j].y, xs[j].y, a);
+        }
+        a = warp_sum(a);
+        if (lane == 0) res_w[cw] = a;  // scratch before the loop
     }
     __syncthreads();
-
-    // ||x*||^2 and RES_0 (per warp, identical everywhere)
     double xs_nrm = 0.0;
-    double res = 0.0;
     if (!RESMODE) {
-        double a = 0.0, bnum = 0.0;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const double2 s = xs2[lane + 32 * v];
-            a = __fma_rn(s.x, s.x, a);
-            a = __fma_rn(s.y, s.y, a);
-            const double ex = xr[v].x - s.x, ey = xr[v].y - s.y;
-            bnum = __fma_rn(ex, ex, bnum);
-            bnum = __fma_rn(ey, ey, bnum);
-        }
-        xs_nrm = warp_sum(a);
-        bnum = warp_sum(bnum);
-        res = xs_nrm > 0.0 ? bnum / xs_nrm : bnum;
+        xs_nrm = res_w[0];
+        for (int c = 1; c < Wc; ++c) xs_nrm = xs_nrm + res_w[c];
     }
     const double bb = RESMODE ? *p.bb : 0.0;
+    __syncthreads();
 
-    int64_t k = 0;
-    int64_t last = -1;
+    const bool prof = p.phase_cycles != nullptr && cta == 0 && lane == 0 && warp < 2;
+    int64_t ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64();
+#define CSK_PHASE(i)                    \
+    if (prof) {                         \
+        const long long tn = clock64(); \
+        ph[i] += tn - tp;               \
+        tp = tn;                        \
+    }
+
+    int64_t k = 0, last = -1;
     int term = -1;
+    double res = 0.0;
     for (;; ++k) {
-        // trace x_k (CTA 0, warp 0)
-        if (cta == 0 && warp == 0 && k < p.trace_cap) {
-            if (p.x_trace) {
+        // ---- S5 partial: ||x_k - x*||^2 over team 0's pairs; trace x_k ----
+        if (team == 0) {
+            if (!RESMODE) {
+                double a = 0.0;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const int64_t q = lane + 32 * v;
+                for (int j = 0; j < P; ++j) {
+                    const double ex = xr[j].x - xs[j].x, ey = xr[j].y - xs[j].y;
+                    a = __fma_rn(ex, ex, a);
+                    a = __fma_rn(ey, ey, a);
+                }
+                a = warp_sum(a);
+                if (lane == 0) res_w[cw] = a;
+            }
+            if (cta == 0 && p.x_trace && k < p.trace_cap) {
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    const int64_t q = static_cast<int64_t>(cw) * 32 * P + lane + 32 * j;
                     if (q < npairs) {
-                        p.x_trace[k * n + 2 * q] = xr[v].x;
-                        if (2 * q + 1 < n) p.x_trace[k * n + 2 * q + 1] = xr[v].y;
+                        p.x_trace[k * n + 2 * q] = xr[j].x;
+                        if (2 * q + 1 < n) p.x_trace[k * n + 2 * q + 1] = xr[j].y;
                     }
                 }
             }
-            if (!RESMODE && p.res_trace && lane == 0) p.res_trace[k] = res;
-        }
-        if (!RESMODE) {
-            if (res <= p.tol) { term = CSK_CONVERGED; break; }
-            if (k == p.max_iters) { term = CSK_MAX_ITERS; break; }
         }
 
-        // ---- S6/S7 local: GEMV over this warp's rows, warp argmax ----
-        double best_s = -2.0, best_l = 0.0, rr = 0.0;
-        int64_t best_i = INT64_MAX;
-        for (int l0 = warp * R; l0 < rows; l0 += W * R) {
-            double acc[R];
+        // ---- S6: GEMV partials for this team's 32-row groups ----
+        for (int g = team; g < ngroups; g += Wr) {
+            double acc[32];
 #pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = 0.0;
+            for (int r = 0; r < 32; ++r) acc[r] = 0.0;
+            const int lbase = g * 32;
+            const bool in_smem = lbase + 32 <= srows || (srows == rows);
+            const bool full = lbase + 32 <= rows;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const int64_t q = lane + 32 * v;
+            for (int j = 0; j < P; ++j) {
+                const int64_t q = static_cast<int64_t>(cw) * 32 * P + lane + 32 * j;
                 if (q < npairs) {
+                    if (in_smem) {
+                        const double2 *src = arows + static_cast<int64_t>(lbase) * npairs + q;
+                        if (full) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int l = l0 + r;
-                        if (l < rows) {
-                            const double2 a = (l < srows)
-                                                  ? arows[static_cast<int64_t>(l) * npairs + q]
-                                                  : load_pair_global<EVEN>(p.At + (r0 + l) * n, q, n);
-                            acc[r] = __fma_rn(a.x, xr[v].x, acc[r]);
-                            acc[r] = __fma_rn(a.y, xr[v].y, acc[r]);
+                            for (int r = 0; r < 32; ++r) {
+                                const double2 a = src[static_cast<int64_t>(r) * npairs];
+                                acc[r] = __fma_rn(a.x, xr[j].x, acc[r]);
+                                acc[r] = __fma_rn(a.y, xr[j].y, acc[r]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int r = 0; r < 32; ++r) {
+                                if (lbase + r < rows) {
+                                    const double2 a = src[static_cast<int64_t>(r) * npairs];
+                                    acc[r] = __fma_rn(a.x, xr[j].x, acc[r]);
+                                    acc[r] = __fma_rn(a.y, xr[j].y, acc[r]);
+                                }
+                            }
+                        }
+                    } else {
+                        const double *src = p.At + (r0 + lbase) * n;
+                        if (full) {
+#pragma unroll
+                            for (int r = 0; r < 32; ++r) {
+                                const double2 a = load_pair_global<EVEN>(src + static_cast<int64_t>(r) * n, q, n);
+                                acc[r] = __fma_rn(a.x, xr[j].x, acc[r]);
+                                acc[r] = __fma_rn(a.y, xr[j].y, acc[r]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int r = 0; r < 32; ++r) {
+                                if (lbase + r < rows) {
+                                    const double2 a = load_pair_global<EVEN>(src + static_cast<int64_t>(r) * n, q, n);
+                                    acc[r] = __fma_rn(a.x, xr[j].x, acc[r]);
+                                    acc[r] = __fma_rn(a.y, xr[j].y, acc[r]);
+                                }
+                            }
                         }
                     }
                 }
             }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int l = l0 + r;
-                const double dot = warp_sum(acc[r]);
+            const double s = transpose_reduce32(acc, lane);
+            part[(static_cast<size_t>(g) * Wc + cw) * 32 + lane] = s;
+        }
+        CSK_PHASE(0)
+        __syncthreads();  // B1
+        CSK_PHASE(1)
+
+        // ---- S7 local: finalize rows (one per lane), warp argmax ----
+        {
+            double bs = -2.0, br = 0.0, rr = 0.0;
+            int64_t bi = INT64_MAX;
+            for (int l = warp * 32 + lane; l - lane < rows; l += kThreads) {
                 if (l < rows) {
+                    const int g = l >> 5, ln = l & 31;
+                    double dot = part[(static_cast<size_t>(g) * Wc) * 32 + ln];
+                    for (int c = 1; c < Wc; ++c) dot = dot + part[(static_cast<size_t>(g) * Wc + c) * 32 + ln];
                     const double ri = bt_loc[l] - dot;
                     const double ns = nsq_loc[l];
                     const double sc = ns > 0.0 ? (ri * ri) / ns : -1.0;
                     if (RESMODE) rr = __fma_rn(ri, ri, rr);
-                    if (sc > best_s) {  // rows visited in ascending order: keep the first max
-                        best_s = sc;
-                        best_i = r0 + l;
-                        best_l = ns > 0.0 ? ri / ns : 0.0;
-                    }
+                    if (better(sc, r0 + l, bs, bi)) { bs = sc; bi = r0 + l; br = ri; }
                 }
             }
+            if (RESMODE) rr = warp_sum(rr);
+            warp_argmax(bs, bi, br);
+            if (lane == 0) cand[warp] = Cand{bs, br, rr, bi};
         }
-        if (lane == 0) cand[warp] = Cand{best_s, best_l, rr, best_i};
-        __syncthreads();
+        __syncthreads();  // B1b
+        CSK_PHASE(2)
 
-        // ---- S7 grid: CTA candidate -> exchange -> global winner (warp 0) ----
+        // ---- S5 stop test + S7 grid exchange (warp 0) ----
         if (warp == 0) {
-            double cs = -2.0, cl = 0.0;
-            int64_t ci = INT64_MAX;
-            if (lane < W) {
-                cs = cand[lane].score;
-                cl = cand[lane].lambda;
-                ci = cand[lane].idx;
+            int stop = -1;
+            if (!RESMODE) {
+                double a = res_w[0];
+                for (int c = 1; c < Wc; ++c) a = a + res_w[c];
+                res = xs_nrm > 0.0 ? a / xs_nrm : a;
+                if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                if (res <= p.tol) stop = CSK_CONVERGED;
+                else if (k == p.max_iters) stop = CSK_MAX_ITERS;
             }
-            warp_argmax(cs, ci, cl);
-            double crr = 0.0;
-            if (RESMODE) {
-                for (int w = 0; w < W; ++w) crr = crr + cand[w].rr;  // fixed order
-            }
-            const uint32_t tag = static_cast<uint32_t>(k + 1);
-            uint64_t *slot_base = p.slots + static_cast<size_t>(k & 1) * G * kSlotWords;
-            if (lane == 0) {
+            double ws = -2.0, wl = 0.0, wrr = 0.0;
+            int64_t wi = INT64_MAX;
+            if (stop < 0) {
+                double cs = -2.0, cr = 0.0, crr = 0.0;
+                int64_t ci = INT64_MAX;
+                if (lane < kWarps) { cs = cand[lane].score; cr = cand[lane].r; ci = cand[lane].idx; }
+                warp_argmax(cs, ci, cr);
+                if (RESMODE) {
+                    for (int w = 0; w < kWarps; ++w) crr = crr + cand[w].rr;  // fixed order
+                }
+                const double cl = (cs > 0.0) ? cr / nsq_loc[ci - r0] : 0.0;
+                const uint32_t tag = static_cast<uint32_t>(k + 1);
                 const uint64_t sb = __double_as_longlong(cs), lb = __double_as_longlong(cl),
                                rb = __double_as_longlong(crr);
-                uint64_t *s = slot_base + static_cast<size_t>(cta) * kSlotWords;
-                st_relaxed_v2u64(s + 0, pack(static_cast<uint32_t>(sb >> 32), tag),
-                                 pack(static_cast<uint32_t>(sb), tag));
-                st_relaxed_v2u64(s + 2, pack(static_cast<uint32_t>(lb >> 32), tag),
-                                 pack(static_cast<uint32_t>(lb), tag));
-                st_relaxed_v2u64(s + 4, pack(static_cast<uint32_t>(rb >> 32), tag),
-                                 pack(static_cast<uint32_t>(rb), tag));
-                st_relaxed_v2u64(s + 6, pack(static_cast<uint32_t>(ci), tag), pack(0u, tag));
-            }
-            // poll every CTA's slot (lane l owns slots l, l+32, ...)
-            double gs[kMaxSlotsPerLane], gl[kMaxSlotsPerLane], gr[kMaxSlotsPerLane];
-            int64_t gi[kMaxSlotsPerLane];
-            uint32_t pending = 0;
-#pragma unroll
-            for (int j = 0; j < kMaxSlotsPerLane; ++j) {
-                gs[j] = -2.0; gl[j] = 0.0; gr[j] = 0.0; gi[j] = INT64_MAX;
-                if (lane + 32 * j < G) pending |= 1u << j;
-            }
-            while (true) {
+                const uint64_t w0 = pack(static_cast<uint32_t>(sb >> 32), tag), w1 = pack(static_cast<uint32_t>(sb), tag);
+                const uint64_t w2 = pack(static_cast<uint32_t>(lb >> 32), tag), w3 = pack(static_cast<uint32_t>(lb), tag);
+                const uint64_t w4 = pack(static_cast<uint32_t>(rb >> 32), tag), w5 = pack(static_cast<uint32_t>(rb), tag);
+                const uint64_t w6 = pack(static_cast<uint32_t>(ci), tag), w7 = pack(0u, tag);
+                uint64_t *par = p.slots + static_cast<size_t>(k & 1) * G * G * kSlotWords;
+                // push: this CTA's candidate into every reader's inbox (lane l -> readers l + 32j)
 #pragma unroll
                 for (int j = 0; j < kMaxSlotsPerLane; ++j) {
-                    if (pending & (1u << j)) {
-                        const uint64_t *s = slot_base + static_cast<size_t>(lane + 32 * j) * kSlotWords;
-                        uint64_t w0, w1, w2, w3, w4, w5, w6, w7;
-                        ld_relaxed_v2u64(s + 0, w0, w1);
-                        ld_relaxed_v2u64(s + 2, w2, w3);
-                        ld_relaxed_v2u64(s + 4, w4, w5);
-                        ld_relaxed_v2u64(s + 6, w6, w7);
-                        const bool ok = static_cast<uint32_t>(w0) == tag &&
-                                        static_cast<uint32_t>(w1) == tag &&
-                                        static_cast<uint32_t>(w2) == tag &&
-                                        static_cast<uint32_t>(w3) == tag &&
-                                        static_cast<uint32_t>(w4) == tag &&
-                                        static_cast<uint32_t>(w5) == tag &&
-                                        static_cast<uint32_t>(w6) == tag;
-                        if (ok) {
-                            gs[j] = __longlong_as_double(static_cast<long long>((w0 >> 32) << 32 | (w1 >> 32)));
-                            gl[j] = __longlong_as_double(static_cast<long long>((w2 >> 32) << 32 | (w3 >> 32)));
-                            gr[j] = __longlong_as_double(static_cast<long long>((w4 >> 32) << 32 | (w5 >> 32)));
-                            const uint32_t iw = static_cast<uint32_t>(w6 >> 32);
-                            gi[j] = (iw == 0xffffffffu) ? INT64_MAX : static_cast<int64_t>(iw);
-                            pending &= ~(1u << j);
-                        }
+                    const int rd = lane + 32 * j;
+                    if (rd < G) {
+                        uint64_t *s = par + (static_cast<size_t>(rd) * G + cta) * kSlotWords;
+                        st_relaxed_v2u64(s + 0, w0, w1);
+                        st_relaxed_v2u64(s + 2, w2, w3);
+                        st_relaxed_v2u64(s + 4, w4, w5);
+                        st_relaxed_v2u64(s + 6, w6, w7);
                     }
                 }
-                if (__all_sync(0xffffffffu, pending == 0)) break;
-            }
-            // combine in a fixed order: lane's slots ascending, then butterfly
-            double ws = -2.0, wl = 0.0, wr = 0.0;
-            int64_t wi = INT64_MAX;
+                CSK_PHASE(3)
+                // poll own inbox (lane l owns writers l, l+32, ...)
+                const uint64_t *inbox = par + static_cast<size_t>(cta) * G * kSlotWords;
+                double gs[kMaxSlotsPerLane], gl[kMaxSlotsPerLane], gr[kMaxSlotsPerLane];
+                int64_t gi[kMaxSlotsPerLane];
+                uint32_t pending = 0;
 #pragma unroll
-            for (int j = 0; j < kMaxSlotsPerLane; ++j) {
-                if (better(gs[j], gi[j], ws, wi)) { ws = gs[j]; wi = gi[j]; wl = gl[j]; }
-                if (RESMODE) wr = wr + gr[j];
-            }
-            warp_argmax(ws, wi, wl);
-            if (RESMODE) wr = warp_sum(wr);
-            if (lane == 0) {
-                win_i[0] = wi;
-                win_i[1] = __double_as_longlong(wl);
-                win_i[2] = __double_as_longlong(ws);
-                win_i[3] = __double_as_longlong(wr);
-            }
-            // stage the winner row A~^(ik) in shared memory
-            if (ws > 0.0) {
-                const double *src = p.At + wi * n;
+                for (int j = 0; j < kMaxSlotsPerLane; ++j) {
+                    gs[j] = -2.0; gl[j] = 0.0; gr[j] = 0.0; gi[j] = INT64_MAX;
+                    if (lane + 32 * j < G) pending |= 1u << j;
+                }
+                while (true) {
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const int64_t q = lane + 32 * v;
-                    if (q < npairs) wrow[q] = load_pair_global<EVEN>(src, q, n);
+                    for (int j = 0; j < kMaxSlotsPerLane; ++j) {
+                        if (pending & (1u << j)) {
+                            const uint64_t *s = inbox + static_cast<size_t>(lane + 32 * j) * kSlotWords;
+                            uint64_t a0, a1, a2, a3, a4, a5, a6, a7;
+                            ld_relaxed_v2u64(s + 0, a0, a1);
+                            ld_relaxed_v2u64(s + 2, a2, a3);
+                            ld_relaxed_v2u64(s + 4, a4, a5);
+                            ld_relaxed_v2u64(s + 6, a6, a7);
+                            const bool ok = static_cast<uint32_t>(a0) == tag && static_cast<uint32_t>(a1) == tag &&
+                                            static_cast<uint32_t>(a2) == tag && static_cast<uint32_t>(a3) == tag &&
+                                            static_cast<uint32_t>(a4) == tag && static_cast<uint32_t>(a5) == tag &&
+                                            static_cast<uint32_t>(a6) == tag;
+                            if (ok) {
+                                gs[j] = __longlong_as_double(static_cast<long long>((a0 >> 32) << 32 | (a1 >> 32)));
+                                gl[j] = __longlong_as_double(static_cast<long long>((a2 >> 32) << 32 | (a3 >> 32)));
+                                gr[j] = __longlong_as_double(static_cast<long long>((a4 >> 32) << 32 | (a5 >> 32)));
+                                const uint32_t iw = static_cast<uint32_t>(a6 >> 32);
+                                gi[j] = (iw == 0xffffffffu) ? INT64_MAX : static_cast<int64_t>(iw);
+                                pending &= ~(1u << j);
+                            }
+                        }
+                    }
+                    if (__all_sync(0xffffffffu, pending == 0)) break;
+                }
+                CSK_PHASE(4)
+                // combine in a fixed order: lane's slots ascending, then butterfly
+#pragma unroll
+                for (int j = 0; j < kMaxSlotsPerLane; ++j) {
+                    if (better(gs[j], gi[j], ws, wi)) { ws = gs[j]; wi = gi[j]; wl = gl[j]; }
+                    if (RESMODE) wrr = wrr + gr[j];
+                }
+                warp_argmax(ws, wi, wl);
+                if (RESMODE) {
+                    wrr = warp_sum(wrr);
+                    res = bb > 0.0 ? wrr / bb : wrr;
+                    if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                    if (res <= p.tol) stop = CSK_CONVERGED;
+                    else if (k == p.max_iters) stop = CSK_MAX_ITERS;
+                }
+                if (stop < 0) {
+                    if (ws < 0.0) stop = -2;                 // every row masked: zero sketch
+                    else if (ws == 0.0) stop = CSK_STAGNATED;
+                }
+                if (stop < 0) {
+                    // stage the winner row A~^(ik) in shared memory
+                    const double *src = p.At + wi * n;
+                    for (int64_t q = lane; q < npairs; q += 32) wrow[q] = load_pair_global<EVEN>(src, q, n);
+                    if (cta == 0 && lane == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wi;
                 }
             }
+            if (lane == 0) {
+                win[0] = wi;
+                win[1] = __double_as_longlong(wl);
+                win[2] = stop;
+                win[3] = __double_as_longlong(res);
+            }
+            CSK_PHASE(5)
         }
-        __syncthreads();
-
-        const int64_t wi = win_i[0];
-        const double wl = __longlong_as_double(win_i[1]);
-        const double ws = __longlong_as_double(win_i[2]);
-        if (RESMODE) {
-            const double rrt = __longlong_as_double(win_i[3]);
-            res = bb > 0.0 ? rrt / bb : rrt;
-            if (cta == 0 && tid == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
-            if (res <= p.tol) { term = CSK_CONVERGED; break; }
-            if (k == p.max_iters) { term = CSK_MAX_ITERS; break; }
+        __syncthreads();  // B2
+        CSK_PHASE(6)
+        const int stop = static_cast<int>(win[2]);
+        if (stop >= 0 || stop == -2) {
+            term = stop;
+            res = __longlong_as_double(win[3]);
+            break;
         }
-        if (ws < 0.0) { term = -2; break; }            // every row masked: zero sketch
-        if (ws == 0.0) { term = CSK_STAGNATED; break; }
-        if (cta == 0 && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wi;
-
         // ---- S8: x_{k+1} = x_k + lambda A~^(ik)T ----
+        const double wl = __longlong_as_double(win[1]);
+        last = win[0];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const int64_t q = lane + 32 * v;
+        for (int j = 0; j < P; ++j) {
+            const int64_t q = static_cast<int64_t>(cw) * 32 * P + lane + 32 * j;
             if (q < npairs) {
                 const double2 a = wrow[q];
-                xr[v].x = __fma_rn(wl, a.x, xr[v].x);
-                xr[v].y = __fma_rn(wl, a.y, xr[v].y);
+                xr[j].x = __fma_rn(wl, a.x, xr[j].x);
+                xr[j].y = __fma_rn(wl, a.y, xr[j].y);
             }
         }
-        last = wi;
-        // ---- S5: RES_{k+1} ----
-        if (!RESMODE) {
-            double bnum = 0.0;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const double2 s = xs2[lane + 32 * v];
-                const double ex = xr[v].x - s.x, ey = xr[v].y - s.y;
-                bnum = __fma_rn(ex, ex, bnum);
-                bnum = __fma_rn(ey, ey, bnum);
-            }
-            bnum = warp_sum(bnum);
-            res = xs_nrm > 0.0 ? bnum / xs_nrm : bnum;
-        }
+        CSK_PHASE(7)
+    }
+#undef CSK_PHASE
+    if (prof) {
+        for (int i = 0; i < 8; ++i) p.phase_cycles[warp * 8 + i] = ph[i];
     }
 
-    // ---- epilogue: CTA 0 writes x and the report ----
-    if (cta == 0 && warp == 0) {
+    // ---- epilogue: CTA 0 team 0 writes x; thread 0 the report ----
+    if (cta == 0 && team == 0) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const int64_t q = lane + 32 * v;
+        for (int j = 0; j < P; ++j) {
+            const int64_t q = static_cast<int64_t>(cw) * 32 * P + lane + 32 * j;
             if (q < npairs) {
-                p.x[2 * q] = xr[v].x;
-                if (2 * q + 1 < n) p.x[2 * q + 1] = xr[v].y;
+                p.x[2 * q] = xr[j].x;
+                if (2 * q + 1 < n) p.x[2 * q + 1] = xr[j].y;
             }
         }
-        if (lane == 0) {
+        if (tid == 0) {
             p.report[0] = k;
             p.report[1] = __double_as_longlong(res);
             p.report[2] = term;
@@ -413,31 +496,24 @@ __global__ void k_sumsq(const double *v, int64_t len, double *out) {
 
 using KernelFn = void (*)(const SolveParams);
 
-template <int NV, bool EVEN, bool RESMODE>
-KernelFn pick_w() {
-    constexpr int R = NV >= 32 ? 1 : 2;
-    constexpr int W = NV <= 4 ? 16 : 8;
-    return k_solve<NV, R, W, EVEN, RESMODE>;
-}
-template <int NV>
-KernelFn pick_mode(bool even, bool resmode, int &warps) {
-    warps = NV <= 4 ? 16 : 8;
-    if (even) return resmode ? pick_w<NV, true, true>() : pick_w<NV, true, false>();
-    return resmode ? pick_w<NV, false, true>() : pick_w<NV, false, false>();
+template <int P>
+KernelFn pick_mode(bool even, bool resmode) {
+    if (even) return resmode ? k_solve<P, true, true> : k_solve<P, true, false>;
+    return resmode ? k_solve<P, false, true> : k_solve<P, false, false>;
 }
 
-KernelFn pick_kernel(int64_t n, bool resmode, int &nv, int &warps) {
+// P = column pairs per lane (power of two), Wc = column warps (power of two <= 8).
+KernelFn pick_kernel(int64_t n, bool resmode, int &P, int &wc) {
     const int64_t npairs = (n + 1) / 2;
+    P = 1;
+    while (32 * kWarps * P < npairs) P *= 2;
+    wc = 1;
+    while (wc < kWarps && 32 * P * wc < npairs) wc *= 2;
     const bool even = (n & 1) == 0;
-    nv = 1;
-    while (32 * nv < npairs) nv *= 2;
-    switch (nv) {
-        case 1: return pick_mode<1>(even, resmode, warps);
-        case 2: return pick_mode<2>(even, resmode, warps);
-        case 4: return pick_mode<4>(even, resmode, warps);
-        case 8: return pick_mode<8>(even, resmode, warps);
-        case 16: return pick_mode<16>(even, resmode, warps);
-        case 32: return pick_mode<32>(even, resmode, warps);
+    switch (P) {
+        case 1: return pick_mode<1>(even, resmode);
+        case 2: return pick_mode<2>(even, resmode);
+        case 4: return pick_mode<4>(even, resmode);
         default: return nullptr;
     }
 }
@@ -454,37 +530,44 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     if (d >= (int64_t(1) << 31) - 1) return fail(ctx, CSK_E_ARG, "csk_solve: d >= 2^31");
     if (n > CSK_MAX_N) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n > CSK_MAX_N");
     if ((n % 2 == 0) && !aligned16(At)) return fail(ctx, CSK_E_ARG, "csk_solve: A~ not 16-byte aligned");
+    if (ctx->pending) return fail(ctx, CSK_E_ARG, "csk_solve: a CSK_SOLVE_ASYNC solve is still in flight (call csk_solve_wait)");
     const bool resmode = (x_star == nullptr);
-    int nv = 0, warps = 0;
-    KernelFn fn = pick_kernel(n, resmode, nv, warps);
+    int P = 0, wc = 0;
+    KernelFn fn = pick_kernel(n, resmode, P, wc);
     if (!fn) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n out of range");
-    const int threads = warps * 32;
 
     int G = ctx->num_sms;
     if (opts && opts->num_ctas > 0) G = opts->num_ctas;
     if (G > kMaxG) G = kMaxG;
     if (G > d) G = static_cast<int>(d);
     const int64_t rows_max = (d + G - 1) / G;
+    const int64_t ngroups = (rows_max + 31) / 32;
     const int64_t npairs = (n + 1) / 2;
-    const size_t fixed = static_cast<size_t>(2 * 32 * nv) * 16 + static_cast<size_t>(rows_max) * 16 +
-                         static_cast<size_t>(warps) * sizeof(Cand) + 4 * 8 + 64;
+    const int64_t npairs_pad = static_cast<int64_t>(wc) * 32 * P;
+    const size_t fixed = static_cast<size_t>(npairs_pad) * 16 + static_cast<size_t>(ngroups) * wc * 32 * 8 +
+                         static_cast<size_t>(rows_max) * 16 + 8 * 8 + kWarps * sizeof(Cand) + 64 + 64;
     const size_t avail = ctx->max_smem_optin > static_cast<int>(fixed) ? ctx->max_smem_optin - fixed : 0;
     int64_t srows = static_cast<int64_t>(avail / (static_cast<size_t>(npairs) * 16));
-    if (srows > rows_max) srows = rows_max;
-    if (opts && opts->smem_rows > 0 && opts->smem_rows < srows) srows = opts->smem_rows;
+    if (srows >= rows_max) {
+        srows = rows_max;
+    } else {
+        srows = (srows / 32) * 32;  // whole 32-row groups so every group has one source
+    }
+    if (opts && opts->smem_rows > 0 && opts->smem_rows < srows) srows = (opts->smem_rows / 32) * 32;
     if (opts && opts->smem_rows < 0) srows = 0;
     const size_t smem = fixed + static_cast<size_t>(srows) * npairs * 16;
 
     CSK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
-    CSK_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+    CSK_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
     if (per_sm * ctx->num_sms < G)
         return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
 
-    CSK_CHECK(ensure(ctx, ctx->slots, static_cast<size_t>(2) * G * kSlotWords * 8));
+    const size_t slot_bytes = static_cast<size_t>(2) * G * G * kSlotWords * 8;
+    CSK_CHECK(ensure(ctx, ctx->slots, slot_bytes));
     CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
-    CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, static_cast<size_t>(2) * G * kSlotWords * 8, stream));
+    CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, slot_bytes, stream));
     double *bb = static_cast<double *>(ctx->scalars.ptr);
     if (resmode) k_sumsq<<<1, 1024, 0, stream>>>(bt, d, bb);
 
@@ -495,14 +578,16 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     prm.report = static_cast<int64_t *>(ctx->report.ptr);
     prm.bb = bb;
     prm.smem_rows_cap = static_cast<int>(srows);
+    prm.wc = wc;
     prm.trace_cap = opts ? opts->trace_cap : 0;
     prm.idx_trace = opts ? opts->idx_trace : nullptr;
     prm.res_trace = opts ? opts->res_trace : nullptr;
     prm.x_trace = opts ? opts->x_trace : nullptr;
+    prm.phase_cycles = opts ? opts->phase_cycles : nullptr;
     if (prm.trace_cap <= 0) { prm.idx_trace = nullptr; prm.res_trace = nullptr; prm.x_trace = nullptr; prm.trace_cap = 0; }
 
     void *args[] = {&prm};
-    CSK_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void *>(fn), dim3(G), dim3(threads), args, smem, stream));
+    CSK_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void *>(fn), dim3(G), dim3(kThreads), args, smem, stream));
     CSK_CHECK(ensure_host_report(ctx));
     CSK_CUDA(ctx, cudaMemcpyAsync(ctx->report_host, ctx->report.ptr, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
     ctx->pending_stream = stream;
