@@ -84,7 +84,7 @@ typedef struct {
     int32_t smem_rows;     /* rows of A~ kept in shared memory per CTA: 0 = auto (max),
                               -1 = none (every row re-read from L2/HBM), k > 0 = at most k */
     int32_t flags;         /* CSK_SOLVE_ASYNC */
-    int32_t reserved;
+    int32_t cluster_size;  /* CTAs per thread-block cluster (power of two <= 16); 0 = auto */
     int64_t trace_cap;     /* capacity of the traces below (iterations) */
     int64_t *idx_trace;    /* device int64[trace_cap]: i_k, or NULL */
     double *res_trace;     /* device double[trace_cap]: stop quantity at x_k, or NULL */
@@ -180,6 +180,11 @@ CSK_API csk_status_t csk_solve_ex(csk_ctx_t ctx, const double *A_tilde, const do
  * solve on this ctx and fill *report (host).  Returns that solve's status
  * (e.g. CSK_E_ZERO_SKETCH).  x is valid only after this returns. */
 CSK_API csk_status_t csk_solve_wait(csk_ctx_t ctx, csk_report_t *report);
+
+/* Launch geometry the last csk_solve* on this ctx used: CTAs, CTAs per cluster, rows of
+ * A~ kept in shared memory per CTA (any pointer may be NULL). */
+CSK_API csk_status_t csk_last_solve_geometry(csk_ctx_t ctx, int32_t *num_ctas, int32_t *cluster_size,
+                                             int32_t *smem_rows);
 
 /* ---- Whole Algorithm 1 (INPUT A, b, d, x0 -> OUTPUT x) ---------------- */
 /* Plan + sketch + norms + loop on device buffers (workspace for A~, b~, nsq owned

@@ -49,7 +49,7 @@ class Report(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("num_ctas", ctypes.c_int32), ("smem_rows", ctypes.c_int32),
-                ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
                 ("trace_cap", ctypes.c_int64), ("idx_trace", ctypes.c_void_p),
                 ("res_trace", ctypes.c_void_p), ("x_trace", ctypes.c_void_p),
                 ("phase_cycles", ctypes.c_void_p)]
@@ -78,6 +78,8 @@ def _load():
         "csk_solve_ex": ([P, P, P, P, i64, i64, P, P, dbl, i64, ctypes.POINTER(SolveOpts),
                           ctypes.POINTER(Report), P], i32),
         "csk_solve_wait": ([P, ctypes.POINTER(Report)], i32),
+        "csk_last_solve_geometry": ([P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int32)], i32),
         "csk_run": ([P, P, i64, P, i64, i64, i64, u64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
         "csk_run_host": ([P, P, i64, P, i64, i64, i64, u64, P, P, dbl, i64,
                           ctypes.POINTER(Report), P], i32),
@@ -273,8 +275,9 @@ class SolveResult:
 
 
 def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
-              num_ctas: int = 0, smem_rows: int = 0, trace: int = 0, trace_x: bool = False,
-              phase_cycles: torch.Tensor | None = None, ctx: Context | None = None) -> SolveResult:
+              num_ctas: int = 0, smem_rows: int = 0, cluster_size: int = 0, trace: int = 0,
+              trace_x: bool = False, phase_cycles: torch.Tensor | None = None,
+              ctx: Context | None = None) -> SolveResult:
     """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel."""
     ctx = ctx or default_context()
     _need(At, torch.float64, "A_tilde", 2)
@@ -287,6 +290,7 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
     opts = SolveOpts()
     opts.num_ctas = num_ctas
     opts.smem_rows = smem_rows
+    opts.cluster_size = cluster_size
     idx_t = res_t = x_t = None
     if trace:
         idx_t = torch.full((trace,), -1, dtype=torch.int64, device=At.device)
@@ -312,7 +316,8 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
 
 
 def csk_solve_async(At, bt, nsq, x, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
-                    num_ctas: int = 0, smem_rows: int = 0, ctx: Context | None = None):
+                    num_ctas: int = 0, smem_rows: int = 0, cluster_size: int = 0,
+                    ctx: Context | None = None):
     """Launch the loop without waiting (CSK_SOLVE_ASYNC); x (in/out) is updated in place.
     Call ``csk_solve_wait(ctx)`` for the report."""
     ctx = ctx or default_context()
@@ -320,9 +325,18 @@ def csk_solve_async(At, bt, nsq, x, x_star=None, tol: float = 1e-6, max_iters: i
     opts = SolveOpts()
     opts.num_ctas = num_ctas
     opts.smem_rows = smem_rows
+    opts.cluster_size = cluster_size
     opts.flags = SOLVE_ASYNC
     ctx.check(lib.csk_solve_ex(ctx.handle, _ptr(At), _ptr(bt), _ptr(nsq), d, n, _ptr(x), _ptr(x_star),
                                float(tol), int(max_iters), ctypes.byref(opts), None, _stream()))
+
+
+def csk_last_solve_geometry(ctx: Context | None = None) -> dict:
+    """{'num_ctas', 'cluster_size', 'smem_rows'} of the last solve on ``ctx``."""
+    ctx = ctx or default_context()
+    g, c, r = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    ctx.check(lib.csk_last_solve_geometry(ctx.handle, ctypes.byref(g), ctypes.byref(c), ctypes.byref(r)))
+    return {"num_ctas": g.value, "cluster_size": c.value, "smem_rows": r.value}
 
 
 def csk_solve_wait(ctx: Context | None = None) -> Report:

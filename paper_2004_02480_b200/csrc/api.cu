@@ -191,6 +191,15 @@ csk_status_t csk_solve_wait(csk_ctx_t ctx, csk_report_t *report) {
     return finish_solve(ctx, report);
 }
 
+csk_status_t csk_last_solve_geometry(csk_ctx_t ctx, int32_t *num_ctas, int32_t *cluster_size,
+                                     int32_t *smem_rows) {
+    if (!ctx) return CSK_E_ARG;
+    if (num_ctas) *num_ctas = ctx->last_solve_geom[0];
+    if (cluster_size) *cluster_size = ctx->last_solve_geom[1];
+    if (smem_rows) *smem_rows = ctx->last_solve_geom[2];
+    return CSK_OK;
+}
+
 csk_status_t csk_run(csk_ctx_t ctx, const double *A, int64_t lda, const double *b, int64_t m,
                      int64_t n, int64_t d, uint64_t seed, double *x, const double *x_star,
                      double tol, int64_t max_iters, csk_report_t *report, void *stream) {

@@ -38,6 +38,7 @@ struct csk_ctx_s {
     cudaStream_t pending_stream = nullptr;
     bool pending = false;
     bool pending_resmode = false;
+    int last_solve_geom[3] = {0, 0, 0};  // CTAs, cluster size, smem rows
 };
 
 namespace csk {
@@ -173,6 +174,41 @@ __device__ __forceinline__ void ld_relaxed_v2u64(const uint64_t *p, uint64_t &a,
                  : "=l"(a), "=l"(b)
                  : "l"(p)
                  : "memory");
+}
+
+// ---- thread-block-cluster / DSMEM helpers (sm_90+) ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// Address of the same shared-memory offset in cluster CTA `rank`.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v2u64(uint32_t addr, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.cluster.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void ld_cluster_local_v2u64(uint32_t addr, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.relaxed.cluster.shared::cta.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ double2 ld_dsmem_v2f64(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+// Same, for data that is immutable while the kernel runs (not volatile: may be batched).
+__device__ __forceinline__ double2 ld_dsmem_v2f64_nc(uint32_t addr) {
+    double2 v;
+    asm("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace csk

@@ -150,13 +150,16 @@ def test_solve_parity_small_configs(csk, name):
     assert abs(g.final_res - oracle.solve(_np(At), _np(bt), _np(nsq), x0=_np(g.x), x_star=_np(p.x_star), max_iters=0).final_res) <= 1e-12
 
 
-@pytest.mark.parametrize("num_ctas,smem_rows", [(1, 0), (7, 0), (148, -1), (37, 3), (2, -1)])
-def test_solve_launch_shapes_and_streamed_rows(csk, num_ctas, smem_rows):
-    """The L2/HBM-streamed GEMV path (smem_rows = -1: no resident rows) and odd grids."""
+@pytest.mark.parametrize("num_ctas,smem_rows,cluster", [
+    (1, 0, 1), (7, 0, 1), (148, -1, 1), (37, 40, 0), (2, -1, 2), (32, 0, 16), (112, -1, 16),
+    (64, 17, 4), (16, 0, 8), (0, 0, 0), (146, 5, 2)])
+def test_solve_launch_shapes_and_streamed_rows(csk, num_ctas, smem_rows, cluster):
+    """Grids, cluster sizes (the DSMEM / global exchange hops) and the L2/HBM-streamed
+    GEMV path (smem_rows = -1: no resident rows; k > 0: resident/streamed split)."""
     p = make_dense(8000, 300, "lognormal_rows", 91, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, 1500, seed=4)
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, num_ctas=num_ctas, smem_rows=smem_rows,
-                      trace=300, trace_x=True)
+                      cluster_size=cluster, trace=300, trace_x=True)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), trace=300)
     _free_running(g, o)
     _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 300)
@@ -186,10 +189,11 @@ def test_solve_ragged_n(csk, n):
         _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 8)
 
 
-def test_solve_residual_mode(csk):
+@pytest.mark.parametrize("num_ctas,cluster", [(0, 0), (148, 1), (64, 16)])
+def test_solve_residual_mode(csk, num_ctas, cluster):
     p = make_dense(6000, 40, "gauss", 12, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, 400, seed=2)
-    g = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-10)
+    g = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-10, num_ctas=num_ctas, cluster_size=cluster)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=None, tol=1e-10)
     assert g.stop_mode == csk.STOP_RESIDUAL and g.termination == csk.CONVERGED
     assert abs(g.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
