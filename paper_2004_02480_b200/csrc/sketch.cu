@@ -25,20 +25,31 @@ namespace {
 
 constexpr int kPmax = 4;               // column pairs per consumer thread (template max)
 constexpr int kMaxConsumers = 256;     // consumer threads per CTA
-constexpr int kMaxSlots = 64;          // ring depth cap
-constexpr int kRingBudget = 192 * 1024;
+constexpr int kMaxStages = 32;         // ring depth cap
+constexpr int kMaxRB = 32;             // rows per stage cap
+constexpr int kRingBudget = 200 * 1024;
+constexpr int kStageTarget = 16 * 1024;  // bytes per stage (TMA batch)
 
 struct DenseGeom {
     int tc;          // consumer threads (multiple of 32)
     int p;           // pairs per consumer thread (1, 2 or 4)
     int chunk_cols;  // columns per chunk (even), = 2 * tc * p
     int chunks;      // ceil(n / chunk_cols)
-    int slot_bytes;  // ring slot stride (multiple of 128)
-    int slots;       // ring depth
+    int slot_bytes;  // bytes per row slot (multiple of 128)
+    int rb;          // rows per ring stage
+    int stages;      // ring depth
+    size_t header;   // barriers + metadata
     size_t smem;     // dynamic shared memory
 };
 
-DenseGeom dense_geom(int64_t n) {
+size_t dense_header(int stages, int rb) {
+    // full[stages], empty[stages] (8 B), meta[stages][kMaxRB] (4 B), red[2][8] doubles (last 128 B)
+    (void)rb;
+    size_t h = static_cast<size_t>(stages) * 16 + static_cast<size_t>(stages) * kMaxRB * 4 + 2 * 8 * 8;
+    return (h + 127) / 128 * 128;
+}
+
+DenseGeom dense_geom(int64_t n, bool tma) {
     DenseGeom g{};
     const int64_t pairs = (n + 1) / 2;
     int64_t tc = ((pairs + 31) / 32) * 32;
@@ -51,15 +62,18 @@ DenseGeom dense_geom(int64_t n) {
     g.chunk_cols = 2 * g.tc * g.p;
     g.chunks = static_cast<int>((n + g.chunk_cols - 1) / g.chunk_cols);
     const int64_t cols0 = n < g.chunk_cols ? n : g.chunk_cols;
-    g.slot_bytes = static_cast<int>(((cols0 * 8 + 127) / 128) * 128);
-    int slots = kRingBudget / g.slot_bytes;
-    if (slots > kMaxSlots) slots = kMaxSlots;
-    if (slots < 2) slots = 2;
-    g.slots = slots;
-    // header: full[slots], empty[slots] (8 B each), sign/row[slots] (4 B each), red[2][8] doubles
-    size_t header = static_cast<size_t>(slots) * 16 + static_cast<size_t>(slots) * 8 + 2 * 8 * 8;
-    header = (header + 127) / 128 * 128;
-    g.smem = header + static_cast<size_t>(slots) * g.slot_bytes;
+    g.slot_bytes = tma ? static_cast<int>(((cols0 * 8 + 127) / 128) * 128) : 0;
+    int rb = tma ? kStageTarget / g.slot_bytes : 8;
+    if (rb < 1) rb = 1;
+    if (rb > kMaxRB) rb = kMaxRB;
+    while (rb & (rb - 1)) rb &= rb - 1;  // power of two: whole stages per 32-row perm window
+    g.rb = rb;
+    int stages = tma ? kRingBudget / (rb * g.slot_bytes) : 4;
+    if (stages > kMaxStages) stages = kMaxStages;
+    if (stages < 2) stages = 2;
+    g.stages = stages;
+    g.header = dense_header(stages, rb);
+    g.smem = g.header + static_cast<size_t>(stages) * rb * g.slot_bytes;
     return g;
 }
 
@@ -92,21 +106,23 @@ __device__ __forceinline__ double warp_sum(double v) {
 // TMA = true: rows staged by 1-D bulk copies (A 16-byte aligned, lda even).
 // TMA = false: any alignment; the producer only publishes the row order and the
 // consumers read their columns straight from global memory (same adds, same order).
-template <int P, bool TMA>
+// The CTA's rows are the contiguous range [t0, t1) of `perm`; the ring moves them in
+// stages of `rb` rows (one full/empty mbarrier pair per stage); slot and phase are
+// tracked incrementally (no division on the per-row path).
+template <int P, bool TMA, int RB>
 __global__ void __launch_bounds__(kMaxConsumers + 64, 1)
 k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m,
                int64_t n, int64_t d, const int32_t *__restrict__ perm,
                const int32_t *__restrict__ offsets, double *__restrict__ At,
                double *__restrict__ bt, double *__restrict__ nsq, int tc, int chunk_cols,
-               int chunks, int slot_bytes, int slots) {
+               int chunks, int slot_bytes, int rb, int stages, int header) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + slots;
-    int32_t *slot_row = reinterpret_cast<int32_t *>(empty + slots);  // row | sign bit
-    double *red = reinterpret_cast<double *>(slot_row + slots + (slots & 1));  // [2][8]
-    size_t header = static_cast<size_t>(slots) * 16 + static_cast<size_t>(slots) * 8 + 2 * 8 * 8;
-    header = (header + 127) / 128 * 128;
+    uint64_t *empty = full + stages;
+    int32_t *meta = reinterpret_cast<int32_t *>(empty + stages);   // [stages][kMaxRB] row | sign bit
+    double *red = reinterpret_cast<double *>(smem + header) - 16;  // [2][8] (end of header)
     unsigned char *ring = smem + header;
+    const int stage_bytes = rb * slot_bytes;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -119,7 +135,7 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
         cta_buckets(offsets, m, d, blockIdx.x, gridDim.x, j0, j1);
         s_j0 = j0;
         s_j1 = j1;
-        for (int s = 0; s < slots; ++s) {
+        for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], wc);
         }
@@ -130,33 +146,44 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
     if (j0 >= j1) return;
     const int64_t t0 = offsets[j0];
     const int64_t t1 = offsets[j1];
+    const int64_t nrows = t1 - t0;
+    const int64_t nst = (nrows + rb - 1) / rb;  // stages per chunk
 
     if (warp == wc) {
         // ------------------------------------------------ producer warp (TMA)
-        int64_t u = 0;
+        int s = 0;
+        uint32_t ph = 0;   // phase of the current use of stage s
+        int64_t use = 0;   // total stage uses so far
         for (int c = 0; c < chunks; ++c) {
             const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
             const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
             const uint32_t bytes = TMA ? static_cast<uint32_t>(((c1 - c0) & ~int64_t(1)) * 8) : 0u;
-            for (int64_t tb = t0; tb < t1; tb += 32) {
-                const int64_t tl = tb + lane;
-                const int32_t mine = tl < t1 ? __ldg(perm + tl) : 0;
-                const int cnt = static_cast<int>((t1 - tb) < 32 ? (t1 - tb) : 32);
-                for (int k = 0; k < cnt; ++k, ++u) {
-                    const int32_t pr = __shfl_sync(0xffffffffu, mine, k);
-                    if (lane == 0) {
-                        const int s = static_cast<int>(u % slots);
-                        const int64_t use = u / slots;
-                        if (use > 0) mbar_wait(&empty[s], static_cast<uint32_t>((use - 1) & 1));
-                        slot_row[s] = pr;
-                        mbar_arrive_expect_tx(&full[s], bytes);
-                        if (bytes) {
-                            const int64_t row = pr & 0x7fffffff;
-                            bulk_g2s(ring + static_cast<size_t>(s) * slot_bytes,
-                                     A + row * lda + c0, bytes, &full[s]);
-                        }
-                    }
+            // perm is read 32 rows (32/rb whole stages) at a time, one window ahead
+            int32_t cur = (t0 + lane < t1) ? __ldg(perm + t0 + lane) : 0;
+            int32_t nxt = 0;
+            for (int64_t u = 0; u < nst; ++u, ++use) {
+                const int64_t tb = t0 + u * rb;
+                const int wofs = static_cast<int>((u * rb) & 31);
+                if (wofs == 0) {
+                    if (u > 0) cur = nxt;
+                    const int64_t tn = tb + 32 + lane;
+                    nxt = (tn < t1) ? __ldg(perm + tn) : 0;
                 }
+                const int cnt = static_cast<int>((t1 - tb) < rb ? (t1 - tb) : rb);
+                const int32_t mine = __shfl_sync(0xffffffffu, cur, (wofs + lane) & 31);
+                if (use >= stages) mbar_wait(&empty[s], ph ^ 1u);
+                if (lane < cnt) meta[s * kMaxRB + lane] = mine;
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[s], bytes * static_cast<uint32_t>(cnt));
+                }
+                __syncwarp();
+                if (bytes && lane < cnt) {
+                    const int64_t row = mine & 0x7fffffff;
+                    bulk_g2s(ring + static_cast<size_t>(s) * stage_bytes + static_cast<size_t>(lane) * slot_bytes,
+                             A + row * lda + c0, bytes, &full[s]);
+                }
+                if (++s == stages) { s = 0; ph ^= 1u; }
             }
         }
         return;
@@ -188,68 +215,41 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
     }
 
     // ---------------------------------------------------- consumer warps
-    int64_t u = 0;
+    int s = 0;
+    uint32_t ph = 0;
     int red_parity = 0;
     for (int c = 0; c < chunks; ++c) {
         const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
         const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
         const int64_t ce = TMA ? c0 + ((c1 - c0) & ~int64_t(1)) : c0;  // end of the TMA-copied columns
-        for (int64_t j = j0; j < j1; ++j) {
-            double2 acc[P];
+        int64_t j = j0;
+        int64_t e = offsets[j + 1];  // end (exclusive) of bucket j in perm order
+        double2 acc[P];
 #pragma unroll
-            for (int p = 0; p < P; ++p) acc[p] = make_double2(0.0, 0.0);
-            const int64_t e = offsets[j + 1];
-            for (int64_t t = offsets[j]; t < e; ++t, ++u) {
-                const int s = static_cast<int>(u % slots);
-                mbar_wait(&full[s], static_cast<uint32_t>((u / slots) & 1));
-                const int32_t pr = slot_row[s];
-                const bool neg = pr < 0;
-                const double2 *srow =
-                    reinterpret_cast<const double2 *>(ring + static_cast<size_t>(s) * slot_bytes);
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const int q = tid + tc * p;
-                    const int64_t col = c0 + 2 * static_cast<int64_t>(q);
-                    if (col + 1 < ce) {
-                        double2 v = srow[q];
-                        if (neg) { v.x = -v.x; v.y = -v.y; }
-                        acc[p].x = acc[p].x + v.x;
-                        acc[p].y = acc[p].y + v.y;
-                    } else if (col < c1) {  // columns not in the bulk copy: read directly
-                        const double *src = A + static_cast<int64_t>(pr & 0x7fffffff) * lda + col;
-                        double v = src[0];
-                        if (neg) v = -v;
-                        acc[p].x = acc[p].x + v;
-                        if (col + 1 < c1) {
-                            double w = src[1];
-                            if (neg) w = -w;
-                            acc[p].y = acc[p].y + w;
-                        }
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-            }
-            // epilogue: store the row of A~, fused squared norm (S4)
+        for (int q = 0; q < P; ++q) acc[q] = make_double2(0.0, 0.0);
+
+        // bucket epilogue: store the row of A~ and (fused S4) its squared norm
+        auto flush = [&](int64_t jj) {
             double part = 0.0;
-            double *dst = At + j * n;
+            double *dst = At + jj * n;
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const int q = tid + tc * p;
-                const int64_t col = c0 + 2 * static_cast<int64_t>(q);
+            for (int q = 0; q < P; ++q) {
+                const int qq = tid + tc * q;
+                const int64_t col = c0 + 2 * static_cast<int64_t>(qq);
                 if (col + 1 < c1) {
                     if ((n & 1) == 0) {
-                        *reinterpret_cast<double2 *>(dst + col) = acc[p];
+                        *reinterpret_cast<double2 *>(dst + col) = acc[q];
                     } else {
-                        dst[col] = acc[p].x;
-                        dst[col + 1] = acc[p].y;
+                        dst[col] = acc[q].x;
+                        dst[col + 1] = acc[q].y;
                     }
-                    part = __fma_rn(acc[p].x, acc[p].x, part);
-                    part = __fma_rn(acc[p].y, acc[p].y, part);
+                    part = __fma_rn(acc[q].x, acc[q].x, part);
+                    part = __fma_rn(acc[q].y, acc[q].y, part);
                 } else if (col < c1) {
-                    dst[col] = acc[p].x;
-                    part = __fma_rn(acc[p].x, acc[p].x, part);
+                    dst[col] = acc[q].x;
+                    part = __fma_rn(acc[q].x, acc[q].x, part);
                 }
+                acc[q] = make_double2(0.0, 0.0);
             }
             if (nsq != nullptr) {
                 part = warp_sum(part);
@@ -258,10 +258,79 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
                 if (tid == 0) {
                     double tot = red[red_parity * 8];
                     for (int w = 1; w < wc; ++w) tot = tot + red[red_parity * 8 + w];
-                    nsq[j] = (c == 0) ? tot : nsq[j] + tot;
+                    nsq[jj] = (c == 0) ? tot : nsq[jj] + tot;
                 }
                 red_parity ^= 1;
             }
+        };
+
+        int64_t t = t0;
+        // leading empty buckets
+        while (j < j1 && e == t) { flush(j); ++j; if (j < j1) e = offsets[j + 1]; }
+        for (int64_t u = 0; u < nst; ++u) {
+            const int cnt = static_cast<int>((t1 - t) < rb ? (t1 - t) : rb);
+            mbar_wait(&full[s], ph);
+            const int32_t *mrow = meta + s * kMaxRB;
+            const unsigned char *sbase = ring + static_cast<size_t>(s) * stage_bytes;
+            if (TMA && RB > 1 && cnt == RB && rb == RB && e - t >= RB && ce == c1) {
+                // fast path: full stage, no bucket boundary inside, every column in the copy:
+                // issue all loads of the stage, then fold them in row order
+                double2 v[RB][P];
+                uint64_t sg[RB];
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    sg[r] = mrow[r] < 0 ? 0x8000000000000000ULL : 0ULL;
+                    const double2 *srow = reinterpret_cast<const double2 *>(sbase + static_cast<size_t>(r) * slot_bytes);
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int qq = tid + tc * q;
+                        v[r][q] = (c0 + 2 * static_cast<int64_t>(qq) < c1) ? srow[qq] : make_double2(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        // sign flip = xor of the sign bit (exact, same bits as -v)
+                        acc[q].x = acc[q].x + __longlong_as_double(__double_as_longlong(v[r][q].x) ^ sg[r]);
+                        acc[q].y = acc[q].y + __longlong_as_double(__double_as_longlong(v[r][q].y) ^ sg[r]);
+                    }
+                }
+                t += RB;
+                while (j < j1 && e == t) { flush(j); ++j; if (j < j1) e = offsets[j + 1]; }
+            } else {
+            for (int r = 0; r < cnt; ++r, ++t) {
+                const int32_t pr = mrow[r];
+                const bool neg = pr < 0;
+                const double2 *srow = reinterpret_cast<const double2 *>(sbase + static_cast<size_t>(r) * slot_bytes);
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int qq = tid + tc * q;
+                    const int64_t col = c0 + 2 * static_cast<int64_t>(qq);
+                    if (col + 1 < ce) {
+                        double2 v = srow[qq];
+                        if (neg) { v.x = -v.x; v.y = -v.y; }
+                        acc[q].x = acc[q].x + v.x;
+                        acc[q].y = acc[q].y + v.y;
+                    } else if (col < c1) {  // columns not in the bulk copy: read directly
+                        const double *src = A + static_cast<int64_t>(pr & 0x7fffffff) * lda + col;
+                        double v = src[0];
+                        if (neg) v = -v;
+                        acc[q].x = acc[q].x + v;
+                        if (col + 1 < c1) {
+                            double w = src[1];
+                            if (neg) w = -w;
+                            acc[q].y = acc[q].y + w;
+                        }
+                    }
+                }
+                // bucket boundary after row t (and any empty buckets that follow)
+                while (j < j1 && e == t + 1) { flush(j); ++j; if (j < j1) e = offsets[j + 1]; }
+            }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == stages) { s = 0; ph ^= 1u; }
         }
     }
 }
@@ -368,32 +437,33 @@ __global__ void k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t 
 
 }  // namespace
 
-int norm_team_threads(int64_t n) { return dense_geom(n).tc; }
+int norm_team_threads(int64_t n) { return dense_geom(n, true).tc; }
 
 csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
                                  int64_t m, int64_t n, int64_t d, const int32_t *perm,
                                  const int32_t *offsets, double *At, double *bt, double *nsq,
                                  cudaStream_t stream) {
-    DenseGeom g = dense_geom(n);
+    const bool tma = aligned16(A) && (lda % 2 == 0);
+    const DenseGeom g = dense_geom(n, tma);
     int grid = ctx->num_sms;
     if (grid > d) grid = static_cast<int>(d);
     const int threads = g.tc + 64;
-    const bool tma = aligned16(A) && (lda % 2 == 0);
-    if (!tma) {  // no ring payload: only the slot metadata
-        g.slots = kMaxSlots;
-        g.slot_bytes = 0;
-        size_t header = static_cast<size_t>(g.slots) * 16 + static_cast<size_t>(g.slots) * 8 + 2 * 8 * 8;
-        g.smem = (header + 127) / 128 * 128;
-    }
     cudaError_t e = cudaSuccess;
-#define CSK_LAUNCH_DENSE(PP, T)                                                                      \
-    {                                                                                                \
-        e = cudaFuncSetAttribute(k_sketch_dense<PP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 static_cast<int>(g.smem));                                          \
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(k_sketch_dense)");       \
-        k_sketch_dense<PP, T><<<grid, threads, g.smem, stream>>>(A, lda, b, m, n, d, perm, offsets,  \
-                                                                 At, bt, nsq, g.tc, g.chunk_cols,    \
-                                                                 g.chunks, g.slot_bytes, g.slots);   \
+#define CSK_LAUNCH_DENSE_RB(PP, T, R)                                                                   \
+    {                                                                                                   \
+        e = cudaFuncSetAttribute(k_sketch_dense<PP, T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 static_cast<int>(g.smem));                                             \
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(k_sketch_dense)");          \
+        k_sketch_dense<PP, T, R><<<grid, threads, g.smem, stream>>>(                                    \
+            A, lda, b, m, n, d, perm, offsets, At, bt, nsq, g.tc, g.chunk_cols, g.chunks,               \
+            g.slot_bytes, g.rb, g.stages, static_cast<int>(g.header));                                  \
+    }
+#define CSK_LAUNCH_DENSE(PP, T)                                        \
+    {                                                                  \
+        if (T && g.rb == 2) CSK_LAUNCH_DENSE_RB(PP, T, 2)              \
+        else if (T && g.rb == 4) CSK_LAUNCH_DENSE_RB(PP, T, 4)         \
+        else if (T && g.rb >= 8) CSK_LAUNCH_DENSE_RB(PP, T, 8)         \
+        else CSK_LAUNCH_DENSE_RB(PP, T, 1)                             \
     }
     switch (g.p * 2 + (tma ? 1 : 0)) {
         case 3: CSK_LAUNCH_DENSE(1, true) break;
@@ -405,13 +475,14 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
         default: return fail(ctx, CSK_E_UNSUPPORTED, "sketch geometry");
     }
 #undef CSK_LAUNCH_DENSE
+#undef CSK_LAUNCH_DENSE_RB
     CSK_CUDA(ctx, cudaGetLastError());
     return CSK_OK;
 }
 
 csk_status_t launch_row_norms(csk_ctx_t ctx, const double *At, int64_t d, int64_t n, double *nsq,
                               cudaStream_t stream) {
-    const DenseGeom g = dense_geom(n);
+    const DenseGeom g = dense_geom(n, true);
     int64_t grid = d < int64_t(ctx->num_sms) * 8 ? d : int64_t(ctx->num_sms) * 8;
     switch (g.p) {
         case 1: k_row_norms<1><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
