@@ -202,6 +202,51 @@ CSK_API csk_status_t csk_run_host(csk_ctx_t ctx, const double *A_host, int64_t l
                           const double *x_star_host, double tol, int64_t max_iters,
                           csk_report_t *report, void *stream);
 
+/* ---- S9/S10: row-sharded multi-GPU path (one process per GPU, NCCL) --------------- */
+/* Bucket ownership: rank p of P owns rows [p c, min((p+1) c, total)) of A~, c = ceil(total/P)
+ * (equal blocks, as ncclReduceScatter requires).  Host-only, no GPU needed. */
+CSK_API csk_status_t csk_shard_range(int64_t total, int32_t nranks, int32_t rank, int64_t *lo,
+                                     int64_t *hi);
+
+/* NCCL bootstrap: rank 0 calls csk_comm_unique_id (128 host bytes), the caller broadcasts the
+ * bytes (e.g. torch.distributed), every rank calls csk_comm_create.  One comm per ctx. */
+CSK_API csk_status_t csk_comm_unique_id(void *uid_out);
+CSK_API csk_status_t csk_comm_create(csk_ctx_t ctx, const void *uid, int32_t nranks, int32_t rank);
+CSK_API csk_status_t csk_comm_destroy(csk_ctx_t ctx);
+
+/* S9 (north_star "NCCL reduce-scatter of partial A~ by bucket range"): this rank holds rows
+ * [row_offset, row_offset + m_local) of A (m rows in total) and hashes them with their GLOBAL
+ * indices, so the union over ranks is exactly S A.  On return this rank owns A~ rows
+ * [*d_lo, *d_hi) (csk_shard_range(d, P, rank)) in A_tilde_local ((d_hi-d_lo) x n), b~ rows in
+ * b_tilde_local and, if nsq_local != NULL, their squared norms.  Partial sums are combined by
+ * ncclReduceScatter(sum): A~ equals the P = 1 result up to summation order.
+ * Collective: every rank must call it.  Blocks only as NCCL does. */
+CSK_API csk_status_t csk_sketch_sharded(csk_ctx_t ctx, const double *A_local, int64_t lda,
+                                        const double *b_local, int64_t m_local, int64_t row_offset,
+                                        int64_t m, int64_t n, int64_t d, uint64_t seed,
+                                        double *A_tilde_local, double *b_tilde_local,
+                                        double *nsq_local, int64_t *d_lo, int64_t *d_hi,
+                                        void *stream);
+
+/* S10: Algorithm 1 with the rows of A~ sharded across ranks (rows [d_lo, d_hi) here) and x
+ * replicated.  Per iteration: local GEMV + argmax, one ncclAllGather of (score, global row,
+ * lambda, sum r^2, winning local row), identical winner/update on every rank (ties -> lowest
+ * global row).  Collective; blocks; fills *report (identical on every rank). */
+CSK_API csk_status_t csk_solve_sharded(csk_ctx_t ctx, const double *A_tilde_local,
+                                       const double *b_tilde_local, const double *nsq_local,
+                                       int64_t d_lo, int64_t d_hi, int64_t d, int64_t n, double *x,
+                                       const double *x_star, double tol, int64_t max_iters,
+                                       csk_report_t *report, void *stream);
+
+/* The same sharded loop with `nranks` virtual ranks on this one GPU (loopback exchange):
+ * A_tilde is the full d x n sketch, virtual rank p owns csk_shard_range(d, nranks, p).
+ * x_copies (optional, nranks x n) receives every virtual rank's final x (they must agree). */
+CSK_API csk_status_t csk_solve_virtual_ranks(csk_ctx_t ctx, const double *A_tilde,
+                                             const double *b_tilde, const double *nsq, int64_t d,
+                                             int64_t n, int32_t nranks, double *x,
+                                             const double *x_star, double tol, int64_t max_iters,
+                                             double *x_copies, csk_report_t *report, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,24 +93,21 @@ def _load():
 
 
 def _extend_sharded(lib):
-    P, i64, u64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+    P, i64, u64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double
+    pi64 = ctypes.POINTER(ctypes.c_int64)
     extra = {
+        "csk_shard_range": ([i64, i32, i32, pi64, pi64], i32),
         "csk_comm_unique_id": ([P], i32),
         "csk_comm_create": ([P, P, i32, i32], i32),
         "csk_comm_destroy": ([P], i32),
-        "csk_shard_range": ([i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
-        "csk_sketch_sharded": ([P, P, i64, P, i64, i64, i64, i64, i64, u64, P, P, P,
-                                ctypes.POINTER(i64), ctypes.POINTER(i64), P], i32),
-        "csk_solve_sharded": ([P, P, P, P, i64, i64, i64, i64, P, P, dbl, i64,
-                               ctypes.POINTER(Report), P], i32),
-        "csk_solve_virtual_ranks": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P,
-                                     ctypes.POINTER(Report), P], i32),
+        "csk_sketch_sharded": ([P, P, i64, P, i64, i64, i64, i64, i64, u64, P, P, P, pi64, pi64, P], i32),
+        "csk_solve_sharded": ([P, P, P, P, i64, i64, i64, i64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
+        "csk_solve_virtual_ranks": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P, ctypes.POINTER(Report), P], i32),
     }
     for name, (args, res) in extra.items():
-        if hasattr(lib, name):
-            fn = getattr(lib, name)
-            fn.argtypes = args
-            fn.restype = res
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
 
 
 lib = _load()
@@ -375,3 +372,84 @@ def csk_run_host(A, b, d: int, seed: int = 0, x0=None, x_star=None, tol: float =
                                seed & (2**64 - 1), _ptr(x), _ptr(x_star), float(tol), int(max_iters),
                                ctypes.byref(rep), _stream()))
     return x, rep
+
+
+# ------------------------------------------------------------------ S9/S10 sharded path
+NCCL_UID_BYTES = 128
+
+
+def shard_range(total: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Rows [lo, hi) of A~ owned by `rank` (equal ceil blocks; host-only)."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    st = lib.csk_shard_range(total, nranks, rank, ctypes.byref(lo), ctypes.byref(hi))
+    if st != CSK_OK:
+        raise CskError(st, "csk_shard_range: bad arguments")
+    return lo.value, hi.value
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0; the caller broadcasts the 128 bytes)."""
+    buf = ctypes.create_string_buffer(NCCL_UID_BYTES)
+    st = lib.csk_comm_unique_id(buf)
+    if st != CSK_OK:
+        raise CskError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def comm_create(uid: bytes, nranks: int, rank: int, ctx: Context | None = None):
+    ctx = ctx or default_context()
+    buf = ctypes.create_string_buffer(bytes(uid), NCCL_UID_BYTES)
+    ctx.check(lib.csk_comm_create(ctx.handle, buf, nranks, rank))
+
+
+def comm_destroy(ctx: Context | None = None):
+    ctx = ctx or default_context()
+    ctx.check(lib.csk_comm_destroy(ctx.handle))
+
+
+def csk_sketch_sharded(A_local, b_local, row_offset: int, m: int, d: int, nranks: int, rank: int,
+                       seed: int = 0, ctx: Context | None = None):
+    """S9: this rank's rows of (A, b) -> its bucket rows of (A~, b~, nsq) (NCCL reduce-scatter)."""
+    ctx = ctx or default_context()
+    _need(A_local, torch.float64, "A_local", 2)
+    _need(b_local, torch.float64, "b_local", 1)
+    ml, n = A_local.shape
+    lo, hi = shard_range(d, nranks, rank)
+    rows = max(hi - lo, 0)
+    At = torch.empty(max(rows, 1), n, dtype=torch.float64, device=A_local.device)
+    bt = torch.empty(max(rows, 1), dtype=torch.float64, device=A_local.device)
+    nsq = torch.empty(max(rows, 1), dtype=torch.float64, device=A_local.device)
+    dlo, dhi = ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(lib.csk_sketch_sharded(ctx.handle, _ptr(A_local), A_local.stride(0), _ptr(b_local.contiguous()),
+                                     ml, row_offset, m, n, d, seed & (2**64 - 1), _ptr(At), _ptr(bt), _ptr(nsq),
+                                     ctypes.byref(dlo), ctypes.byref(dhi), _stream()))
+    return At[:rows], bt[:rows], nsq[:rows], dlo.value, dhi.value
+
+
+def csk_solve_sharded(At_local, bt_local, nsq_local, d_lo: int, d_hi: int, d: int, n: int,
+                      x0=None, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
+                      ctx: Context | None = None):
+    """S10: Algorithm 1 loop with A~ rows sharded across ranks (x replicated)."""
+    ctx = ctx or default_context()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = torch.zeros(n, dtype=torch.float64, device=dev) if x0 is None else x0.clone().contiguous()
+    rep = Report()
+    ctx.check(lib.csk_solve_sharded(ctx.handle, _ptr(At_local.contiguous()), _ptr(bt_local.contiguous()),
+                                    _ptr(nsq_local.contiguous()), d_lo, d_hi, d, n, _ptr(x), _ptr(x_star),
+                                    float(tol), int(max_iters), ctypes.byref(rep), _stream()))
+    return x, rep
+
+
+def csk_solve_virtual_ranks(At, bt, nsq, nranks: int, x0=None, x_star=None, tol: float = 1e-6,
+                            max_iters: int = 50_000, ctx: Context | None = None):
+    """The sharded loop with `nranks` virtual ranks on this GPU (loopback exchange)."""
+    ctx = ctx or default_context()
+    At = At.contiguous()
+    d, n = At.shape
+    x = torch.zeros(n, dtype=torch.float64, device=At.device) if x0 is None else x0.clone().contiguous()
+    copies = torch.empty(nranks, n, dtype=torch.float64, device=At.device)
+    rep = Report()
+    ctx.check(lib.csk_solve_virtual_ranks(ctx.handle, _ptr(At), _ptr(bt.contiguous()), _ptr(nsq.contiguous()),
+                                          d, n, nranks, _ptr(x), _ptr(x_star), float(tol), int(max_iters),
+                                          _ptr(copies), ctypes.byref(rep), _stream()))
+    return x, copies, rep

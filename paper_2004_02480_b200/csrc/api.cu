@@ -39,6 +39,49 @@ csk_status_t ensure(csk_ctx_t ctx, Workspace &w, size_t bytes) {
     return CSK_OK;
 }
 
+csk_status_t raise_smem(csk_ctx_t ctx, const void *fn) {
+    if (ctx->smem_raised.count(fn)) return CSK_OK;
+    cudaFuncAttributes fa;
+    CSK_CUDA(ctx, cudaFuncGetAttributes(&fa, fn));
+    const int dyn = ctx->max_smem_optin - static_cast<int>(fa.sharedSizeBytes);
+    CSK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    CSK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    ctx->smem_raised.insert(fn);
+    return CSK_OK;
+}
+
+csk_status_t max_resident(csk_ctx_t ctx, const void *fn, int cs, int threads, size_t smem, int *out) {
+    const auto key = std::make_tuple(fn, cs, smem);
+    auto it = ctx->occ_cache.find(key);
+    if (it != ctx->occ_cache.end()) {
+        *out = it->second;
+        return CSK_OK;
+    }
+    CSK_CHECK(raise_smem(ctx, fn));
+    int v = 0;
+    if (cs > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CSK_CUDA(ctx, cudaOccupancyMaxActiveClusters(&v, fn, &cfg));
+    } else {
+        int per = 0;
+        CSK_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem));
+        v = per * ctx->num_sms;
+    }
+    ctx->occ_cache[key] = v;
+    *out = v;
+    return CSK_OK;
+}
+
 static void release(Workspace &w) {
     if (w.ptr) cudaFree(w.ptr);
     w.ptr = nullptr;

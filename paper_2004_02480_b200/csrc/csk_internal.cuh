@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "../../include/csk.h"
 
@@ -39,6 +42,11 @@ struct csk_ctx_s {
     bool pending = false;
     bool pending_resmode = false;
     int last_solve_geom[3] = {0, 0, 0};  // CTAs, cluster size, smem rows
+    // host-side memo of driver queries that would otherwise sit between short kernels
+    std::set<const void *> smem_raised;                              // kernels set to max dyn smem
+    std::map<std::tuple<const void *, int, size_t>, int> occ_cache;  // (fn, cluster, smem) -> n
+    int64_t cub_key_m = -1, cub_key_bits = -1;
+    size_t cub_bytes = 0;
 };
 
 namespace csk {
@@ -47,6 +55,10 @@ csk_status_t fail(csk_ctx_t ctx, csk_status_t st, const std::string &msg);
 csk_status_t cuda_fail(csk_ctx_t ctx, cudaError_t e, const char *what);
 // Grow-only device workspace.
 csk_status_t ensure(csk_ctx_t ctx, Workspace &w, size_t bytes);
+// Raise a kernel's dynamic shared-memory limit to the device opt-in maximum (once).
+csk_status_t raise_smem(csk_ctx_t ctx, const void *fn);
+// cudaOccupancyMaxActiveClusters (cs > 1) or blocks-per-SM x SMs (cs == 1), memoised.
+csk_status_t max_resident(csk_ctx_t ctx, const void *fn, int cs, int threads, size_t smem, int *out);
 
 #define CSK_CUDA(ctx, call)                                   \
     do {                                                      \

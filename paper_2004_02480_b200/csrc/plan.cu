@@ -99,9 +99,16 @@ csk_status_t build_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_
     int end_bit = 1;
     while ((int64_t(1) << end_bit) < d) ++end_bit;
     size_t tmp_bytes = 0;
-    CSK_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in,
-                                                  vals_out, static_cast<int>(m), 0, end_bit,
-                                                  stream));
+    if (ctx->cub_key_m == m && ctx->cub_key_bits == end_bit) {
+        tmp_bytes = ctx->cub_bytes;
+    } else {
+        CSK_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in,
+                                                      vals_out, static_cast<int>(m), 0, end_bit,
+                                                      stream));
+        ctx->cub_key_m = m;
+        ctx->cub_key_bits = end_bit;
+        ctx->cub_bytes = tmp_bytes;
+    }
     CSK_CHECK(ensure(ctx, ctx->cub_tmp, tmp_bytes));
     CSK_CUDA(ctx, cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.ptr, tmp_bytes, keys_in, keys_out,
                                                   vals_in, vals_out, static_cast<int>(m), 0,

@@ -448,12 +448,9 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
     int grid = ctx->num_sms;
     if (grid > d) grid = static_cast<int>(d);
     const int threads = g.tc + 64;
-    cudaError_t e = cudaSuccess;
 #define CSK_LAUNCH_DENSE_RB(PP, T, R)                                                                   \
     {                                                                                                   \
-        e = cudaFuncSetAttribute(k_sketch_dense<PP, T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 static_cast<int>(g.smem));                                             \
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(k_sketch_dense)");          \
+        CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_dense<PP, T, R>)));           \
         k_sketch_dense<PP, T, R><<<grid, threads, g.smem, stream>>>(                                    \
             A, lda, b, m, n, d, perm, offsets, At, bt, nsq, g.tc, g.chunk_cols, g.chunks,               \
             g.slot_bytes, g.rb, g.stages, static_cast<int>(g.header));                                  \
@@ -504,8 +501,7 @@ csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int3
     if (wpb > 16) wpb = 16;
     if (wpb < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
     const size_t smem = static_cast<size_t>(wpb) * stride * 8;
-    CSK_CUDA(ctx, cudaFuncSetAttribute(k_sketch_csr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+    CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_csr)));
     int64_t grid = (d + wpb - 1) / wpb;
     const int64_t cap = int64_t(ctx->num_sms) * 4;
     if (grid > cap) grid = cap;

@@ -30,6 +30,7 @@
 //       stay bit-identical and every CTA takes the same stop decision locally.
 //   S5  RES_k = ||x_k - x*||^2/||x*||^2 from register partials, or in residual
 //       mode ||r||^2/||b~||^2 from the exchanged partial sums.
+#include <stdlib.h>
 #include <string.h>
 
 #include "csk_internal.cuh"
@@ -776,7 +777,7 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     KernelFn fn = pick_kernel(n, resmode, P, wc);
     if (!fn) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n out of range");
     const int64_t npairs = (n + 1) / 2;
-    CSK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
 
     // ---- launch geometry: cluster size CS, number of clusters NC ----
     int CS = opts && opts->cluster_size > 0 ? opts->cluster_size : 0;
@@ -788,20 +789,7 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
         return static_cast<size_t>(ctx->max_smem_optin);
     };
     auto max_clusters = [&](int cs, size_t smem, int &out) -> csk_status_t {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cs;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(cs);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CSK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        CSK_CUDA(ctx, cudaOccupancyMaxActiveClusters(&out, reinterpret_cast<void *>(fn), &cfg));
-        return CSK_OK;
+        return max_resident(ctx, reinterpret_cast<const void *>(fn), cs, kThreads, smem, &out);
     };
     if (CS == 0) {
         // auto: the smallest number of 16-CTA clusters that keeps all of A~ on chip; if none
@@ -838,14 +826,8 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
         return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory (use more CTAs)");
 
     int per = 0;
-    if (CS > 1) {
-        CSK_CHECK(max_clusters(CS, smem, per));
-        if (per < NC) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: clusters cannot be co-resident");
-    } else {
-        CSK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        CSK_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem));
-        if (per * ctx->num_sms < G) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
-    }
+    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), CS, kThreads, smem, &per));
+    if (per < (CS > 1 ? NC : G)) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
 
     const size_t slot_bytes = static_cast<size_t>(2) * NC * NC * kSlotWords * 8;
     CSK_CHECK(ensure(ctx, ctx->slots, slot_bytes));
@@ -887,6 +869,11 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     cfg.stream = stream;
     cfg.attrs = at;
     cfg.numAttrs = CS > 1 ? 2 : 1;
+    // Profiling only: ncu cannot launch cooperative + cluster kernels, so CSK_PROFILE_NONCOOP=1
+    // launches the same kernel and geometry without the cooperative attribute (residency is
+    // still checked above against the occupancy API; the GPU must be otherwise idle).
+    static const bool noncoop = getenv("CSK_PROFILE_NONCOOP") != nullptr;
+    if (noncoop) { cfg.attrs = at + 1; cfg.numAttrs = CS > 1 ? 1 : 0; }
     CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, prm));
     ctx->last_solve_geom[0] = G;
     ctx->last_solve_geom[1] = CS;

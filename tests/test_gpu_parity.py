@@ -300,3 +300,46 @@ def test_C4_full_size_sampled(csk):
     g20 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=12, tol=1e-30, trace=13, trace_x=True)
     _lockstep(At, bt, nsq, g20.x_trace, g20.idx_trace, 12)
     assert np.array_equal(_np(g20.idx_trace), _np(g.idx_trace)[:12])
+
+
+# ---------------------------------------------------------------- CSR input (config C5)
+def _csr_np(p):
+    return _np(p.row_ptr), _np(p.col), _np(p.val), _np(p.b)
+
+
+@pytest.mark.parametrize("m,n,d,k", [(3000, 64, 300, 5), (20000, 2000, 1000, 10), (4001, 33, 777, 7)])
+def test_sketch_csr_bitexact(csk, m, n, d, k):
+    from csk_synth import make_csr
+    p = make_csr(m, n, k, seed=31 + m, device="cuda")
+    At, bt, nsq = csk.csk_sketch_csr(p.row_ptr, p.col, p.val, p.b, n, d, seed=5)
+    rp, col, val, b = _csr_np(p)
+    At_o, bt_o = oracle.sketch_csr(rp, col, val, b, n, d, seed=5)
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+    nsq_o = oracle.row_norms(At_o)
+    assert np.all(np.abs(_np(nsq) - nsq_o) <= 2 * n * U * nsq_o)
+
+
+def test_C5_full_size_sampled(csk):
+    """4e6 x 2000 CSR (4e7 nnz): sampled buckets against the oracle's fold of exactly those
+    rows; the first iterations in lockstep against the oracle's residual."""
+    cfg = CONFIGS["C5"]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = csk.csk_sketch_csr(p.row_ptr, p.col, p.val, p.b, cfg.n, cfg.d, seed=cfg.sketch_seed)
+    torch.cuda.synchronize()
+    h, s = oracle.hash_map(cfg.sketch_seed, cfg.m, cfg.d)
+    rp = _np(p.row_ptr)
+    rng = np.random.default_rng(1)
+    for j in rng.choice(cfg.d, 16, replace=False).tolist() + [0, cfg.d - 1]:
+        rows = np.nonzero(h == j)[0]
+        if not len(rows):
+            assert not _np(At[j]).any() and _np(bt[j]) == 0.0
+            continue
+        sub_rp = np.concatenate([[0], np.cumsum(rp[rows + 1] - rp[rows])]).astype(np.int64)
+        idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
+        cols = _np(p.col[torch.as_tensor(idx, device="cuda")])
+        vals = _np(p.val[torch.as_tensor(idx, device="cuda")])
+        bs = _np(p.b[torch.as_tensor(rows, device="cuda")])
+        a1, b1 = oracle.sketch_csr(sub_rp, cols, vals, bs, cfg.n, 1, h=np.zeros(len(rows), np.int32), s=s[rows])
+        assert np.array_equal(_np(At[j]), a1[0]) and _np(bt[j]) == b1[0]
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=6, tol=1e-30, trace=7, trace_x=True)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6)
