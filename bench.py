@@ -10,9 +10,9 @@ is flushed by writing a 256 MiB buffer (untimed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
-N > 1 (torchrun): each rank solves its own independent C-config problem (weak
-scaling, no data-path collective) -- the sharded single-problem path is measured
-separately.
+N > 1 (torchrun): ONE problem, row-sharded across the ranks (strong scaling): the sketch
+with csk_sketch_sharded (NCCL reduce-scatter of partial A~ by bucket range, S9) and the loop
+with csk_solve_sharded (per-iteration NCCL all-gather max-loc + winning row, S10).
 """
 from __future__ import annotations
 
@@ -393,6 +393,83 @@ def run_reference(args):
             "iterations": r.iterations, "vs_baseline": None}
 
 
+def run_sharded(args, dist, rank, ws):
+    """N > 1: the same workload, sharded (S9/S10); CUDA events, max over ranks."""
+    import paper_2004_02480_b200 as csk
+    from paper_2004_02480_b200.parallel import init_comm, row_shard
+
+    cfg = CONFIGS[args.config]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p = make_config(cfg, dev)                    # every rank draws the same problem ...
+    lo, hi = row_shard(cfg.m, ws, rank)          # ... and keeps its contiguous row shard
+    A_loc = p.A[lo:hi].contiguous()
+    b_loc = p.b[lo:hi].contiguous()
+    xs = p.x_star
+    del p
+    torch.cuda.empty_cache()
+    ctx = csk.Context()
+    init_comm(ctx)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(st)
+        At, bt, nsq, dlo, dhi = csk.csk_sketch_sharded(A_loc, b_loc, lo, cfg.m, cfg.d, ws, rank,
+                                                       seed=cfg.sketch_seed, ctx=ctx)
+        if ev:
+            ev[1].record(st)
+        x, rep = csk.csk_solve_sharded(At, bt, nsq, dlo, dhi, cfg.d, cfg.n, x_star=xs, tol=cfg.tol,
+                                       max_iters=cfg.max_iters, ctx=ctx)
+        if ev:
+            ev[2].record(st)
+        return rep
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    reps = []
+    _barrier(dist)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(1.0)
+        reps.append(step(evs[k]))
+    torch.cuda.synchronize()
+    _barrier(dist)
+    t1 = time.perf_counter()
+    sampler.stop()
+    sk = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    sv = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    ms = _max_over_ranks(dist, sk + sv)
+    sk = _max_over_ranks(dist, sk)
+    sv = _max_over_ranks(dist, sv)
+    it = reps[-1].iterations
+    out = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (torch Philox, PAPER.md:180 recipe; csk_synth.py)",
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "kind": cfg.kind,
+                   "tol": cfg.tol, "max_iters": cfg.max_iters, "parallelism": f"row-sharded x{ws} (NCCL)",
+                   "l2": "flushed between steps (256 MiB write, untimed)"},
+        "iterations": it, "final_res": reps[-1].final_res,
+        "termination": ["converged", "max_iters", "stagnated"][reps[-1].termination],
+        "iterations_per_s": round(it / (sv * 1e-3), 1), "sketch_ms": round(sk, 5), "solve_ms": round(sv, 4),
+        "sketch_hbm_gbs": round(alg_bytes_sketch(cfg) / (sk * 1e-3) / 1e9, 1),
+        "clocks": sampler.summary(t0, t1),
+        "gpu_launches": args.steps * (4 + 3 * ((it // 16) + 1) * 16),
+        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_row_norms + per iteration "
+                             "k_shard_candidate, k_shard_apply (+ NCCL kernels)",
+    }
+    csk.comm_destroy(ctx)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -413,7 +490,7 @@ def main():
         print(json.dumps(run_reference(args)))
         return
     dist, rank, ws, _ = _dist()
-    out = run_ours(args, dist, rank, ws)
+    out = run_ours(args, dist, rank, ws) if ws == 1 else run_sharded(args, dist, rank, ws)
     if rank == 0:
         print(json.dumps(out))
     if dist is not None:
