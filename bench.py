@@ -139,6 +139,21 @@ def _max_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
+def _ncu_traffic(name: str):
+    """dram read+write bytes per launch from a committed ncu summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.split()
+            if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[parts[2]]
+                vals[parts[0]] = float(parts[1].replace(",", "")) * scale
+        return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
+    except Exception:
+        return None
+
+
 def alg_bytes_sketch(cfg) -> int:
     """8mn + 8m + 8dn + 8d (A, b read; A~, b~ written) + 8d (nsq)."""
     return 8 * cfg.m * cfg.n + 8 * cfg.m + 8 * cfg.d * cfg.n + 16 * cfg.d
@@ -241,13 +256,16 @@ def run_ours(args, dist, rank, ws):
         "roofline": {"kernel": "k_solve (persistent loop)", "bound": "smem",
                      "achieved": round(loop_gbs, 1),
                      "peak": round(smem_peak, 1), "unit": "GB/s", "frac": round(loop_gbs / smem_peak, 4),
-                     "traffic": None,
+                     "traffic": _ncu_traffic(f"r01_ncu_solve_{cfg.name}.txt"),
+                     "traffic_note": "DRAM bytes of the whole k_solve launch (one launch = the whole loop): "
+                                     "A~ is read once into shared memory and stays on chip",
                      "peak_source": f"derived: 148 SM x {SMEM_BYTES_PER_CLK_PER_SM} B/clk x {sm_max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                      "alg_bytes_per_iteration": alg_bytes_iter(cfg)},
         "roofline_sketch": {"kernel": "plan + k_sketch_dense", "bound": "hbm",
                             "achieved": round(sketch_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                             "frac": round(sketch_gbs / hbm_peak, 4), "peak_source": peak_src,
-                            "alg_bytes": alg_bytes_sketch(cfg)},
+                            "alg_bytes": alg_bytes_sketch(cfg),
+                            "traffic": _ncu_traffic(f"r01_ncu_sketch_{cfg.name}.txt")},
         "clocks": clocks,
         "gpu_launches": 4 * args.steps,
         "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_solve (+ CUB onesweep radix-sort kernels and one memset)",
