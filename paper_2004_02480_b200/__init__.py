@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcsk.so")
+# CSK_LIB=prof selects the debug build with the in-kernel phase profiler (tools/phase_probe.py)
+LIB_PATH = os.path.join(_PKG, "libcsk_prof.so" if os.environ.get("CSK_LIB") == "prof" else "libcsk.so")
 
 CSK_OK, CSK_E_ARG, CSK_E_ZERO_SKETCH, CSK_E_UNSUPPORTED, CSK_E_CUDA, CSK_E_NCCL, CSK_E_NOMEM = range(7)
 CONVERGED, MAX_ITERS, STAGNATED = 0, 1, 2

@@ -41,6 +41,8 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
+constexpr int kMaxW = 16;  // max warps of any variant (sizes cand[] in the layout)
+constexpr int kResW = 8;   // warps of the resident-only variant
 constexpr int kMaxSlotsPerLane = 5;  // NC <= 160 cluster leaders
 constexpr int kMaxNC = 32 * kMaxSlotsPerLane;
 constexpr int kMaxCS = 16;
@@ -115,6 +117,25 @@ __device__ __forceinline__ Pay warp_combine(Pay v, bool sum_rr) {
     warp_argmax(v.s, v.i, v.l);
     if (sum_rr) v.rr = warp_sum(v.rr);
     return v;
+}
+
+// Monotone 64-bit key of a score: finite scores >= 0 map to bits + 1 (order-preserving for
+// non-negative doubles), masked (-1) / empty (-2) candidates to 0.
+__device__ __forceinline__ uint64_t score_key(double s) {
+    return s >= 0.0 ? static_cast<uint64_t>(__double_as_longlong(s)) + 1ull : 0ull;
+}
+__device__ __forceinline__ uint32_t idx32(int64_t i) {
+    return i == INT64_MAX ? 0xffffffffu : static_cast<uint32_t>(i);
+}
+// Lane holding the (largest key, smallest index) of the warp -- the same total order as
+// better() -- in three redux.sync reductions and a ballot instead of a 5-step butterfly.
+__device__ __forceinline__ int warp_argmax_lane(uint64_t key, uint32_t idx) {
+    const uint32_t kh = static_cast<uint32_t>(key >> 32), kl = static_cast<uint32_t>(key);
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, kh);
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, kh == hi ? kl : 0u);
+    const bool top = kh == hi && kl == lo;
+    const uint32_t mi = __reduce_min_sync(0xffffffffu, top ? idx : 0xffffffffu);
+    return __ffs(__ballot_sync(0xffffffffu, top && idx == mi)) - 1;
 }
 
 __device__ __forceinline__ uint64_t pack(uint32_t data, uint32_t tag) {
@@ -203,8 +224,9 @@ __device__ __forceinline__ int owner_cta(int64_t i, int64_t d, int G) {
     return c;
 }
 
-template <int P, bool EVEN, bool RESMODE>
-__global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
+template <int P, bool EVEN, bool RESMODE, bool STREAM, int W>
+__global__ void __launch_bounds__(W * 32, 1) k_solve(const SolveParams p) {
+    constexpr int kT = W * 32;
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -224,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
     // streamed rows: column-lane GEMV (coalesced) + transposed shuffle reduction
     const int nst = rows - srows;
     const int gt = (nst + 31) >> 5;
-    const int Wc = p.wc, Wr = kWarps / Wc;
+    const int Wc = p.wc, Wr = W / Wc;
     const int cw = warp % Wc, team = warp / Wc;
     const int64_t xpad = (npairs > static_cast<int64_t>(Wc) * 32 * P) ? npairs : static_cast<int64_t>(Wc) * 32 * P;
     const double gd = static_cast<double>(G) / static_cast<double>(d);
@@ -243,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
     double *bt_loc = part_s + static_cast<size_t>(gt_u) * Wc * 32;     // [rows]
     double *nsq_loc = bt_loc + rows_u;                                 // [rows]
     Cand *cand = reinterpret_cast<Cand *>(nsq_loc + rows_u);            // [8] (16-byte aligned)
-    volatile int64_t *win = reinterpret_cast<volatile int64_t *>(cand + kWarps);  // [8]
-    double *resp = reinterpret_cast<double *>(cand + kWarps) + 8;      // [32] RES lane partials
+    volatile int64_t *win = reinterpret_cast<volatile int64_t *>(cand + W);  // [8]
+    double *resp = reinterpret_cast<double *>(cand + W) + 8;      // [32] RES lane partials
     double *xs_nrm_s = resp + 32;                                      // [2]
     int32_t *r0tab = reinterpret_cast<int32_t *>(xs_nrm_s + 2);       // [G+1] first row of each CTA
     double2 *arows = reinterpret_cast<double2 *>(r0tab + kMaxTab);     // [srows][sstride]
@@ -256,9 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
         const size_t need = reinterpret_cast<unsigned char *>(arows + static_cast<int64_t>(srows_u) * sstride) - smem;
         if (need > dyn) __trap();
     }
-    for (int e = tid; e < 2 * kMaxCS * kSlotWords + 2 * kSlotWords; e += kThreads) l1[e] = 0;
-    for (int c = tid; c <= G; c += kThreads) r0tab[c] = static_cast<int32_t>(d * c / G);
-    for (int64_t e = tid; e < static_cast<int64_t>(srows) * npairs; e += kThreads) {
+    for (int e = tid; e < 2 * kMaxCS * kSlotWords + 2 * kSlotWords; e += kT) l1[e] = 0;
+    for (int c = tid; c <= G; c += kT) r0tab[c] = static_cast<int32_t>(d * c / G);
+    for (int64_t e = tid; e < static_cast<int64_t>(srows) * npairs; e += kT) {
         const int64_t l = e / npairs, q = e - l * npairs;
         const double *src = p.At + (r0 + l) * n;
         double2 v;
@@ -270,11 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
         }
         arows[l * sstride + q] = v;
     }
-    for (int l = tid; l < rows; l += kThreads) {
+    for (int l = tid; l < rows; l += kT) {
         bt_loc[l] = p.bt[r0 + l];
         nsq_loc[l] = p.nsq[r0 + l];
     }
-    for (int64_t q = tid; q < xpad; q += kThreads) {
+    for (int64_t q = tid; q < xpad; q += kT) {
         double2 v = make_double2(0.0, 0.0), w = make_double2(0.0, 0.0);
         if (q < npairs) {
             v.x = p.x[2 * q];
@@ -324,15 +346,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
     if (CS > 1) cluster_sync_all();  // every CTA's slots are zeroed before any remote write
     else __syncthreads();
 
+#if CSK_PHASE_PROF
+    // debug build only (libcsk_prof.so): per-phase SM-cycle totals of CTA 0, warps 0 and 1
     const bool prof = p.phase_cycles != nullptr && cta == 0 && lane == 0 && warp < 2;
-    int64_t ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long tp = clock64();
+    int64_t ph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64(), tf = tp;
 #define CSK_PHASE(i)                    \
     if (prof) {                         \
         const long long tn = clock64(); \
         ph[i] += tn - tp;               \
         tp = tn;                        \
+        tf = tn;                        \
     }
+// fine-grained points inside warp 0's exchange (no barriers in between: exact)
+#define CSK_FINE(i)                     \
+    if (prof) {                         \
+        const long long tn = clock64(); \
+        ph[8 + (i)] += tn - tf;         \
+        tf = tn;                        \
+    }
+#else
+#define CSK_PHASE(i)
+#define CSK_FINE(i)
+#endif
 
     if (win[2] != -1) {
         term = static_cast<int>(win[2]);
@@ -350,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
 
             // ---- S5 (deferred): RES_k from warp 0's lane partials of the last update; the
             //      test result is read by warp 0 after B1 (warp 7 is off the critical path) ----
-            if (!RESMODE && warp == kWarps - 1 && k > 0) {
+            if (!RESMODE && warp == W - 1 && k > 0) {
                 const double e2 = warp_sum(resp[lane]);
                 const double rk = xs_nrm_s[0] > 0.0 ? e2 / xs_nrm_s[0] : e2;
                 int st = -1;
@@ -364,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
             }
 
             // ---- S6a: resident rows, lane-per-row, work items (group, chunk) over warps ----
-            for (int it = warp; it < gs * Wk; it += kWarps) {
+            for (int it = warp; it < gs * Wk; it += W) {
                 const int g = it / Wk, kc = it - g * Wk;
                 const int l = g * 32 + lane;
                 const int64_t q0 = kc * chunk;
@@ -390,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                 part_r[static_cast<size_t>(it) * 32 + lane] = a0 + a1;
             }
             // ---- S6b: streamed rows (L2/HBM), column-lane mapping ----
-            for (int g = team; g < gt; g += Wr) {
+            if constexpr (STREAM) for (int g = team; g < gt; g += Wr) {
                 double2 xr[P];
 #pragma unroll
                 for (int j = 0; j < P; ++j) xr[j] = xsm[static_cast<int64_t>(cw) * 32 * P + lane + 32 * j];
@@ -436,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
             if (!small || warp == 0) {
                 double bs = -2.0, bl = 0.0, rr = 0.0;
                 int64_t bi = INT64_MAX;
-                const int step = small ? 32 : kThreads;
+                const int step = small ? 32 : kT;
                 for (int l = small ? lane : tid; l - lane < rows; l += step) {
                     if (l < rows) {
                         double dot;
@@ -459,7 +495,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                     }
                 }
                 if (RESMODE) rr = warp_sum(rr);
-                warp_argmax(bs, bi, bl);
+                {
+                    const int wl = warp_argmax_lane(score_key(bs), idx32(bi));
+                    bs = __shfl_sync(0xffffffffu, bs, wl);
+                    bi = __shfl_sync(0xffffffffu, bi, wl);
+                    bl = __shfl_sync(0xffffffffu, bl, wl);
+                }
                 if (lane == 0) cand[warp] = Cand{bs, bl, rr, bi};
             }
             if (!small) __syncthreads();  // B1b
@@ -478,30 +519,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                     cv.s = cand[0].score; cv.l = cand[0].r; cv.i = cand[0].idx;
                     if (RESMODE) cv.rr = cand[0].rr;
                 } else {
-                    if (lane < kWarps) { cv.s = cand[lane].score; cv.l = cand[lane].r; cv.i = cand[lane].idx; }
-#pragma unroll
-                    for (int o = 4; o > 0; o >>= 1) {
-                        const double os = __shfl_xor_sync(0xffffffffu, cv.s, o);
-                        const int64_t oi = __shfl_xor_sync(0xffffffffu, cv.i, o);
-                        const double ol = __shfl_xor_sync(0xffffffffu, cv.l, o);
-                        if (better(os, oi, cv.s, cv.i)) { cv.s = os; cv.i = oi; cv.l = ol; }
-                    }
-                    cv.s = __shfl_sync(0xffffffffu, cv.s, 0);
-                    cv.i = __shfl_sync(0xffffffffu, cv.i, 0);
-                    cv.l = __shfl_sync(0xffffffffu, cv.l, 0);
+                    if (lane < W) { cv.s = cand[lane].score; cv.l = cand[lane].r; cv.i = cand[lane].idx; }
+                    const int wl = warp_argmax_lane(score_key(cv.s), idx32(cv.i));
+                    cv.s = __shfl_sync(0xffffffffu, cv.s, wl);
+                    cv.i = __shfl_sync(0xffffffffu, cv.i, wl);
+                    cv.l = __shfl_sync(0xffffffffu, cv.l, wl);
                     if (RESMODE) {
-                        for (int w = 0; w < kWarps; ++w) cv.rr = cv.rr + cand[w].rr;  // fixed order
+                        for (int w = 0; w < W; ++w) cv.rr = cv.rr + cand[w].rr;  // fixed order
                     }
                 }
                 const uint32_t tag = static_cast<uint32_t>(k + 1);
                 const int par = static_cast<int>(k & 1);
                 uint64_t w[8];
+                CSK_FINE(0)
                 // hop 2: cluster all-to-all over DSMEM (lane r -> rank r), combine 16 lanes
                 Pay cl = cv;
                 if (CS > 1) {
                     encode(cv, tag, w);
                     const uint32_t my_slot = smem_u32(l1 + (par * kMaxCS + rank) * kSlotWords);
                     if (lane < CS) st_dsmem_slot(mapa_shared(my_slot, static_cast<uint32_t>(lane)), w);
+                    CSK_FINE(1)
                     Pay got{-2.0, 0.0, 0.0, INT64_MAX};
                     bool ok = lane >= CS;
                     const uint32_t rd = smem_u32(l1 + (par * kMaxCS + (lane < CS ? lane : 0)) * kSlotWords);
@@ -512,17 +549,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                             ok = decode(r8, tag, got);
                         }
                     }
+                    CSK_FINE(2)
+                    if (RESMODE) {
 #pragma unroll
-                    for (int o = 8; o > 0; o >>= 1) {
-                        const double os = __shfl_xor_sync(0xffffffffu, got.s, o);
-                        const int64_t oi = __shfl_xor_sync(0xffffffffu, got.i, o);
-                        const double ol = __shfl_xor_sync(0xffffffffu, got.l, o);
-                        if (RESMODE) got.rr = got.rr + __shfl_xor_sync(0xffffffffu, got.rr, o);
-                        if (better(os, oi, got.s, got.i)) { got.s = os; got.i = oi; got.l = ol; }
+                        for (int o = 8; o > 0; o >>= 1) got.rr = got.rr + __shfl_xor_sync(0xffffffffu, got.rr, o);
                     }
-                    cl.s = __shfl_sync(0xffffffffu, got.s, 0);
-                    cl.i = __shfl_sync(0xffffffffu, got.i, 0);
-                    cl.l = __shfl_sync(0xffffffffu, got.l, 0);
+                    const int wl = warp_argmax_lane(score_key(got.s), idx32(got.i));
+                    cl.s = __shfl_sync(0xffffffffu, got.s, wl);
+                    cl.i = __shfl_sync(0xffffffffu, got.i, wl);
+                    cl.l = __shfl_sync(0xffffffffu, got.l, wl);
                     cl.rr = __shfl_sync(0xffffffffu, got.rr, 0);
                 }
                 CSK_PHASE(3)
@@ -537,6 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                             const int rdr = lane + 32 * j;
                             if (rdr < NC) st_global_slot(gpar + (static_cast<size_t>(rdr) * NC + clus) * kSlotWords, w);
                         }
+                        CSK_FINE(3)
                         const uint64_t *inbox = gpar + static_cast<size_t>(clus) * NC * kSlotWords;
                         Pay g[kMaxSlotsPerLane];
                         uint32_t pending = 0;
@@ -556,13 +592,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                             }
                             if (__all_sync(0xffffffffu, pending == 0)) break;
                         }
+                        CSK_FINE(4)
                         Pay acc{-2.0, 0.0, 0.0, INT64_MAX};
 #pragma unroll
                         for (int j = 0; j < kMaxSlotsPerLane; ++j) {
                             if (better(g[j].s, g[j].i, acc.s, acc.i)) { acc.s = g[j].s; acc.i = g[j].i; acc.l = g[j].l; }
                             if (RESMODE) acc.rr = acc.rr + g[j].rr;
                         }
-                        wv = warp_combine(acc, RESMODE);
+                        if (RESMODE) acc.rr = warp_sum(acc.rr);
+                        {
+                            const int wl = warp_argmax_lane(score_key(acc.s), idx32(acc.i));
+                            wv.s = __shfl_sync(0xffffffffu, acc.s, wl);
+                            wv.i = __shfl_sync(0xffffffffu, acc.i, wl);
+                            wv.l = __shfl_sync(0xffffffffu, acc.l, wl);
+                            wv.rr = acc.rr;
+                        }
                         if (CS > 1) {
                             encode(wv, tag, w);
                             const uint32_t rslot = smem_u32(rs + par * kSlotWords);
@@ -578,6 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                             ok = decode(r8, tag, got);
                         }
                         wv = got;
+                        CSK_FINE(5)
                     }
                 }
                 CSK_PHASE(4)
@@ -608,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                     const double *gsrc = p.At + wv.i * n;
                     // loads in blocks of 8 independent pairs per lane (one round trip each), then the update
                     double e2 = 0.0;
+                    CSK_FINE(6)
                     for (int64_t qb = 0; qb < npairs; qb += 8 * 32) {
                         double2 av[8];
 #pragma unroll
@@ -633,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
                             }
                         }
                     }
+                    CSK_FINE(7)
                     applied = 1;
                     last = wv.i;
                     if (!RESMODE) resp[lane] = e2;  // reduced by warp 7 next iteration (S5)
@@ -661,14 +708,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(const SolveParams p) {
         }
     }
 #undef CSK_PHASE
+#undef CSK_FINE
+#if CSK_PHASE_PROF
     if (prof) {
-        for (int i = 0; i < 8; ++i) p.phase_cycles[warp * 8 + i] = ph[i];
+        for (int i = 0; i < 16; ++i) p.phase_cycles[warp * 16 + i] = ph[i];
     }
+#endif
 
     // ---- epilogue: CTA 0 writes x (and the trace of the final iterate); thread 0 the report ----
     if (cta == 0) {
         const bool tr = p.x_trace && k < p.trace_cap;
-        for (int64_t q = tid; q < npairs; q += kThreads) {
+        for (int64_t q = tid; q < npairs; q += kT) {
             const double2 x = xsm[q];
             p.x[2 * q] = x.x;
             if (2 * q + 1 < n) p.x[2 * q + 1] = x.y;
@@ -705,14 +755,21 @@ __global__ void k_sumsq(const double *v, int64_t len, double *out) {
 
 using KernelFn = void (*)(const SolveParams);
 
+// STREAM = some rows are re-read from L2/HBM (8 warps, the column-lane GEMV compiled in);
+// otherwise every row is resident and the lighter kernel runs 16 warps for latency hiding.
 template <int P>
-KernelFn pick_mode(bool even, bool resmode) {
-    if (even) return resmode ? k_solve<P, true, true> : k_solve<P, true, false>;
-    return resmode ? k_solve<P, false, true> : k_solve<P, false, false>;
+KernelFn pick_mode(bool even, bool resmode, bool stream) {
+    if (stream) {
+        if (even) return resmode ? k_solve<P, true, true, true, 8> : k_solve<P, true, false, true, 8>;
+        return resmode ? k_solve<P, false, true, true, 8> : k_solve<P, false, false, true, 8>;
+    }
+    if (even) return resmode ? k_solve<P, true, true, false, kResW> : k_solve<P, true, false, false, kResW>;
+    return resmode ? k_solve<P, false, true, false, kResW> : k_solve<P, false, false, false, kResW>;
 }
 
-// P = column pairs per lane (power of two), Wc = column warps (power of two <= 8).
-KernelFn pick_kernel(int64_t n, bool resmode, int &P, int &wc) {
+// P = column pairs per lane (power of two), Wc = column warps (power of two <= 8) of the
+// streamed-row GEMV.
+KernelFn pick_kernel(int64_t n, bool resmode, bool stream, int &P, int &wc) {
     const int64_t npairs = (n + 1) / 2;
     P = 1;
     while (32 * kWarps * P < npairs) P *= 2;
@@ -720,9 +777,9 @@ KernelFn pick_kernel(int64_t n, bool resmode, int &P, int &wc) {
     while (wc < kWarps && 32 * P * wc < npairs) wc *= 2;
     const bool even = (n & 1) == 0;
     switch (P) {
-        case 1: return pick_mode<1>(even, resmode);
-        case 2: return pick_mode<2>(even, resmode);
-        case 4: return pick_mode<4>(even, resmode);
+        case 1: return pick_mode<1>(even, resmode, stream);
+        case 2: return pick_mode<2>(even, resmode, stream);
+        case 4: return pick_mode<4>(even, resmode, stream);
         default: return nullptr;
     }
 }
@@ -734,28 +791,28 @@ size_t smem_layout(int64_t rows_max, int64_t srows, int64_t npairs, int64_t wc, 
     return static_cast<size_t>(2 * kMaxCS * kSlotWords + 2 * kSlotWords) * 8 +  // slots
            static_cast<size_t>(2 * xpad) * 16 +                                // x, x*
            static_cast<size_t>(gs * wk + gt * wc) * 32 * 8 +                   // partials
-           static_cast<size_t>(rows_max) * 16 + kWarps * sizeof(Cand) +        // b~, nsq, cand
+           static_cast<size_t>(rows_max) * 16 + kMaxW * sizeof(Cand) +         // b~, nsq, cand
            8 * 8 + 32 * 8 + 2 * 8 + kMaxTab * 4 +                              // win, resp, xs_nrm, r0tab
            static_cast<size_t>(srows) * (npairs | 1) * 16 + 64;                // resident rows
 }
 
 // Column chunks for the resident-row GEMV: enough (group, chunk) items to occupy the 8
 // warps, chunks of at least 8 pairs.
-int pick_wk(int64_t rows_res, int64_t npairs);
+int pick_wk(int64_t rows_res, int64_t npairs, int warps = kMaxW);
 // Largest number of resident rows whose layout fits `cap` bytes.
 int64_t fit_srows(int64_t rows_max, int64_t npairs, int64_t wc, int64_t P, size_t cap) {
     int64_t lo = 0, hi = rows_max;
     while (lo < hi) {
         const int64_t mid = (lo + hi + 1) / 2;
-        if (smem_layout(rows_max, mid, npairs, wc, P, pick_wk(mid, npairs)) <= cap) lo = mid; else hi = mid - 1;
+        if (smem_layout(rows_max, mid, npairs, wc, P, pick_wk(mid, npairs, kMaxW)) <= cap) lo = mid; else hi = mid - 1;
     }
     return lo;
 }
 
-int pick_wk(int64_t rows_res, int64_t npairs) {
+int pick_wk(int64_t rows_res, int64_t npairs, int warps) {
     const int64_t groups = (rows_res + 31) / 32;
     int wk = 1;
-    while (wk < kWarps && groups * wk < kWarps && npairs / (2 * wk) >= 8) wk *= 2;
+    while (wk < warps && groups * wk < warps && npairs / (2 * wk) >= 8) wk *= 2;
     return wk;
 }
 
@@ -774,7 +831,7 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     if (ctx->pending) return fail(ctx, CSK_E_ARG, "csk_solve: a CSK_SOLVE_ASYNC solve is still in flight (call csk_solve_wait)");
     const bool resmode = (x_star == nullptr);
     int P = 0, wc = 0;
-    KernelFn fn = pick_kernel(n, resmode, P, wc);
+    KernelFn fn = pick_kernel(n, resmode, true, P, wc);  // geometry probe (8-warp variant)
     if (!fn) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n out of range");
     const int64_t npairs = (n + 1) / 2;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
@@ -820,13 +877,16 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     int64_t srows = fit_srows(rows_max, npairs, wc, P, static_cast<size_t>(ctx->max_smem_optin));
     if (opts && opts->smem_rows > 0 && opts->smem_rows < srows) srows = opts->smem_rows;
     if (opts && opts->smem_rows < 0) srows = 0;
-    const int wk = pick_wk(srows, npairs);
+    const bool streamed = srows < rows_max;
+    const int W = streamed ? kWarps : kResW;
+    fn = pick_kernel(n, resmode, streamed, P, wc);
+    const int wk = pick_wk(srows, npairs, W);
     const size_t smem = smem_layout(rows_max, srows, npairs, wc, P, wk);
     if (smem > static_cast<size_t>(ctx->max_smem_optin))
         return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory (use more CTAs)");
 
     int per = 0;
-    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), CS, kThreads, smem, &per));
+    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), CS, W * 32, smem, &per));
     if (per < (CS > 1 ? NC : G)) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
 
     const size_t slot_bytes = static_cast<size_t>(2) * NC * NC * kSlotWords * 8;
@@ -864,7 +924,7 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(W * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cfg.attrs = at;

@@ -9,6 +9,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+os.environ.setdefault("CSK_LIB", "prof")  # the phase profiler lives in libcsk_prof.so
 import torch  # noqa: E402
 
 import paper_2004_02480_b200 as csk  # noqa: E402
@@ -36,7 +37,7 @@ def main():
         for G in ctas:
           for cs in css:
             for sm in smem_modes:
-                ph = torch.zeros(16, dtype=torch.int64, device="cuda")
+                ph = torch.zeros(32, dtype=torch.int64, device="cuda")
                 csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, smem_rows=sm, cluster_size=cs)
                 st = torch.cuda.Event(enable_timing=True)
                 en = torch.cuda.Event(enable_timing=True)
@@ -50,7 +51,9 @@ def main():
                 it = max(r.iterations, 1)
                 c = ph.cpu().tolist()
                 w0 = " ".join(f"{names_ph[i]}={c[i] / it / 1965:.2f}" for i in range(8))
-                w1 = " ".join(f"{names_ph[i]}={c[8 + i] / it / 1965:.2f}" for i in range(8) if c[8 + i])
+                fine = ["cand", "dpush", "dpoll", "gpush", "gpoll", "rpoll", "rowpre", "rowupd"]
+                w0 += " || " + " ".join(f"{fine[i]}={c[8 + i] / it / 1965:.2f}" for i in range(8))
+                w1 = " ".join(f"{names_ph[i]}={c[16 + i] / it / 1965:.2f}" for i in range(8) if c[16 + i])
                 print(f"{nm} G={geo['num_ctas']} CS={geo['cluster_size']} srows={geo['smem_rows']} IT={r.iterations} {ms * 1e3 / it:.2f} us/it | "
                       f"w0(us/it @1.965GHz): {w0} | w1: {w1}", flush=True)
 
