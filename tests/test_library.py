@@ -22,7 +22,12 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2004_02480_b200 import _build
+    # by path: importing the package would load the (maybe not yet built) libcsk.so
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_csk_build", os.path.join(ROOT, "paper_2004_02480_b200", "_build.py"))
+    _build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_build)
     path = _build.build()
     return ctypes.CDLL(path)
 
