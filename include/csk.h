@@ -77,7 +77,8 @@ typedef struct {
 } csk_report_t;
 
 /* Optional knobs and debug traces for csk_solve_ex.  Zero-initialise for defaults. */
-#define CSK_SOLVE_ASYNC 1 /* opts->flags: return right after the launch; csk_solve_wait fills the report */
+#define CSK_SOLVE_ASYNC 1  /* opts->flags: return right after the launch; csk_solve_wait fills the report */
+#define CSK_SOLVE_LEGACY 2 /* opts->flags: the round-1 cluster/DSMEM kernel (shared-memory rows; A/B only) */
 
 typedef struct {
     int32_t num_ctas;      /* persistent CTAs (<= co-resident limit); 0 = auto */
@@ -89,7 +90,11 @@ typedef struct {
     int64_t *idx_trace;    /* device int64[trace_cap]: i_k, or NULL */
     double *res_trace;     /* device double[trace_cap]: stop quantity at x_k, or NULL */
     double *x_trace;       /* device double[trace_cap * n]: x_k row by row, or NULL */
-    int64_t *phase_cycles; /* debug: device int64[16] per-phase SM-cycle totals of CTA 0, or NULL */
+    int64_t *phase_cycles; /* debug (CSK_SOLVE_LEGACY only): device int64[16] per-phase SM-cycle totals */
+    int32_t reg_rows;      /* rows of A~ per row group kept in registers: 0 = auto (max), -1 = none,
+                              k > 0 = at most k (the default kernel; smem_rows then counts rows per
+                              row group kept in shared memory, the rest re-read from L2/HBM) */
+    int32_t group_warps;   /* warps per row group (1, 2, 4, 8): 0 = auto (fewest with n <= 512 x warps) */
 } csk_solve_opts_t;
 
 typedef struct csk_ctx_s *csk_ctx_t;

@@ -27,6 +27,7 @@ CONVERGED, MAX_ITERS, STAGNATED = 0, 1, 2
 STOP_RES, STOP_RESIDUAL = 0, 1
 MAX_N = 2048
 SOLVE_ASYNC = 1
+SOLVE_LEGACY = 2
 
 
 class CskError(RuntimeError):
@@ -53,7 +54,8 @@ class SolveOpts(ctypes.Structure):
                 ("flags", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
                 ("trace_cap", ctypes.c_int64), ("idx_trace", ctypes.c_void_p),
                 ("res_trace", ctypes.c_void_p), ("x_trace", ctypes.c_void_p),
-                ("phase_cycles", ctypes.c_void_p)]
+                ("phase_cycles", ctypes.c_void_p), ("reg_rows", ctypes.c_int32),
+                ("group_warps", ctypes.c_int32)]
 
 
 def _load():
@@ -275,6 +277,7 @@ class SolveResult:
 def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
               num_ctas: int = 0, smem_rows: int = 0, cluster_size: int = 0, trace: int = 0,
               trace_x: bool = False, phase_cycles: torch.Tensor | None = None,
+              reg_rows: int = 0, group_warps: int = 0, legacy: bool = False,
               ctx: Context | None = None) -> SolveResult:
     """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel."""
     ctx = ctx or default_context()
@@ -289,6 +292,9 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
     opts.num_ctas = num_ctas
     opts.smem_rows = smem_rows
     opts.cluster_size = cluster_size
+    opts.reg_rows = reg_rows
+    opts.group_warps = group_warps
+    opts.flags = SOLVE_LEGACY if legacy else 0
     idx_t = res_t = x_t = None
     if trace:
         idx_t = torch.full((trace,), -1, dtype=torch.int64, device=At.device)

@@ -41,7 +41,7 @@ struct csk_ctx_s {
     cudaStream_t pending_stream = nullptr;
     bool pending = false;
     bool pending_resmode = false;
-    int last_solve_geom[3] = {0, 0, 0};  // CTAs, cluster size, smem rows
+    int last_solve_geom[5] = {0, 0, 0, 0, 0};  // CTAs, cluster size, smem rows, register rows, warps/group
     // host-side memo of driver queries that would otherwise sit between short kernels
     std::set<const void *> smem_raised;                              // kernels set to max dyn smem
     std::map<std::tuple<const void *, int, size_t>, int> occ_cache;  // (fn, cluster, smem) -> n
@@ -101,6 +101,10 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
                        int64_t d, int64_t n, double *x, const double *x_star, double tol,
                        int64_t max_iters, const csk_solve_opts_t *opts, csk_report_t *report,
                        cudaStream_t stream);
+// (loop.cu) register-resident loop with the flat atomic exchange (default)
+csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq, int64_t d,
+                      int64_t n, double *x, const double *x_star, double tol, int64_t max_iters,
+                      const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream);
 csk_status_t ensure_host_report(csk_ctx_t ctx);
 csk_status_t finish_solve(csk_ctx_t ctx, csk_report_t *report);
 

@@ -1,0 +1,671 @@
+// loop.cu -- S5..S8: the Algorithm 1 loop as ONE persistent kernel,
+// A~ held in REGISTERS (then shared memory, then re-read from L2/HBM), one flat
+// atomic exchange per iteration.
+//
+// Grid: G cooperative CTAs (default: one per SM), 8 warps each, no clusters.  CTA c owns
+// the contiguous rows [d c/G, d (c+1)/G) of A~.  Its warps form RG = 8/WPG row groups of
+// WPG warps (TG = 32 WPG threads); group g owns a balanced contiguous slice of the CTA's
+// rows, and thread t of a group owns the columns c_q = t + TG q (q < CB), so every group
+// holds all n columns and keeps its own copy of x_k in registers (CB doubles per thread).
+// Row i of a group lives in
+//   i <  rr            : registers   (a[i][q], CB doubles per row per thread)
+//   rr <= i < rr + rs  : shared memory, [i][q][t] (a warp reads 32 consecutive doubles)
+//   otherwise          : re-read from L2/HBM every iteration (coalesced along c_q).
+//
+// Iteration k (no launch, no grid barrier beyond the exchange itself):
+//   S6  GEMV: thread partials sum_q fma(a[i][q], x_q) in q order; register rows reduce
+//       across the warp with a transposed shuffle tree (row i ends in a fixed lane group),
+//       other rows with a xor butterfly; warp partials of a row are added in warp order.
+//       Fixed order everywhere -> identical bits in every run.
+//   S5  RES_k = ||x_k - x*||^2 / ||x*||^2 from group 0's registers, in every CTA
+//       (identical arithmetic -> every CTA takes the same stop decision, no communication).
+//   S7  score_i = r_i^2/nsq_i (masked rows never win).  A row's 64-bit key is
+//       (score bits >> (b-1)) << b | (2^b - 1 - i), b = bits(d+1): max key = max score,
+//       ties (equal in the kept 53-b mantissa bits) -> lowest row index (R-15).
+//       CTA argmax -> one red.max.u64 of the key + one red.release.add of an arrival
+//       counter on the same 16-byte pair; thread 0 spins on a 16-byte acquire load of
+//       {count, max} until all G CTAs arrived (3 rotating pairs, CTA 0 clears the next).
+//   S8  every CTA reads the winner's (lambda, score) slot, TMA-copies A~^(ik) into shared
+//       memory, and applies x_q += lambda a_ik[c_q] with the same fma in every copy, so all
+//       copies of x stay bit-identical.
+#include <stdlib.h>
+#include <string.h>
+
+#include "csk_internal.cuh"
+
+namespace csk {
+
+namespace {
+
+constexpr int kLW = 8;             // warps per CTA
+constexpr int kLT = kLW * 32;      // threads per CTA
+constexpr int kXchWords = 16;      // one 128-byte line per {count, max} pair
+constexpr int kSlotDoubles = 4;    // lambda, score, rr, pad
+
+struct LoopParams {
+    const double *At;
+    const double *bt;
+    const double *nsq;
+    int64_t d, n;
+    double *x;
+    const double *x_star;
+    double tol;
+    int64_t max_iters;
+    unsigned long long *xch;  // [3][kXchWords]: {count, max key}
+    double *slots;            // [2][G][kSlotDoubles]
+    int64_t *report;          // [0]=iterations, [1]=final_res bits, [2]=termination, [3]=last idx
+    const double *bb;         // residual mode: ||b~||^2 (device scalar)
+    int wpg;                  // warps per row group (1, 2, 4, 8)
+    int rr;                   // rows per group held in registers (<= RRMAX)
+    int rs;                   // rows per group held in shared memory
+    int key_bits;             // b
+    int rows_max;             // max rows per CTA (sizes the shared-memory carve-up)
+    int64_t trace_cap;
+    int64_t *idx_trace;
+    double *res_trace;
+    double *x_trace;
+    int64_t *phase_cycles;    // debug (libcsk_prof.so only): [2 warps][16] SM-cycle totals of CTA 0
+};
+
+// ---- PTX helpers specific to the exchange ----
+__device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2_u64(unsigned long long *p, unsigned long long a,
+                                                  unsigned long long b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2_f64(double *p, double a, double b) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v2(const unsigned long long *p, unsigned long long &a,
+                                              unsigned long long &b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// order this thread's generic-proxy view of global memory before its later async-proxy (TMA) reads
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ double ld_relaxed_f64(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ double lwarp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// 64-bit key of row i with score s (see header).  Masked rows (s < 0) -> 0.
+__device__ __forceinline__ unsigned long long row_key(double s, int64_t i, int b) {
+    if (!(s >= 0.0)) return 0ull;
+    const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(s));
+    const unsigned long long mask = (1ull << b) - 1ull;
+    return ((sb >> (b - 1)) << b) | (mask - static_cast<unsigned long long>(i));
+}
+
+// Warp max of a 64-bit key (unique per row): the lane holding it (keys 0 -> lane 0).
+__device__ __forceinline__ int warp_max_key_lane(unsigned long long key, unsigned long long &kmax) {
+    const uint32_t kh = static_cast<uint32_t>(key >> 32), kl = static_cast<uint32_t>(key);
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, kh);
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, kh == hi ? kl : 0u);
+    kmax = (static_cast<unsigned long long>(hi) << 32) | lo;
+    const unsigned bal = __ballot_sync(0xffffffffu, key == kmax);
+    return bal ? __ffs(bal) - 1 : 0;
+}
+
+// Transposed reduction of V per-lane row partials over the 32 lanes: afterwards lanes
+// [r 32/V, (r+1) 32/V) all hold the warp sum of row r (fixed tree, identical bits).
+template <int V>
+__device__ __forceinline__ double treduce(double (&v)[V], int lane) {
+    int cnt = V;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        if (cnt > 1) {
+            const int half = cnt >> 1;
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int j = 0; j < V / 2; ++j) {
+                if (j < half) {
+                    const double send = upper ? v[j] : v[j + half];
+                    const double keep = upper ? v[j + half] : v[j];
+                    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            cnt = half;
+        } else {
+            v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+        }
+    }
+    return v[0];
+}
+
+template <int N>
+struct Pow2Ceil {
+    static constexpr int v = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+};
+
+// Shared-memory carve-up (bytes), identical on host and device.
+struct LoopSmem {
+    size_t ctl, mbar, slotbuf, cand, resp, r0tab, btl, nsql, dotp, xs, rowbuf, arows, total;
+};
+__host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs, int g) {
+    LoopSmem L;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+    const int tg = 32 * wpg;
+    L.ctl = take(64);
+    L.mbar = take(16);
+    L.slotbuf = take(kSlotDoubles * 8);
+    L.cand = take(kLW * 32);  // [RG][4] doubles
+    L.resp = take(16 * 8);
+    L.r0tab = take(static_cast<size_t>(g + 1) * 4);
+    L.btl = take(static_cast<size_t>(rows_max) * 8);
+    L.nsql = take(static_cast<size_t>(rows_max) * 8);
+    L.dotp = take(static_cast<size_t>(wpg) * rows_max * 8);
+    L.xs = take(static_cast<size_t>(tg) * cb * 8);
+    L.rowbuf = take(static_cast<size_t>(n + 2) * 8);
+    L.arows = take(static_cast<size_t>(rs) * cb * kLT * 8);
+    L.total = o;
+    return L;
+}
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int CB, int RRMAX, bool RESMODE>
+__global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
+    constexpr int V = Pow2Ceil<RRMAX>::v;
+    constexpr int LPR = 32 / V;  // lanes per row after the transposed tree
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int64_t d = p.d;
+    const int n = static_cast<int>(p.n);
+    const int WPG = p.wpg, TG = 32 * WPG, RG = kLW / WPG;
+    const int grp = warp / WPG, wg = warp - grp * WPG, tg = tid - grp * TG;
+    const int64_t r0 = d * cta / G, r1 = d * (cta + 1) / G;
+    const int R = static_cast<int>(r1 - r0);
+    const int lr0 = R * grp / RG, lr1 = R * (grp + 1) / RG;  // CTA-local rows of this group
+    const int ng = lr1 - lr0;
+    const int rr = ng < p.rr ? ng : p.rr;
+    const int rs = (ng - rr) < p.rs ? (ng - rr) : p.rs;
+    const int b = p.key_bits;
+    const int RM = p.rows_max;
+
+    const LoopSmem L = loop_smem(RM, WPG, CB, n, p.rs, G);
+    volatile int64_t *ctl = reinterpret_cast<volatile int64_t *>(smem + L.ctl);  // [0..3] B2, [4..5] RES
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L.mbar);
+    const double *slotbuf = reinterpret_cast<const double *>(smem + L.slotbuf);  // winner's slot (TMA)
+    double *cand = reinterpret_cast<double *>(smem + L.cand);  // [RG][4]: key bits, lambda, score, rr
+    double *resp = reinterpret_cast<double *>(smem + L.resp);
+    int32_t *r0tab = reinterpret_cast<int32_t *>(smem + L.r0tab);
+    double *btl = reinterpret_cast<double *>(smem + L.btl);
+    double *nsql = reinterpret_cast<double *>(smem + L.nsql);
+    double *dotp = reinterpret_cast<double *>(smem + L.dotp);  // [WPG][RM]
+    double *xs = reinterpret_cast<double *>(smem + L.xs);      // x* by padded column
+    double *rowbuf = reinterpret_cast<double *>(smem + L.rowbuf);
+    double *arows = reinterpret_cast<double *>(smem + L.arows) + static_cast<size_t>(grp) * p.rs * CB * TG;
+
+    if (tid == 0) {
+        uint32_t dyn;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        if (L.total > dyn) __trap();
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+    }
+
+    // ---- prologue: x (registers), x* (smem), b~, nsq (smem), rows into their tiers ----
+    double x[CB];
+#pragma unroll
+    for (int q = 0; q < CB; ++q) {
+        const int c = tg + TG * q;
+        x[q] = c < n ? p.x[c] : 0.0;
+    }
+    for (int c = tid; c < TG * CB; c += kLT) xs[c] = (!RESMODE && c < n) ? p.x_star[c] : 0.0;
+    for (int c = tid; c <= G; c += kLT) r0tab[c] = static_cast<int32_t>(d * c / G);
+    for (int l = tid; l < R; l += kLT) {
+        btl[l] = p.bt[r0 + l];
+        nsql[l] = p.nsq[r0 + l];
+    }
+    double a[RRMAX][CB];
+#pragma unroll
+    for (int i = 0; i < RRMAX; ++i) {
+        const double *src = p.At + (r0 + lr0 + i) * n;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+            const int c = tg + TG * q;
+            a[i][q] = (i < rr && c < n) ? src[c] : 0.0;
+        }
+    }
+    for (int i = 0; i < rs; ++i) {
+        const double *src = p.At + (r0 + lr0 + rr + i) * n;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+            const int c = tg + TG * q;
+            arows[(static_cast<size_t>(i) * CB + q) * TG + tg] = c < n ? src[c] : 0.0;
+        }
+    }
+    __syncthreads();
+
+    // ||x*||^2 by the last row group (every group holds all of x; fixed order: thread q-order
+    // fma, warp butterfly, warps in order).  The last group also owns the RES test and the
+    // x trace, keeping them off warp 0's exchange path.
+    const bool resgrp = grp == RG - 1;
+    if (!RESMODE && resgrp) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+            const double v = xs[tg + TG * q];
+            s = __fma_rn(v, v, s);
+        }
+        s = lwarp_sum(s);
+        if (lane == 0) resp[8 + wg] = s;
+    }
+    __syncthreads();
+    double xs_nrm = 0.0;
+    if (!RESMODE)
+        for (int w = 0; w < WPG; ++w) xs_nrm = xs_nrm + resp[8 + w];
+    const double bb = RESMODE ? *p.bb : 0.0;
+    const bool even = (n & 1) == 0;
+    const unsigned long long kmask = (1ull << b) - 1ull;
+    const double gd = static_cast<double>(G) / static_cast<double>(d);
+
+    int64_t k = 0, last = -1;
+    int term = -1;
+    double res = 0.0;
+    uint32_t mphase = 0;
+#if CSK_PHASE_PROF
+    const bool prof = p.phase_cycles != nullptr && cta == 0 && lane == 0 && (warp == 0 || warp == kLW - 1);
+    long long ph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64();
+#define LP(i)                           \
+    if (prof) {                         \
+        const long long tn = clock64(); \
+        ph[i] += tn - tp;               \
+        tp = tn;                        \
+    }
+#else
+#define LP(i)
+#endif
+    for (;; ++k) {
+        // ---- S6 GEMV: register rows (transposed tree: row i ends in lanes [i LPR, (i+1) LPR)) ----
+        {
+            double acc[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] = 0.0;
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+#pragma unroll
+                for (int i = 0; i < RRMAX; ++i) acc[i] = __fma_rn(a[i][q], x[q], acc[i]);
+            }
+            const double s = treduce<V>(acc, lane);
+            const int i = lane / LPR;
+            if ((lane % LPR) == 0 && i < rr) dotp[wg * RM + lr0 + i] = s;
+        }
+        // ---- S6 GEMV: shared-memory rows ----
+        for (int i = 0; i < rs; ++i) {
+            const double *ar = arows + static_cast<size_t>(i) * CB * TG + tg;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < CB; ++q) s = __fma_rn(ar[q * TG], x[q], s);
+            s = lwarp_sum(s);
+            if (lane == 0) dotp[wg * RM + lr0 + rr + i] = s;
+        }
+        // ---- S6 GEMV: streamed rows (L2/HBM), two rows per pass ----
+        for (int i = rr + rs; i < ng; i += 2) {
+            const bool two = i + 1 < ng;
+            const double *s0 = p.At + (r0 + lr0 + i) * n;
+            const double *s1 = two ? s0 + n : s0;
+            double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                const int c = tg + TG * q;
+                const double v0 = c < n ? ldg_stream1(s0 + c) : 0.0;
+                const double v1 = c < n ? ldg_stream1(s1 + c) : 0.0;
+                u0 = __fma_rn(v0, x[q], u0);
+                u1 = __fma_rn(v1, x[q], u1);
+            }
+            u0 = lwarp_sum(u0);
+            u1 = lwarp_sum(u1);
+            if (lane == 0) {
+                dotp[wg * RM + lr0 + i] = u0;
+                if (two) dotp[wg * RM + lr0 + i + 1] = u1;
+            }
+        }
+        // ---- S7 (group): r_i = b~_i - dot, score, lambda, key; group argmax -> cand[grp] ----
+        if (WPG > 1) group_bar(1 + grp, TG);
+        else __syncwarp();
+        if (wg == 0) {
+            unsigned long long bk = 0ull;
+            double bl = 0.0, bs = -1.0, rr2 = 0.0;
+            for (int l0 = 0; l0 < ng; l0 += 32) {
+                const int l = lr0 + l0 + lane;
+                if (l0 + lane < ng) {
+                    double dot = dotp[l];
+                    for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
+                    const double ri = btl[l] - dot;
+                    const double ns = nsql[l];
+                    const double sc = ns > 0.0 ? (ri * ri) / ns : -1.0;
+                    if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
+                    const unsigned long long kk = row_key(sc, r0 + l, b);
+                    if (kk > bk) { bk = kk; bl = ns > 0.0 ? ri / ns : 0.0; bs = sc; }
+                }
+            }
+            if (RESMODE) rr2 = lwarp_sum(rr2);
+            unsigned long long km;
+            const int wl = warp_max_key_lane(bk, km);
+            if (lane == wl) {
+                cand[grp * 4 + 0] = __longlong_as_double(static_cast<long long>(km));
+                cand[grp * 4 + 1] = bl;
+                cand[grp * 4 + 2] = bs;
+            }
+            if (RESMODE && lane == 0) cand[grp * 4 + 3] = rr2;
+        }
+        LP(0)
+        __syncthreads();  // B1
+        LP(1)
+
+        // ---- S5 (last group, overlapping warp 0's exchange): RES_k = ||x_k - x*||^2/||x*||^2
+        //      (P:180); every CTA computes the same value, so all stop at the same k ----
+        if (!RESMODE && resgrp) {
+            if (cta == 0 && p.x_trace && k < p.trace_cap) {
+#pragma unroll
+                for (int q = 0; q < CB; ++q) {
+                    const int c = tg + TG * q;
+                    if (c < n) p.x_trace[k * n + c] = x[q];
+                }
+            }
+            double e2 = 0.0;
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                const double e = x[q] - xs[tg + TG * q];
+                e2 = __fma_rn(e, e, e2);
+            }
+            e2 = lwarp_sum(e2);
+            if (WPG > 1) {
+                if (lane == 0) resp[wg] = e2;
+                group_bar(1 + grp, TG);
+                e2 = resp[0];
+                for (int w = 1; w < WPG; ++w) e2 = e2 + resp[w];
+            }
+            if (wg == 0 && lane == 0) {
+                const double rk = xs_nrm > 0.0 ? e2 / xs_nrm : e2;
+                ctl[4] = rk <= p.tol ? CSK_CONVERGED : -1;
+                ctl[5] = __double_as_longlong(rk);
+                if (cta == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = rk;
+            }
+        }
+        // ---- S7 exchange (warp 0) ----
+        if (warp == 0) {
+            int stop = (!RESMODE && k == p.max_iters) ? CSK_MAX_ITERS : -1;
+            int64_t wrow = -1;
+            if (stop < 0) {
+                // CTA candidate: max key over the RG group candidates
+                const unsigned long long ck =
+                    lane < RG ? static_cast<unsigned long long>(__double_as_longlong(cand[lane * 4])) : 0ull;
+                unsigned long long km;
+                const int cl = warp_max_key_lane(ck, km);
+                const double cl_l = cand[cl * 4 + 1], cl_s = cand[cl * 4 + 2];
+                double crr = 0.0;
+                if (RESMODE)
+                    for (int g = 0; g < RG; ++g) crr = crr + cand[g * 4 + 3];
+                unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
+                double *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotDoubles;
+                if (lane == 0) {
+                    double *my = slot_k + static_cast<size_t>(cta) * kSlotDoubles;
+                    st_relaxed_v2_f64(my, cl_l, cl_s);
+                    if (RESMODE) st_relaxed_v2_f64(my + 2, crr, 0.0);
+                    if (cta == 0) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                    red_max_u64(pair + 1, km);
+                    red_add_release_u64(pair, 1ull);
+                }
+                LP(2)
+                unsigned long long c, mx;
+                do {  // relaxed polls (an acquire load would invalidate L1 on every poll) ...
+                    ld_relaxed_v2(pair, c, mx);
+                } while (c < static_cast<unsigned long long>(G));
+                fence_acq_rel_gpu();         // ... then one acquire fence: the winner's slot is visible
+                fence_proxy_async_global();  // ... to this thread's TMA reads as well
+                LP(3)
+                if (mx != 0ull) {
+                    wrow = static_cast<int64_t>(kmask - (mx & kmask));
+                    if (lane == 0) {
+                        int own = static_cast<int>(static_cast<double>(wrow) * gd);
+                        if (own > G - 1) own = G - 1;
+                        while (own + 1 < G && r0tab[own + 1] <= wrow) ++own;
+                        while (own > 0 && r0tab[own] > wrow) --own;
+                        // winner's (lambda, score) slot and A~^(ik) -> shared memory, one mbarrier
+                        // (odd n: the row is read with plain loads in the update)
+                        const uint32_t rb = even ? static_cast<uint32_t>(n) * 8u : 0u;
+                        mbar_arrive_expect_tx(mbar, rb + 16u);
+                        bulk_g2s(const_cast<double *>(slotbuf), slot_k + static_cast<size_t>(own) * kSlotDoubles, 16u, mbar);
+                        if (even) bulk_g2s(rowbuf, p.At + wrow * n, rb, mbar);
+                    }
+                }
+                if (RESMODE) {
+                    // ||r_k||^2: the G CTA partials in fixed order
+                    double t = 0.0;
+                    for (int cc = lane; cc < G; cc += 32) t = t + ld_relaxed_f64(slot_k + static_cast<size_t>(cc) * kSlotDoubles + 2);
+                    t = lwarp_sum(t);
+                    res = bb > 0.0 ? t / bb : t;
+                    if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                    if (res <= p.tol) stop = CSK_CONVERGED;
+                    else if (k == p.max_iters) stop = CSK_MAX_ITERS;
+                }
+                if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
+                if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copies
+            }
+            if (lane == 0) {
+                ctl[0] = stop;  // -1: copies in flight on mbar
+                ctl[1] = wrow;
+                ctl[3] = __double_as_longlong(res);
+            }
+        }
+        LP(4)
+        __syncthreads();  // B2
+        LP(5)
+        int stop = static_cast<int>(ctl[0]);
+        double lam = 0.0;
+        if (stop == -1) {  // the winner's slot (and row) arrive on the mbarrier
+            mbar_wait(mbar, mphase);
+            mphase ^= 1u;
+            lam = slotbuf[0];
+            if (slotbuf[1] == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
+        }
+        LP(6)
+        if (!RESMODE) {
+            res = __longlong_as_double(ctl[5]);
+            if (ctl[4] == CSK_CONVERGED) stop = CSK_CONVERGED;  // RES_k <= tol: no update
+        } else {
+            res = __longlong_as_double(ctl[3]);
+        }
+        if (stop != -1) {
+            term = stop;
+            break;
+        }
+        // ---- S8: x += lambda A~^(ik) ----
+        const int64_t wrow = ctl[1];
+        if (cta == 0 && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wrow;
+        last = wrow;
+        if (even) {
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                const int c = tg + TG * q;
+                if (c < n) x[q] = __fma_rn(lam, rowbuf[c], x[q]);
+            }
+        } else {
+            const double *src = p.At + wrow * n;
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                const int c = tg + TG * q;
+                if (c < n) x[q] = __fma_rn(lam, ldg_stream1(src + c), x[q]);
+            }
+        }
+        LP(7)
+    }
+#undef LP
+#if CSK_PHASE_PROF
+    if (prof)
+        for (int i = 0; i < 16; ++i) p.phase_cycles[(warp == 0 ? 0 : 1) * 16 + i] = ph[i];
+#endif
+    // ---- epilogue: CTA 0's last group writes x (and the trace of the final iterate) ----
+    if (cta == 0 && resgrp) {
+        const bool tr = p.x_trace && k < p.trace_cap;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+            const int c = tg + TG * q;
+            if (c < n) {
+                p.x[c] = x[q];
+                if (tr) p.x_trace[k * n + c] = x[q];
+            }
+        }
+        if (tid == (RG - 1) * TG) {
+            p.report[0] = k;
+            p.report[1] = __double_as_longlong(res);
+            p.report[2] = term;
+            p.report[3] = last;
+        }
+    }
+}
+
+using LoopFn = void (*)(const LoopParams);
+
+// rows per thread held in registers for a given column count per thread (~160 registers)
+constexpr int rr_max_for(int cb) { return cb >= 16 ? 5 : cb >= 8 ? 10 : cb >= 4 ? 20 : 32; }
+
+template <bool RM>
+LoopFn pick_cb(int cb) {
+    switch (cb) {
+        case 1: return k_loop<1, rr_max_for(1), RM>;
+        case 2: return k_loop<2, rr_max_for(2), RM>;
+        case 4: return k_loop<4, rr_max_for(4), RM>;
+        case 8: return k_loop<8, rr_max_for(8), RM>;
+        case 16: return k_loop<16, rr_max_for(16), RM>;
+        default: return nullptr;
+    }
+}
+
+__global__ void k_sumsq_loop(const double *v, int64_t len, double *out) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) a = __fma_rn(v[i], v[i], a);
+    a = lwarp_sum(a);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = red[0];
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = t + red[w];
+        *out = t;
+    }
+}
+
+}  // namespace
+
+csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq, int64_t d,
+                      int64_t n, double *x, const double *x_star, double tol, int64_t max_iters,
+                      const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream) {
+    const bool resmode = (x_star == nullptr);
+    // group width and columns per thread: the fewest warps per group with n <= 32 WPG 16
+    int wpg = 1;
+    while (wpg < kLW && 32 * wpg * 16 < n) wpg *= 2;
+    if (opts && opts->group_warps > 0) {
+        if (opts->group_warps > kLW || (opts->group_warps & (opts->group_warps - 1)))
+            return fail(ctx, CSK_E_ARG, "csk_solve: group_warps must be 1, 2, 4 or 8");
+        if (opts->group_warps > wpg) wpg = opts->group_warps;
+    }
+    if (32 * wpg * 16 < n) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n too large for the register GEMV");
+    int cb = 1;
+    while (32 * wpg * cb < n) cb *= 2;
+    LoopFn fn = resmode ? pick_cb<true>(cb) : pick_cb<false>(cb);
+    if (!fn) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
+    CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
+
+    int G = opts && opts->num_ctas > 0 ? opts->num_ctas : ctx->num_sms;
+    if (G > d) G = static_cast<int>(d);
+    int per = 0;
+    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, 0, &per));
+    const int rows_max = static_cast<int>((d + G - 1) / G);
+    const int rg = kLW / wpg;
+    const int rb = (rows_max + rg - 1) / rg;  // max rows per group
+    int rr = rr_max_for(cb);
+    if (opts && opts->reg_rows < 0) rr = 0;
+    else if (opts && opts->reg_rows > 0 && opts->reg_rows < rr) rr = opts->reg_rows;
+    if (rr > rb) rr = rb;
+    int rs_fit = 0;
+    while (rs_fit < rb - rr &&
+           loop_smem(rows_max, wpg, cb, n, rs_fit + 1, G).total <= static_cast<size_t>(ctx->max_smem_optin))
+        ++rs_fit;
+    int rs = rs_fit;
+    if (opts && opts->smem_rows < 0) rs = 0;
+    else if (opts && opts->smem_rows > 0 && opts->smem_rows < rs) rs = opts->smem_rows;
+    const size_t smem = loop_smem(rows_max, wpg, cb, n, rs, G).total;
+    if (smem > static_cast<size_t>(ctx->max_smem_optin))
+        return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory (use more CTAs)");
+    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, smem, &per));
+    if (per < G) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
+    int kb = 1;
+    while ((1ll << kb) < d + 1) ++kb;
+
+    const size_t xch_bytes = 3 * kXchWords * 8;
+    const size_t slot_bytes = static_cast<size_t>(2) * G * kSlotDoubles * 8;
+    CSK_CHECK(ensure(ctx, ctx->slots, xch_bytes + slot_bytes));
+    CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
+    CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
+    CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, xch_bytes + slot_bytes, stream));
+    double *bb = static_cast<double *>(ctx->scalars.ptr);
+    if (resmode) k_sumsq_loop<<<1, 1024, 0, stream>>>(bt, d, bb);
+
+    LoopParams prm{};
+    prm.At = At; prm.bt = bt; prm.nsq = nsq; prm.d = d; prm.n = n; prm.x = x;
+    prm.x_star = x_star; prm.tol = tol; prm.max_iters = max_iters;
+    prm.xch = static_cast<unsigned long long *>(ctx->slots.ptr);
+    prm.slots = reinterpret_cast<double *>(static_cast<unsigned char *>(ctx->slots.ptr) + xch_bytes);
+    prm.report = static_cast<int64_t *>(ctx->report.ptr);
+    prm.bb = bb;
+    prm.wpg = wpg;
+    prm.rr = rr;
+    prm.rs = rs;
+    prm.key_bits = kb;
+    prm.rows_max = rows_max;
+    prm.trace_cap = opts ? opts->trace_cap : 0;
+    prm.idx_trace = opts ? opts->idx_trace : nullptr;
+    prm.res_trace = opts ? opts->res_trace : nullptr;
+    prm.x_trace = opts ? opts->x_trace : nullptr;
+    prm.phase_cycles = opts ? opts->phase_cycles : nullptr;
+    if (prm.trace_cap <= 0) { prm.idx_trace = nullptr; prm.res_trace = nullptr; prm.x_trace = nullptr; prm.trace_cap = 0; }
+
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kLT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // Profiling only (ncu cannot replay cooperative launches): same kernel without the attribute.
+    static const bool noncoop = getenv("CSK_PROFILE_NONCOOP") != nullptr;
+    if (noncoop) cfg.numAttrs = 0;
+    CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, prm));
+    ctx->last_solve_geom[0] = G;
+    ctx->last_solve_geom[1] = 1;
+    ctx->last_solve_geom[2] = rs;
+    ctx->last_solve_geom[3] = rr;
+    ctx->last_solve_geom[4] = wpg;
+    CSK_CHECK(ensure_host_report(ctx));
+    CSK_CUDA(ctx, cudaMemcpyAsync(ctx->report_host, ctx->report.ptr, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    ctx->pending_stream = stream;
+    ctx->pending_resmode = resmode;
+    ctx->pending = true;
+    if (opts && (opts->flags & CSK_SOLVE_ASYNC)) return CSK_OK;
+    return finish_solve(ctx, report);
+}
+
+}  // namespace csk

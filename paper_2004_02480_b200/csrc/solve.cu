@@ -829,6 +829,8 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
     if (n > CSK_MAX_N) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n > CSK_MAX_N");
     if ((n % 2 == 0) && !aligned16(At)) return fail(ctx, CSK_E_ARG, "csk_solve: A~ not 16-byte aligned");
     if (ctx->pending) return fail(ctx, CSK_E_ARG, "csk_solve: a CSK_SOLVE_ASYNC solve is still in flight (call csk_solve_wait)");
+    if (!(opts && (opts->flags & CSK_SOLVE_LEGACY)))
+        return run_loop(ctx, At, bt, nsq, d, n, x, x_star, tol, max_iters, opts, report, stream);
     const bool resmode = (x_star == nullptr);
     int P = 0, wc = 0;
     KernelFn fn = pick_kernel(n, resmode, true, P, wc);  // geometry probe (8-warp variant)

@@ -1,0 +1,56 @@
+"""Debug probe: per-phase cycle breakdown of the default loop kernel (loop.cu, CTA 0, warps 0/1).
+
+python tools/loop_probe.py [C1 C2 C3 C4] [--ctas=148,74]
+Phases: 0 GEMV + group finalize, 1 B1 wait, 2 CTA argmax + publish, 3 spin, 4 TMA issue +
+slot load, 5 B2 wait, 6 row wait, 7 update.  w0 = warp 0 (exchange), w7 = last warp (RES test).
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+os.environ.setdefault("CSK_LIB", "prof")  # the phase profiler lives in libcsk_prof.so
+import torch  # noqa: E402
+
+import paper_2004_02480_b200 as csk  # noqa: E402
+from csk_synth import CONFIGS, make_config  # noqa: E402
+
+NAMES = ["gemv+final", "B1", "combine+publish", "spin", "post", "B2", "rowwait", "upd"]
+
+
+def main():
+    names = [a for a in sys.argv[1:] if a in CONFIGS] or ["C1", "C2", "C3"]
+    ctas = [0]
+    wpgs = [0]
+    for a in sys.argv[1:]:
+        if a.startswith("--ctas="):
+            ctas = [int(v) for v in a.split("=")[1].split(",")]
+        if a.startswith("--wpg="):
+            wpgs = [int(v) for v in a.split("=")[1].split(",")]
+    for nm in names:
+        cfg = CONFIGS[nm]
+        p = make_config(cfg, "cuda")
+        At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
+        cap = cfg.max_iters if nm != "C4" else 3000
+        for G, wpg in [(g, w) for g in ctas for w in wpgs]:
+            csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, group_warps=wpg)
+            ph = torch.zeros(32, dtype=torch.int64, device="cuda")
+            st = torch.cuda.Event(enable_timing=True)
+            en = torch.cuda.Event(enable_timing=True)
+            st.record()
+            r = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, group_warps=wpg,
+                              phase_cycles=ph)
+            en.record()
+            torch.cuda.synchronize()
+            geo = csk.csk_last_solve_geometry()
+            ms = st.elapsed_time(en)
+            it = max(r.iterations, 1)
+            c = ph.cpu().tolist()
+            w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(8))
+            w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(9) if c[16 + i])
+            print(f"{nm} G={geo['num_ctas']} wpg={wpg} IT={r.iterations} {ms * 1e3 / it:.2f} us/it = "
+                  f"{ms * 1e6 / it * 1.965:.0f} cyc/it | w0 cyc/it: {w0} | w7: {w7}", flush=True)
+
+
+if __name__ == "__main__":
+    main()

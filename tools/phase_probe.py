@@ -38,12 +38,12 @@ def main():
           for cs in css:
             for sm in smem_modes:
                 ph = torch.zeros(32, dtype=torch.int64, device="cuda")
-                csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, smem_rows=sm, cluster_size=cs)
+                csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, smem_rows=sm, cluster_size=cs, legacy=True)
                 st = torch.cuda.Event(enable_timing=True)
                 en = torch.cuda.Event(enable_timing=True)
                 st.record()
                 r = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, smem_rows=sm,
-                                  cluster_size=cs, phase_cycles=ph)
+                                  cluster_size=cs, phase_cycles=ph, legacy=True)
                 geo = csk.csk_last_solve_geometry()
                 en.record()
                 torch.cuda.synchronize()
