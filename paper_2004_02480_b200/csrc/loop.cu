@@ -40,7 +40,7 @@ namespace {
 constexpr int kLW = 8;             // warps per CTA
 constexpr int kLT = kLW * 32;      // threads per CTA
 constexpr int kXchWords = 16;      // one 128-byte line per {count, max} pair
-constexpr int kSlotDoubles = 4;    // lambda, score, rr, pad
+constexpr int kSlotWords = 8;      // LL slot: lambda, score, rr as tagged 32-bit halves + pad
 
 struct LoopParams {
     const double *At;
@@ -52,7 +52,7 @@ struct LoopParams {
     double tol;
     int64_t max_iters;
     unsigned long long *xch;  // [3][kXchWords]: {count, max key}
-    double *slots;            // [2][G][kSlotDoubles]
+    unsigned long long *slots;  // [2][G][kSlotWords] LL-tagged (tag = k + 1 in every 8-byte word)
     int64_t *report;          // [0]=iterations, [1]=final_res bits, [2]=termination, [3]=last idx
     const double *bb;         // residual mode: ||b~||^2 (device scalar)
     int wpg;                  // warps per row group (1, 2, 4, 8)
@@ -78,21 +78,38 @@ __device__ __forceinline__ void st_relaxed_v2_u64(unsigned long long *p, unsigne
                                                   unsigned long long b) {
     asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
-__device__ __forceinline__ void st_relaxed_v2_f64(double *p, double a, double b) {
-    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+// LL (low-latency) encoding: a double as two 8-byte words {32 data bits | 32-bit tag}; 8-byte
+// aligned accesses are single-copy atomic, so a reader that sees the tag in both words holds
+// a consistent value without any fence.
+__device__ __forceinline__ void ll_pack(double v, uint32_t tag, unsigned long long &hi, unsigned long long &lo) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    hi = (b & 0xffffffff00000000ull) | tag;
+    lo = (b << 32) | tag;
+}
+__device__ __forceinline__ bool ll_ok(unsigned long long hi, unsigned long long lo, uint32_t tag) {
+    return static_cast<uint32_t>(hi) == tag && static_cast<uint32_t>(lo) == tag;
+}
+__device__ __forceinline__ double ll_val(unsigned long long hi, unsigned long long lo) {
+    return __longlong_as_double(static_cast<long long>((hi & 0xffffffff00000000ull) | (lo >> 32)));
+}
+__device__ __forceinline__ void ld_relaxed_v2_u64(const unsigned long long *p, unsigned long long &a,
+                                                  unsigned long long &b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// spin until the LL-tagged double at p (2 words) carries `tag`
+__device__ __forceinline__ double ll_load(const unsigned long long *p, uint32_t tag) {
+    unsigned long long hi, lo;
+    do {
+        ld_relaxed_v2_u64(p, hi, lo);
+    } while (!ll_ok(hi, lo, tag));
+    return ll_val(hi, lo);
 }
 __device__ __forceinline__ void ld_relaxed_v2(const unsigned long long *p, unsigned long long &a,
                                               unsigned long long &b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // order this thread's generic-proxy view of global memory before its later async-proxy (TMA) reads
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ double ld_relaxed_f64(const double *p) {
-    double v;
-    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    return v;
-}
 
 __device__ __forceinline__ double lwarp_sum(double v) {
 #pragma unroll
@@ -151,7 +168,7 @@ struct Pow2Ceil {
 
 // Shared-memory carve-up (bytes), identical on host and device.
 struct LoopSmem {
-    size_t ctl, mbar, slotbuf, cand, resp, r0tab, btl, nsql, dotp, xs, rowbuf, arows, total;
+    size_t ctl, mbar, slotbuf, cand, resp, r0tab, btl, invl, dotp, xs, rowbuf, arows, total;
 };
 __host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs, int g) {
     LoopSmem L;
@@ -160,12 +177,12 @@ __host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int
     const int tg = 32 * wpg;
     L.ctl = take(64);
     L.mbar = take(16);
-    L.slotbuf = take(kSlotDoubles * 8);
+    L.slotbuf = take(kSlotWords * 8);
     L.cand = take(kLW * 32);  // [RG][4] doubles
     L.resp = take(16 * 8);
     L.r0tab = take(static_cast<size_t>(g + 1) * 4);
     L.btl = take(static_cast<size_t>(rows_max) * 8);
-    L.nsql = take(static_cast<size_t>(rows_max) * 8);
+    L.invl = take(static_cast<size_t>(rows_max) * 8);
     L.dotp = take(static_cast<size_t>(wpg) * rows_max * 8);
     L.xs = take(static_cast<size_t>(tg) * cb * 8);
     L.rowbuf = take(static_cast<size_t>(n + 2) * 8);
@@ -201,12 +218,12 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const LoopSmem L = loop_smem(RM, WPG, CB, n, p.rs, G);
     volatile int64_t *ctl = reinterpret_cast<volatile int64_t *>(smem + L.ctl);  // [0..3] B2, [4..5] RES
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L.mbar);
-    const double *slotbuf = reinterpret_cast<const double *>(smem + L.slotbuf);  // winner's slot (TMA)
+    const unsigned long long *slotbuf = reinterpret_cast<const unsigned long long *>(smem + L.slotbuf);  // winner's slot (TMA)
     double *cand = reinterpret_cast<double *>(smem + L.cand);  // [RG][4]: key bits, lambda, score, rr
     double *resp = reinterpret_cast<double *>(smem + L.resp);
     int32_t *r0tab = reinterpret_cast<int32_t *>(smem + L.r0tab);
     double *btl = reinterpret_cast<double *>(smem + L.btl);
-    double *nsql = reinterpret_cast<double *>(smem + L.nsql);
+    double *invl = reinterpret_cast<double *>(smem + L.invl);  // 1/nsq (0: masked row)
     double *dotp = reinterpret_cast<double *>(smem + L.dotp);  // [WPG][RM]
     double *xs = reinterpret_cast<double *>(smem + L.xs);      // x* by padded column
     double *rowbuf = reinterpret_cast<double *>(smem + L.rowbuf);
@@ -231,7 +248,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     for (int c = tid; c <= G; c += kLT) r0tab[c] = static_cast<int32_t>(d * c / G);
     for (int l = tid; l < R; l += kLT) {
         btl[l] = p.bt[r0 + l];
-        nsql[l] = p.nsq[r0 + l];
+        const double ns = p.nsq[r0 + l];
+        invl[l] = ns > 0.0 ? 1.0 / ns : 0.0;
     }
     double a[RRMAX][CB];
 #pragma unroll
@@ -350,11 +368,12 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     double dot = dotp[l];
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
                     const double ri = btl[l] - dot;
-                    const double ns = nsql[l];
-                    const double sc = ns > 0.0 ? (ri * ri) / ns : -1.0;
+                    const double iv = invl[l];
+                    // score r^2/nsq and lambda r/nsq through the precomputed 1/nsq (R-3)
+                    const double sc = iv > 0.0 ? (ri * ri) * iv : -1.0;
                     if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
                     const unsigned long long kk = row_key(sc, r0 + l, b);
-                    if (kk > bk) { bk = kk; bl = ns > 0.0 ? ri / ns : 0.0; bs = sc; }
+                    if (kk > bk) { bk = kk; bl = ri * iv; bs = sc; }
                 }
             }
             if (RESMODE) rr2 = lwarp_sum(rr2);
@@ -416,22 +435,32 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 if (RESMODE)
                     for (int g = 0; g < RG; ++g) crr = crr + cand[g * 4 + 3];
                 unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
-                double *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotDoubles;
+                unsigned long long *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotWords;
+                const uint32_t tag = static_cast<uint32_t>(k + 1);
                 if (lane == 0) {
-                    double *my = slot_k + static_cast<size_t>(cta) * kSlotDoubles;
-                    st_relaxed_v2_f64(my, cl_l, cl_s);
-                    if (RESMODE) st_relaxed_v2_f64(my + 2, crr, 0.0);
                     if (cta == 0) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
                     red_max_u64(pair + 1, km);
-                    red_add_release_u64(pair, 1ull);
+                    red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
+                    // the slot needs no ordering: readers validate its LL tags
+                    unsigned long long *my = slot_k + static_cast<size_t>(cta) * kSlotWords;
+                    unsigned long long h0, l0, h1, l1;
+                    ll_pack(cl_l, tag, h0, l0);
+                    ll_pack(cl_s, tag, h1, l1);
+                    st_relaxed_v2_u64(my, h0, l0);
+                    st_relaxed_v2_u64(my + 2, h1, l1);
+                    if (RESMODE) {
+                        ll_pack(crr, tag, h0, l0);
+                        st_relaxed_v2_u64(my + 4, h0, l0);
+                    }
                 }
                 LP(2)
                 unsigned long long c, mx;
                 do {  // relaxed polls (an acquire load would invalidate L1 on every poll) ...
                     ld_relaxed_v2(pair, c, mx);
                 } while (c < static_cast<unsigned long long>(G));
-                fence_acq_rel_gpu();         // ... then one acquire fence: the winner's slot is visible
-                fence_proxy_async_global();  // ... to this thread's TMA reads as well
+                // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the proxy
+                // fence orders this thread's generic view before its TMA reads
+                fence_proxy_async_global();
                 LP(3)
                 if (mx != 0ull) {
                     wrow = static_cast<int64_t>(kmask - (mx & kmask));
@@ -443,15 +472,16 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         // winner's (lambda, score) slot and A~^(ik) -> shared memory, one mbarrier
                         // (odd n: the row is read with plain loads in the update)
                         const uint32_t rb = even ? static_cast<uint32_t>(n) * 8u : 0u;
-                        mbar_arrive_expect_tx(mbar, rb + 16u);
-                        bulk_g2s(const_cast<double *>(slotbuf), slot_k + static_cast<size_t>(own) * kSlotDoubles, 16u, mbar);
+                        mbar_arrive_expect_tx(mbar, rb + 32u);
+                        bulk_g2s(const_cast<unsigned long long *>(slotbuf), slot_k + static_cast<size_t>(own) * kSlotWords, 32u, mbar);
                         if (even) bulk_g2s(rowbuf, p.At + wrow * n, rb, mbar);
+                        ctl[2] = own;
                     }
                 }
                 if (RESMODE) {
                     // ||r_k||^2: the G CTA partials in fixed order
                     double t = 0.0;
-                    for (int cc = lane; cc < G; cc += 32) t = t + ld_relaxed_f64(slot_k + static_cast<size_t>(cc) * kSlotDoubles + 2);
+                    for (int cc = lane; cc < G; cc += 32) t = t + ll_load(slot_k + static_cast<size_t>(cc) * kSlotWords + 4, tag);
                     t = lwarp_sum(t);
                     res = bb > 0.0 ? t / bb : t;
                     if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
@@ -475,8 +505,17 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         if (stop == -1) {  // the winner's slot (and row) arrive on the mbarrier
             mbar_wait(mbar, mphase);
             mphase ^= 1u;
-            lam = slotbuf[0];
-            if (slotbuf[1] == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
+            const uint32_t tag = static_cast<uint32_t>(k + 1);
+            double sc;
+            if (ll_ok(slotbuf[0], slotbuf[1], tag) && ll_ok(slotbuf[2], slotbuf[3], tag)) {
+                lam = ll_val(slotbuf[0], slotbuf[1]);
+                sc = ll_val(slotbuf[2], slotbuf[3]);
+            } else {  // the copy raced the owner's slot store: re-read until the tags match
+                const unsigned long long *gs = p.slots + (static_cast<size_t>(k & 1) * G + ctl[2]) * kSlotWords;
+                lam = ll_load(gs, tag);
+                sc = ll_load(gs + 2, tag);
+            }
+            if (sc == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
         }
         LP(6)
         if (!RESMODE) {
@@ -539,16 +578,36 @@ using LoopFn = void (*)(const LoopParams);
 // rows per thread held in registers for a given column count per thread (~160 registers)
 constexpr int rr_max_for(int cb) { return cb >= 16 ? 5 : cb >= 8 ? 10 : cb >= 4 ? 20 : 32; }
 
-template <bool RM>
-LoopFn pick_cb(int cb) {
-    switch (cb) {
-        case 1: return k_loop<1, rr_max_for(1), RM>;
-        case 2: return k_loop<2, rr_max_for(2), RM>;
-        case 4: return k_loop<4, rr_max_for(4), RM>;
-        case 8: return k_loop<8, rr_max_for(8), RM>;
-        case 16: return k_loop<16, rr_max_for(16), RM>;
-        default: return nullptr;
+// Instantiated (CB, RRMAX) pairs: register-row capacities sized to the row counts per group
+// that the configs produce (fewer unused register rows = fewer wasted FMAs and a shorter
+// transposed tree).  Residual mode only gets the full-capacity variant.
+struct LoopVariant {
+    int cb, rrmax;
+    LoopFn fn;
+};
+const LoopVariant kVariants[] = {
+    {1, 2, k_loop<1, 2, false>},   {1, 8, k_loop<1, 8, false>},   {1, 32, k_loop<1, 32, false>},
+    {2, 2, k_loop<2, 2, false>},   {2, 8, k_loop<2, 8, false>},   {2, 32, k_loop<2, 32, false>},
+    {4, 2, k_loop<4, 2, false>},   {4, 4, k_loop<4, 4, false>},   {4, 8, k_loop<4, 8, false>},
+    {4, 20, k_loop<4, 20, false>}, {8, 2, k_loop<8, 2, false>},   {8, 4, k_loop<8, 4, false>},
+    {8, 8, k_loop<8, 8, false>},   {8, 10, k_loop<8, 10, false>}, {16, 2, k_loop<16, 2, false>},
+    {16, 4, k_loop<16, 4, false>}, {16, 5, k_loop<16, 5, false>},
+};
+const LoopVariant kVariantsRes[] = {
+    {1, 32, k_loop<1, 32, true>}, {2, 32, k_loop<2, 32, true>}, {4, 20, k_loop<4, 20, true>},
+    {8, 10, k_loop<8, 10, true>}, {16, 5, k_loop<16, 5, true>},
+};
+// smallest instantiated RRMAX >= want for this CB (want <= rr_max_for(cb))
+const LoopVariant *pick_variant(int cb, int want, bool resmode) {
+    const LoopVariant *best = nullptr;
+    if (resmode) {
+        for (const auto &v : kVariantsRes)
+            if (v.cb == cb) best = &v;
+        return best;
     }
+    for (const auto &v : kVariants)
+        if (v.cb == cb && v.rrmax >= want && (!best || v.rrmax < best->rrmax)) best = &v;
+    return best;
 }
 
 __global__ void k_sumsq_loop(const double *v, int64_t len, double *out) {
@@ -571,9 +630,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
                       int64_t n, double *x, const double *x_star, double tol, int64_t max_iters,
                       const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream) {
     const bool resmode = (x_star == nullptr);
-    // group width and columns per thread: the fewest warps per group with n <= 32 WPG 16
+    // group width: the fewest warps per group with n <= 256 WPG (<= 8 columns per thread:
+    // fewer copies of x to update than 16 columns, still one warp per group for n <= 256)
     int wpg = 1;
-    while (wpg < kLW && 32 * wpg * 16 < n) wpg *= 2;
+    while (wpg < kLW && 32 * wpg * 8 < n) wpg *= 2;
     if (opts && opts->group_warps > 0) {
         if (opts->group_warps > kLW || (opts->group_warps & (opts->group_warps - 1)))
             return fail(ctx, CSK_E_ARG, "csk_solve: group_warps must be 1, 2, 4 or 8");
@@ -582,14 +642,8 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     if (32 * wpg * 16 < n) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n too large for the register GEMV");
     int cb = 1;
     while (32 * wpg * cb < n) cb *= 2;
-    LoopFn fn = resmode ? pick_cb<true>(cb) : pick_cb<false>(cb);
-    if (!fn) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
-    CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
-
     int G = opts && opts->num_ctas > 0 ? opts->num_ctas : ctx->num_sms;
     if (G > d) G = static_cast<int>(d);
-    int per = 0;
-    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, 0, &per));
     const int rows_max = static_cast<int>((d + G - 1) / G);
     const int rg = kLW / wpg;
     const int rb = (rows_max + rg - 1) / rg;  // max rows per group
@@ -597,6 +651,11 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     if (opts && opts->reg_rows < 0) rr = 0;
     else if (opts && opts->reg_rows > 0 && opts->reg_rows < rr) rr = opts->reg_rows;
     if (rr > rb) rr = rb;
+    const LoopVariant *var = pick_variant(cb, rr > 0 ? rr : 1, resmode);
+    if (!var) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
+    const LoopFn fn = var->fn;
+    CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
+    int per = 0;
     int rs_fit = 0;
     while (rs_fit < rb - rr &&
            loop_smem(rows_max, wpg, cb, n, rs_fit + 1, G).total <= static_cast<size_t>(ctx->max_smem_optin))
@@ -613,7 +672,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     while ((1ll << kb) < d + 1) ++kb;
 
     const size_t xch_bytes = 3 * kXchWords * 8;
-    const size_t slot_bytes = static_cast<size_t>(2) * G * kSlotDoubles * 8;
+    const size_t slot_bytes = static_cast<size_t>(2) * G * kSlotWords * 8;
     CSK_CHECK(ensure(ctx, ctx->slots, xch_bytes + slot_bytes));
     CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
@@ -625,7 +684,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.At = At; prm.bt = bt; prm.nsq = nsq; prm.d = d; prm.n = n; prm.x = x;
     prm.x_star = x_star; prm.tol = tol; prm.max_iters = max_iters;
     prm.xch = static_cast<unsigned long long *>(ctx->slots.ptr);
-    prm.slots = reinterpret_cast<double *>(static_cast<unsigned char *>(ctx->slots.ptr) + xch_bytes);
+    prm.slots = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(ctx->slots.ptr) + xch_bytes);
     prm.report = static_cast<int64_t *>(ctx->report.ptr);
     prm.bb = bb;
     prm.wpg = wpg;
