@@ -79,6 +79,8 @@ typedef struct {
 /* Optional knobs and debug traces for csk_solve_ex.  Zero-initialise for defaults. */
 #define CSK_SOLVE_ASYNC 1  /* opts->flags: return right after the launch; csk_solve_wait fills the report */
 #define CSK_SOLVE_LEGACY 2 /* opts->flags: the round-1 cluster/DSMEM kernel (shared-memory rows; A/B only) */
+#define CSK_SOLVE_NO_TMEM 4    /* opts->flags: never keep A~ rows in tensor memory */
+#define CSK_SOLVE_FORCE_TMEM 8 /* opts->flags: use the TMEM row tier whenever the layout allows (tests) */
 
 typedef struct {
     int32_t num_ctas;      /* persistent CTAs (<= co-resident limit); 0 = auto */

@@ -58,6 +58,7 @@ struct LoopParams {
     int wpg;                  // warps per row group (1, 2, 4, 8)
     int rr;                   // rows per group held in registers (<= RRMAX)
     int rs;                   // rows per group held in shared memory
+    int rt;                   // rows per group held in tensor memory (TM variants, <= 16)
     int key_bits;             // b
     int rows_max;             // max rows per CTA (sizes the shared-memory carve-up)
     int64_t trace_cap;
@@ -168,9 +169,9 @@ struct Pow2Ceil {
 
 // Shared-memory carve-up (bytes), identical on host and device.
 struct LoopSmem {
-    size_t ctl, mbar, slotbuf, cand, resp, r0tab, btl, invl, dotp, xs, rowbuf, arows, total;
+    size_t ctl, mbar, slotbuf, cand, resp, btl, invl, dotp, xs, rowbuf, arows, total;
 };
-__host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs, int g) {
+__host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs) {
     LoopSmem L;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
@@ -180,7 +181,6 @@ __host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int
     L.slotbuf = take(kSlotWords * 8);
     L.cand = take(kLW * 32);  // [RG][4] doubles
     L.resp = take(16 * 8);
-    L.r0tab = take(static_cast<size_t>(g + 1) * 4);
     L.btl = take(static_cast<size_t>(rows_max) * 8);
     L.invl = take(static_cast<size_t>(rows_max) * 8);
     L.dotp = take(static_cast<size_t>(wpg) * rows_max * 8);
@@ -191,12 +191,38 @@ __host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int
     return L;
 }
 
+// ---- tensor memory (TMEM) as a row tier: each thread keeps whole A~ row slices in its own
+//      TMEM lane (warp w addresses lanes 32 (w mod 4) .. +31; warps w and w + 4 split the 512
+//      columns), 32-bit column pairs hold one double ----
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ double dbl_of(uint32_t lo, uint32_t hi) {
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+}
+
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CB, int RRMAX, bool RESMODE>
+template <int CB, int RRMAX, bool RESMODE, bool TM>
 __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
+    static_assert(!TM || CB == 8, "the TMEM tier is laid out for 8 columns (16 TMEM columns) per row");
     constexpr int V = Pow2Ceil<RRMAX>::v;
     constexpr int LPR = 32 / V;  // lanes per row after the transposed tree
     extern __shared__ __align__(128) unsigned char smem[];
@@ -206,22 +232,24 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const int n = static_cast<int>(p.n);
     const int WPG = p.wpg, TG = 32 * WPG, RG = kLW / WPG;
     const int grp = warp / WPG, wg = warp - grp * WPG, tg = tid - grp * TG;
-    const int64_t r0 = d * cta / G, r1 = d * (cta + 1) / G;
+    // CTA c owns rows [c RM, min((c+1) RM, d)), RM = ceil(d/G): the owner of row i is i / RM
+    const int64_t r0 = static_cast<int64_t>(cta) * p.rows_max;
+    const int64_t r1 = (r0 + p.rows_max < d) ? r0 + p.rows_max : d;
     const int R = static_cast<int>(r1 - r0);
     const int lr0 = R * grp / RG, lr1 = R * (grp + 1) / RG;  // CTA-local rows of this group
     const int ng = lr1 - lr0;
     const int rr = ng < p.rr ? ng : p.rr;
-    const int rs = (ng - rr) < p.rs ? (ng - rr) : p.rs;
+    const int rt = TM ? ((ng - rr) < p.rt ? (ng - rr) : p.rt) : 0;   // rows in TMEM
+    const int rs = (ng - rr - rt) < p.rs ? (ng - rr - rt) : p.rs;
     const int b = p.key_bits;
     const int RM = p.rows_max;
 
-    const LoopSmem L = loop_smem(RM, WPG, CB, n, p.rs, G);
+    const LoopSmem L = loop_smem(RM, WPG, CB, n, p.rs);
     volatile int64_t *ctl = reinterpret_cast<volatile int64_t *>(smem + L.ctl);  // [0..3] B2, [4..5] RES
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L.mbar);
     const unsigned long long *slotbuf = reinterpret_cast<const unsigned long long *>(smem + L.slotbuf);  // winner's slot (TMA)
     double *cand = reinterpret_cast<double *>(smem + L.cand);  // [RG][4]: key bits, lambda, score, rr
     double *resp = reinterpret_cast<double *>(smem + L.resp);
-    int32_t *r0tab = reinterpret_cast<int32_t *>(smem + L.r0tab);
     double *btl = reinterpret_cast<double *>(smem + L.btl);
     double *invl = reinterpret_cast<double *>(smem + L.invl);  // 1/nsq (0: masked row)
     double *dotp = reinterpret_cast<double *>(smem + L.dotp);  // [WPG][RM]
@@ -236,6 +264,19 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         mbar_init(mbar, 1);
         fence_mbar_init();
     }
+    uint32_t tbase = 0;  // this thread's TMEM row area: lane 32 (warp & 3) + lane, 256 columns
+    if constexpr (TM) {
+        uint32_t *taddr_s = reinterpret_cast<uint32_t *>(const_cast<int64_t *>(ctl) + 6);
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(taddr_s))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tbase = *taddr_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(256 * (warp >> 2));
+    }
 
     // ---- prologue: x (registers), x* (smem), b~, nsq (smem), rows into their tiers ----
     double x[CB];
@@ -245,7 +286,6 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         x[q] = c < n ? p.x[c] : 0.0;
     }
     for (int c = tid; c < TG * CB; c += kLT) xs[c] = (!RESMODE && c < n) ? p.x_star[c] : 0.0;
-    for (int c = tid; c <= G; c += kLT) r0tab[c] = static_cast<int32_t>(d * c / G);
     for (int l = tid; l < R; l += kLT) {
         btl[l] = p.bt[r0 + l];
         const double ns = p.nsq[r0 + l];
@@ -261,8 +301,23 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             a[i][q] = (i < rr && c < n) ? src[c] : 0.0;
         }
     }
+    if constexpr (TM) {
+        for (int j = 0; j < rt; ++j) {  // warp-uniform
+            const double *src = p.At + (r0 + lr0 + rr + j) * n;
+            uint32_t v[16];
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                const int c = tg + TG * q;
+                const double a0 = c < n ? src[c] : 0.0;
+                v[2 * q] = static_cast<uint32_t>(__double2loint(a0));
+                v[2 * q + 1] = static_cast<uint32_t>(__double2hiint(a0));
+            }
+            tmem_st16(tbase + 16u * j, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     for (int i = 0; i < rs; ++i) {
-        const double *src = p.At + (r0 + lr0 + rr + i) * n;
+        const double *src = p.At + (r0 + lr0 + rr + rt + i) * n;
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
             const int c = tg + TG * q;
@@ -292,7 +347,6 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const double bb = RESMODE ? *p.bb : 0.0;
     const bool even = (n & 1) == 0;
     const unsigned long long kmask = (1ull << b) - 1ull;
-    const double gd = static_cast<double>(G) / static_cast<double>(d);
 
     int64_t k = 0, last = -1;
     int term = -1;
@@ -326,17 +380,47 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             const int i = lane / LPR;
             if ((lane % LPR) == 0 && i < rr) dotp[wg * RM + lr0 + i] = s;
         }
-        // ---- S6 GEMV: shared-memory rows ----
-        for (int i = 0; i < rs; ++i) {
-            const double *ar = arows + static_cast<size_t>(i) * CB * TG + tg;
-            double s = 0.0;
+        // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
+        if constexpr (TM) {
+            for (int j0 = 0; j0 < rt; j0 += 8) {
+                double acc8[8];
 #pragma unroll
-            for (int q = 0; q < CB; ++q) s = __fma_rn(ar[q * TG], x[q], s);
-            s = lwarp_sum(s);
-            if (lane == 0) dotp[wg * RM + lr0 + rr + i] = s;
+                for (int j = 0; j < 8; ++j) acc8[j] = 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; j += 2) {
+                    if (j0 + j < rt) {
+                        uint32_t v[32];
+                        tmem_ld32(tbase + 16u * (j0 + j), v);
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) {
+                            acc8[j] = __fma_rn(dbl_of(v[2 * q], v[2 * q + 1]), x[q], acc8[j]);
+                            acc8[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q], v[16 + 2 * q + 1]), x[q], acc8[j + 1]);
+                        }
+                    }
+                }
+                const double s = treduce<8>(acc8, lane);
+                const int i = lane >> 2;
+                if ((lane & 3) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
+            }
+        }
+        // ---- S6 GEMV: shared-memory rows, blocks of 8, transposed tree ----
+        for (int i0 = 0; i0 < rs; i0 += 8) {
+            double acc8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                acc8[j] = 0.0;
+                if (i0 + j < rs) {
+                    const double *ar = arows + static_cast<size_t>(i0 + j) * CB * TG + tg;
+#pragma unroll
+                    for (int q = 0; q < CB; ++q) acc8[j] = __fma_rn(ar[q * TG], x[q], acc8[j]);
+                }
+            }
+            const double s = treduce<8>(acc8, lane);
+            const int i = lane >> 2;
+            if ((lane & 3) == 0 && i0 + i < rs) dotp[wg * RM + lr0 + rr + rt + i0 + i] = s;
         }
         // ---- S6 GEMV: streamed rows (L2/HBM), two rows per pass ----
-        for (int i = rr + rs; i < ng; i += 2) {
+        for (int i = rr + rt + rs; i < ng; i += 2) {
             const bool two = i + 1 < ng;
             const double *s0 = p.At + (r0 + lr0 + i) * n;
             const double *s1 = two ? s0 + n : s0;
@@ -465,10 +549,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 if (mx != 0ull) {
                     wrow = static_cast<int64_t>(kmask - (mx & kmask));
                     if (lane == 0) {
-                        int own = static_cast<int>(static_cast<double>(wrow) * gd);
-                        if (own > G - 1) own = G - 1;
-                        while (own + 1 < G && r0tab[own + 1] <= wrow) ++own;
-                        while (own > 0 && r0tab[own] > wrow) --own;
+                        const int own = static_cast<int>(static_cast<uint32_t>(wrow) / static_cast<uint32_t>(RM));
                         // winner's (lambda, score) slot and A~^(ik) -> shared memory, one mbarrier
                         // (odd n: the row is read with plain loads in the update)
                         const uint32_t rb = even ? static_cast<uint32_t>(n) * 8u : 0u;
@@ -571,6 +652,15 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             p.report[3] = last;
         }
     }
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(
+                             *reinterpret_cast<uint32_t *>(const_cast<int64_t *>(ctl) + 6))
+                         : "memory");
+    }
 }
 
 using LoopFn = void (*)(const LoopParams);
@@ -584,18 +674,23 @@ constexpr int rr_max_for(int cb) { return cb >= 16 ? 5 : cb >= 8 ? 10 : cb >= 4 
 struct LoopVariant {
     int cb, rrmax;
     LoopFn fn;
+    bool tm = false;
 };
 const LoopVariant kVariants[] = {
-    {1, 2, k_loop<1, 2, false>},   {1, 8, k_loop<1, 8, false>},   {1, 32, k_loop<1, 32, false>},
-    {2, 2, k_loop<2, 2, false>},   {2, 8, k_loop<2, 8, false>},   {2, 32, k_loop<2, 32, false>},
-    {4, 2, k_loop<4, 2, false>},   {4, 4, k_loop<4, 4, false>},   {4, 8, k_loop<4, 8, false>},
-    {4, 20, k_loop<4, 20, false>}, {8, 2, k_loop<8, 2, false>},   {8, 4, k_loop<8, 4, false>},
-    {8, 8, k_loop<8, 8, false>},   {8, 10, k_loop<8, 10, false>}, {16, 2, k_loop<16, 2, false>},
-    {16, 4, k_loop<16, 4, false>}, {16, 5, k_loop<16, 5, false>},
+    {1, 2, k_loop<1, 2, false, false>},   {1, 8, k_loop<1, 8, false, false>},   {1, 32, k_loop<1, 32, false, false>},
+    {2, 2, k_loop<2, 2, false, false>},   {2, 8, k_loop<2, 8, false, false>},   {2, 32, k_loop<2, 32, false, false>},
+    {4, 2, k_loop<4, 2, false, false>},   {4, 4, k_loop<4, 4, false, false>},   {4, 8, k_loop<4, 8, false, false>},
+    {4, 20, k_loop<4, 20, false, false>}, {8, 2, k_loop<8, 2, false, false>},   {8, 4, k_loop<8, 4, false, false>},
+    {8, 8, k_loop<8, 8, false, false>},   {8, 10, k_loop<8, 10, false, false>}, {16, 2, k_loop<16, 2, false, false>},
+    {16, 4, k_loop<16, 4, false, false>}, {16, 5, k_loop<16, 5, false, false>},
 };
+// TMEM tier variants (8 columns per thread, 8 register rows + 16 TMEM rows per thread)
+constexpr int kTmRegRows = 8, kTmRows = 16;
+const LoopVariant kVariantTm = {8, kTmRegRows, k_loop<8, kTmRegRows, false, true>, true};
+const LoopVariant kVariantTmRes = {8, kTmRegRows, k_loop<8, kTmRegRows, true, true>, true};
 const LoopVariant kVariantsRes[] = {
-    {1, 32, k_loop<1, 32, true>}, {2, 32, k_loop<2, 32, true>}, {4, 20, k_loop<4, 20, true>},
-    {8, 10, k_loop<8, 10, true>}, {16, 5, k_loop<16, 5, true>},
+    {1, 32, k_loop<1, 32, true, false>}, {2, 32, k_loop<2, 32, true, false>}, {4, 20, k_loop<4, 20, true, false>},
+    {8, 10, k_loop<8, 10, true, false>}, {16, 5, k_loop<16, 5, true, false>},
 };
 // smallest instantiated RRMAX >= want for this CB (want <= rr_max_for(cb))
 const LoopVariant *pick_variant(int cb, int want, bool resmode) {
@@ -645,25 +740,41 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     int G = opts && opts->num_ctas > 0 ? opts->num_ctas : ctx->num_sms;
     if (G > d) G = static_cast<int>(d);
     const int rows_max = static_cast<int>((d + G - 1) / G);
+    G = static_cast<int>((d + rows_max - 1) / rows_max);  // every CTA owns >= 1 row
     const int rg = kLW / wpg;
     const int rb = (rows_max + rg - 1) / rg;  // max rows per group
-    int rr = rr_max_for(cb);
-    if (opts && opts->reg_rows < 0) rr = 0;
-    else if (opts && opts->reg_rows > 0 && opts->reg_rows < rr) rr = opts->reg_rows;
-    if (rr > rb) rr = rb;
-    const LoopVariant *var = pick_variant(cb, rr > 0 ? rr : 1, resmode);
+    // row tiers per group: registers, then TMEM (8 columns per thread only), then shared
+    // memory, then re-read from L2/HBM
+    const int flags = opts ? opts->flags : 0;
+    auto reg_rows = [&](int cap) {
+        int r = cap;
+        if (opts && opts->reg_rows < 0) r = 0;
+        else if (opts && opts->reg_rows > 0 && opts->reg_rows < r) r = opts->reg_rows;
+        return r < rb ? r : rb;
+    };
+    auto smem_fit = [&](int rest) {
+        int f = 0;
+        while (f < rest && loop_smem(rows_max, wpg, cb, n, f + 1).total <= static_cast<size_t>(ctx->max_smem_optin)) ++f;
+        if (opts && opts->smem_rows < 0) f = 0;
+        else if (opts && opts->smem_rows > 0 && opts->smem_rows < f) f = opts->smem_rows;
+        return f;
+    };
+    int rr = reg_rows(rr_max_for(cb));
+    int rt = 0;
+    int rs = smem_fit(rb - rr);
+    const bool allow_tm = cb == 8 && !(flags & CSK_SOLVE_NO_TMEM);
+    if (allow_tm && ((flags & CSK_SOLVE_FORCE_TMEM) || rb - rr > rs)) {
+        rr = reg_rows(kTmRegRows);
+        rt = (rb - rr) < kTmRows ? (rb - rr) : kTmRows;
+        rs = smem_fit(rb - rr - rt);
+    }
+    const LoopVariant *var = rt > 0 ? (resmode ? &kVariantTmRes : &kVariantTm)
+                                    : pick_variant(cb, rr > 0 ? rr : 1, resmode);
     if (!var) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
     const LoopFn fn = var->fn;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
     int per = 0;
-    int rs_fit = 0;
-    while (rs_fit < rb - rr &&
-           loop_smem(rows_max, wpg, cb, n, rs_fit + 1, G).total <= static_cast<size_t>(ctx->max_smem_optin))
-        ++rs_fit;
-    int rs = rs_fit;
-    if (opts && opts->smem_rows < 0) rs = 0;
-    else if (opts && opts->smem_rows > 0 && opts->smem_rows < rs) rs = opts->smem_rows;
-    const size_t smem = loop_smem(rows_max, wpg, cb, n, rs, G).total;
+    const size_t smem = loop_smem(rows_max, wpg, cb, n, rs).total;
     if (smem > static_cast<size_t>(ctx->max_smem_optin))
         return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory (use more CTAs)");
     CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, smem, &per));
@@ -690,6 +801,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.wpg = wpg;
     prm.rr = rr;
     prm.rs = rs;
+    prm.rt = rt;
     prm.key_bits = kb;
     prm.rows_max = rows_max;
     prm.trace_cap = opts ? opts->trace_cap : 0;

@@ -165,6 +165,34 @@ def test_solve_launch_shapes_and_streamed_rows(csk, num_ctas, smem_rows, cluster
     _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 300)
 
 
+@pytest.mark.parametrize("n,d,num_ctas,reg_rows,group_warps", [
+    (200, 1500, 12, 0, 0),    # 8 register + 8 TMEM rows per group
+    (200, 1500, 12, 2, 0),    # 2 register + 14 TMEM rows
+    (201, 1600, 12, 0, 0),    # odd n: TMEM rows, plain-load row update
+    (500, 3000, 10, 0, 0),    # all four tiers: registers, TMEM, shared memory, L2 stream
+    (1000, 2400, 16, 3, 4),   # 4 warps per group (C4's layout), short register tier
+    (2000, 3000, 20, 0, 8)])  # one 8-warp group per CTA (C5's per-GPU layout)
+def test_solve_tmem_tier(csk, n, d, num_ctas, reg_rows, group_warps):
+    """Rows of A~ held in tensor memory (tcgen05.st/ld, 8 columns per thread): same
+    lockstep and free-running bars as the register/shared-memory tiers."""
+    m = max(4 * d, 8 * n)
+    p = make_dense(m, n, "gauss", 500 + n, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, d, seed=5)
+    cap = 20000 if n <= 500 else 300
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=num_ctas, reg_rows=reg_rows,
+                      group_warps=group_warps, tmem=True, trace=min(cap + 1, 400), trace_x=True)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), max_iters=cap,
+                     trace=min(cap + 1, 400))
+    if n <= 500:
+        _free_running(g, o)
+    else:
+        assert g.termination == o.termination == csk.MAX_ITERS
+        assert abs(g.final_res - o.final_res) <= 1e-6 * o.final_res
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 150)
+    n_same = min(len(g.idx_trace), len(o.idx_trace), 400)
+    assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
+
+
 @pytest.mark.parametrize("n", [1, 3, 63, 64, 65, 129, 1023, 2047, 2048])
 def test_solve_ragged_n(csk, n):
     """Ragged widths around the 64-column lane groups and the n <= 2048 register limit.
