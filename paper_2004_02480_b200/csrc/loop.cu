@@ -28,6 +28,7 @@
 //   S8  every CTA reads the winner's (lambda, score) slot, TMA-copies A~^(ik) into shared
 //       memory, and applies x_q += lambda a_ik[c_q] with the same fma in every copy, so all
 //       copies of x stay bit-identical.
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -168,24 +169,30 @@ struct Pow2Ceil {
 };
 
 // Shared-memory carve-up (bytes), identical on host and device.
+constexpr size_t kRowbufOff = 640;
 struct LoopSmem {
     size_t ctl, mbar, slotbuf, cand, resp, btl, invl, dotp, xs, rowbuf, arows, total;
 };
 __host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs) {
+    // The fixed-size control words and the winner-row buffer come first, at compile-time
+    // offsets: the hot loop then addresses them from the shared-memory base without keeping
+    // (or rematerialising) pointers in registers.
     LoopSmem L;
-    size_t o = 0;
-    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+    L.ctl = 0;        // 64 B
+    L.mbar = 64;      // 16 B
+    L.slotbuf = 128;  // 64 B
+    L.cand = 192;     // kLW x 32 B
+    L.resp = 448;     // 16 doubles
+    L.rowbuf = kRowbufOff;
+    size_t o = kRowbufOff;
+    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 127) & ~size_t(127); return r; };  // 128-B aligned
     const int tg = 32 * wpg;
-    L.ctl = take(64);
-    L.mbar = take(16);
-    L.slotbuf = take(kSlotWords * 8);
-    L.cand = take(kLW * 32);  // [RG][4] doubles
-    L.resp = take(16 * 8);
+    const size_t np = static_cast<size_t>(tg) * cb;  // padded width: the row buffer is zero past n
+    take((np > static_cast<size_t>(n) ? np : static_cast<size_t>(n)) * 8);
     L.btl = take(static_cast<size_t>(rows_max) * 8);
     L.invl = take(static_cast<size_t>(rows_max) * 8);
     L.dotp = take(static_cast<size_t>(wpg) * rows_max * 8);
-    L.xs = take(static_cast<size_t>(tg) * cb * 8);
-    L.rowbuf = take(static_cast<size_t>(n + 2) * 8);
+    L.xs = take(np * 8);
     L.arows = take(static_cast<size_t>(rs) * cb * kLT * 8);
     L.total = o;
     return L;
@@ -285,7 +292,10 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         const int c = tg + TG * q;
         x[q] = c < n ? p.x[c] : 0.0;
     }
-    for (int c = tid; c < TG * CB; c += kLT) xs[c] = (!RESMODE && c < n) ? p.x_star[c] : 0.0;
+    for (int c = tid; c < TG * CB; c += kLT) {
+        xs[c] = (!RESMODE && c < n) ? p.x_star[c] : 0.0;
+        if (c >= n) rowbuf[c] = 0.0;  // the TMA writes [0, n); x_q += lambda * 0 past n
+    }
     for (int l = tid; l < R; l += kLT) {
         btl[l] = p.bt[r0 + l];
         const double ns = p.nsq[r0 + l];
@@ -404,7 +414,16 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             }
         }
         // ---- S6 GEMV: shared-memory rows, blocks of 8, transposed tree ----
-        for (int i0 = 0; i0 < rs; i0 += 8) {
+        if constexpr (!TM) {
+            for (int i = 0; i < rs; ++i) {
+                const double *ar = arows + static_cast<size_t>(i) * CB * TG + tg;
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < CB; ++q) s = __fma_rn(ar[q * TG], x[q], s);
+                s = lwarp_sum(s);
+                if (lane == 0) dotp[wg * RM + lr0 + rr + i] = s;
+            }
+        } else for (int i0 = 0; i0 < rs; i0 += 8) {
             double acc8[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -614,11 +633,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         if (cta == 0 && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wrow;
         last = wrow;
         if (even) {
+            const double *rb = reinterpret_cast<const double *>(smem + kRowbufOff) + tg;
 #pragma unroll
-            for (int q = 0; q < CB; ++q) {
-                const int c = tg + TG * q;
-                if (c < n) x[q] = __fma_rn(lam, rowbuf[c], x[q]);
-            }
+            for (int q = 0; q < CB; ++q) x[q] = __fma_rn(lam, rb[TG * q], x[q]);  // zero-padded past n
         } else {
             const double *src = p.At + wrow * n;
 #pragma unroll
@@ -825,6 +842,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     static const bool noncoop = getenv("CSK_PROFILE_NONCOOP") != nullptr;
     if (noncoop) cfg.numAttrs = 0;
     CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, prm));
+    static const bool dbg = getenv("CSK_DEBUG") != nullptr;
+    if (dbg)
+        fprintf(stderr, "[csk] loop: d=%lld n=%lld G=%d wpg=%d cb=%d rrmax=%d tm=%d rr=%d rt=%d rs=%d rows/CTA=%d smem=%zu\n",
+                (long long)d, (long long)n, G, wpg, cb, var->rrmax, (int)var->tm, rr, rt, rs, rows_max, smem);
     ctx->last_solve_geom[0] = G;
     ctx->last_solve_geom[1] = 1;
     ctx->last_solve_geom[2] = rs;
