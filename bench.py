@@ -34,6 +34,7 @@ from csk_synth import CONFIGS, make_config  # noqa: E402
 
 METRIC = "CSK time-to-1e-6 rel err (sketch+iterate); iterations/s; sketch HBM GB/s"
 SMEM_BYTES_PER_CLK_PER_SM = 128  # B300_MICROARCH.md "smem crossbar BW 128/N B/cyc/SM"
+DFMA_PER_CLK_PER_SM = 64         # measured 63.4 (profiles/r01_microbench_k7b.txt, tools/microbench_dfma.cu)
 
 
 def _peaks():
@@ -223,10 +224,14 @@ def run_ours(args, dist, rank, ws):
     it = reps[-1].iterations
     assert all(r.iterations == it for r in reps), "non-deterministic iteration count"
 
-    # roofline: the dominant kernel is the solve loop (A~ resident in SMEM at C1-C3)
+    # roofline: the dominant kernel is the persistent loop k_loop (A~ on chip: registers at
+    # C1-C3; registers + TMEM + shared memory at C4).  north_star frames it as the bytes of A~
+    # per iteration over the on-chip (SMEM/L2) bandwidth; the FP64 FMA bound is reported beside.
     loop_bytes = alg_bytes_iter(cfg) * it
     loop_gbs = loop_bytes / (sv_ms * 1e-3) / 1e9
     smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
+    loop_tflops = 2.0 * cfg.d * cfg.n * it / (sv_ms * 1e-3) / 1e12
+    fp64_peak = 148 * DFMA_PER_CLK_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
     sketch_gbs = alg_bytes_sketch(cfg) / (sk_ms * 1e-3) / 1e9
     out = {
         "metric": METRIC,
@@ -253,14 +258,21 @@ def run_ours(args, dist, rank, ws):
         "solve_ms": round(sv_ms, 5),
         "sketch_hbm_gbs": round(sketch_gbs, 1),
         "us_per_iteration": round(sv_ms * 1e3 / max(it, 1), 4),
-        "roofline": {"kernel": "k_solve (persistent loop)", "bound": "smem",
+        "roofline": {"kernel": "k_loop (persistent Algorithm 1 loop, A~ on chip)", "bound": "smem",
                      "achieved": round(loop_gbs, 1),
                      "peak": round(smem_peak, 1), "unit": "GB/s", "frac": round(loop_gbs / smem_peak, 4),
-                     "traffic": _ncu_traffic(f"r01_ncu_solve_{cfg.name}.txt"),
-                     "traffic_note": "DRAM bytes of the whole k_solve launch (one launch = the whole loop): "
-                                     "A~ is read once into shared memory and stays on chip",
+                     "traffic": _ncu_traffic(f"r01_ncu_loop_{cfg.name}.txt"),
+                     "traffic_note": "DRAM bytes of the whole k_loop launch (one launch = the whole loop): "
+                                     "A~ is read once into registers/TMEM/shared memory and stays on chip",
                      "peak_source": f"derived: 148 SM x {SMEM_BYTES_PER_CLK_PER_SM} B/clk x {sm_max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                      "alg_bytes_per_iteration": alg_bytes_iter(cfg)},
+        "roofline_fp64": {"kernel": "k_loop", "bound": "alu", "achieved": round(loop_tflops, 3),
+                          "peak": round(fp64_peak, 2), "unit": "TFLOP/s", "frac": round(loop_tflops / fp64_peak, 4),
+                          "peak_source": f"derived: 148 SM x {DFMA_PER_CLK_PER_SM} DFMA/clk x 2 x {sm_max_mhz:.0f} MHz "
+                                         "(63.4 DFMA/clk/SM measured, profiles/r01_microbench_k7b.txt)",
+                          "alg_flops_per_iteration": 2 * cfg.d * cfg.n,
+                          "note": "the loop is latency-bound: one grid-wide exchange (atomic max-key + count, "
+                                  "~2.3k cycles floor measured) per iteration"},
         "roofline_sketch": {"kernel": "plan + k_sketch_dense", "bound": "hbm",
                             "achieved": round(sketch_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                             "frac": round(sketch_gbs / hbm_peak, 4), "peak_source": peak_src,
@@ -268,7 +280,7 @@ def run_ours(args, dist, rank, ws):
                             "traffic": _ncu_traffic(f"r01_ncu_sketch_{cfg.name}.txt")},
         "clocks": clocks,
         "gpu_launches": 4 * args.steps,
-        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_solve (+ CUB onesweep radix-sort kernels and one memset)",
+        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB onesweep radix-sort kernels and one memset)",
     }
 
     # ---- e2e: the public API with HOST buffers, copies inside the timed region
