@@ -67,6 +67,7 @@ struct LoopParams {
     double *res_trace;
     double *x_trace;
     int64_t *phase_cycles;    // debug (libcsk_prof.so only): [2 warps][16] SM-cycle totals of CTA 0
+    long long *skew;          // debug (libcsk_prof.so only): [64 iterations][2][G] globaltimer ns
 };
 
 // ---- PTX helpers specific to the exchange ----
@@ -212,6 +213,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// Issue only; the registers are written asynchronously until tmem_wait_ld(v), which names
+// them as operands so the compiler cannot read them before the wait.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+                   "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                   "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+                 :
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
@@ -221,6 +243,22 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 }
 __device__ __forceinline__ double dbl_of(uint32_t lo, uint32_t hi) {
     return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+}
+
+// NB shared-memory rows (from i0, clamped to rs-1) folded against x: columns outer, rows inner.
+template <int NB, int CB>
+__device__ __forceinline__ void smem_block(const double *ar_tg, int i0, int rs, int TG, const double (&x)[CB],
+                                           double (&acc)[NB]) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < CB; ++q) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int jj = (i0 + j < rs) ? i0 + j : rs - 1;
+            acc[j] = __fma_rn(ar_tg[(static_cast<size_t>(jj) * CB + q) * TG], x[q], acc[j]);
+        }
+    }
 }
 
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
@@ -362,6 +400,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     int term = -1;
     double res = 0.0;
     uint32_t mphase = 0;
+    double lam = 0.0;      // lambda of the pending update x += lam A~^(prow)
+    int64_t prow = -1;     // row of the pending update (-1: none)
+    int *arrive = reinterpret_cast<int *>(const_cast<int64_t *>(ctl) + 7);  // group arrivals (smem)
+    if (tid == 0) *arrive = 0;
+    __syncthreads();
 #if CSK_PHASE_PROF
     const bool prof = p.phase_cycles != nullptr && cta == 0 && lane == 0 && (warp == 0 || warp == kLW - 1);
     long long ph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -376,6 +419,39 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
 #define LP(i)
 #endif
     for (;; ++k) {
+        // ---- S8 of iteration k-1, fused at the top of iteration k: x_q += lambda a_{i_{k-1}}[c_q]
+        //      (the row is in the fixed-offset row buffer, zero past n; odd n: from L2) ----
+        if (prow >= 0) {
+            if (even) {
+                const double *rb = reinterpret_cast<const double *>(smem + kRowbufOff) + tg;
+#pragma unroll
+                for (int q = 0; q < CB; ++q) x[q] = __fma_rn(lam, rb[TG * q], x[q]);
+            } else {
+                const double *src = p.At + prow * n;
+#pragma unroll
+                for (int q = 0; q < CB; ++q) {
+                    const int c = tg + TG * q;
+                    if (c < n) x[q] = __fma_rn(lam, ldg_stream1(src + c), x[q]);
+                }
+            }
+        }
+        LP(7)
+        // ---- S5 partial (last group): ||x_k - x*||^2, combined by the group's finalize warp ----
+        double e2 = 0.0;
+        if (!RESMODE && resgrp) {
+            if (cta == 0 && p.x_trace && k < p.trace_cap) {
+#pragma unroll
+                for (int q = 0; q < CB; ++q) {
+                    const int c = tg + TG * q;
+                    if (c < n) p.x_trace[k * n + c] = x[q];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                const double e = x[q] - xs[tg + TG * q];
+                e2 = __fma_rn(e, e, e2);
+            }
+        }
         // ---- S6 GEMV: register rows (transposed tree: row i ends in lanes [i LPR, (i+1) LPR)) ----
         {
             double acc[V];
@@ -392,22 +468,37 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         }
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
         if constexpr (TM) {
+            // 8-row blocks; rows past rt read unused columns of this thread's TMEM area (never
+            // written back).  The next pair's tcgen05.ld is in flight while the current pair is
+            // folded; each row folds its two column halves in separate chains (4 chains/pair).
             for (int j0 = 0; j0 < rt; j0 += 8) {
-                double acc8[8];
+                double lo[8], hi[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc8[j] = 0.0;
+                for (int j = 0; j < 8; ++j) lo[j] = hi[j] = 0.0;
+                uint32_t v[32];
+                tmem_ld32_async(tbase + 16u * j0, v);
+                tmem_wait_ld(v);
 #pragma unroll
                 for (int j = 0; j < 8; j += 2) {
-                    if (j0 + j < rt) {
-                        uint32_t v[32];
-                        tmem_ld32(tbase + 16u * (j0 + j), v);
+                    uint32_t w[32];
+                    if (j + 2 < 8) tmem_ld32_async(tbase + 16u * (j0 + j + 2), w);
 #pragma unroll
-                        for (int q = 0; q < CB; ++q) {
-                            acc8[j] = __fma_rn(dbl_of(v[2 * q], v[2 * q + 1]), x[q], acc8[j]);
-                            acc8[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q], v[16 + 2 * q + 1]), x[q], acc8[j + 1]);
-                        }
+                    for (int q = 0; q < CB / 2; ++q) {
+                        const int q2 = q + CB / 2;
+                        lo[j] = __fma_rn(dbl_of(v[2 * q], v[2 * q + 1]), x[q], lo[j]);
+                        lo[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q], v[16 + 2 * q + 1]), x[q], lo[j + 1]);
+                        hi[j] = __fma_rn(dbl_of(v[2 * q2], v[2 * q2 + 1]), x[q2], hi[j]);
+                        hi[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q2], v[16 + 2 * q2 + 1]), x[q2], hi[j + 1]);
+                    }
+                    if (j + 2 < 8) {
+                        tmem_wait_ld(w);
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) v[t] = w[t];
                     }
                 }
+                double acc8[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc8[j] = lo[j] + hi[j];
                 const double s = treduce<8>(acc8, lane);
                 const int i = lane >> 2;
                 if ((lane & 3) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
@@ -423,20 +514,26 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 s = lwarp_sum(s);
                 if (lane == 0) dotp[wg * RM + lr0 + rr + i] = s;
             }
-        } else for (int i0 = 0; i0 < rs; i0 += 8) {
-            double acc8[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                acc8[j] = 0.0;
-                if (i0 + j < rs) {
-                    const double *ar = arows + static_cast<size_t>(i0 + j) * CB * TG + tg;
-#pragma unroll
-                    for (int q = 0; q < CB; ++q) acc8[j] = __fma_rn(ar[q * TG], x[q], acc8[j]);
+        } else {
+            // blocks of 8 (a tail of <= 4 rows: a block of 4), columns outer so the block's rows
+            // form independent fma chains; rows past rs re-read row rs-1 (never written back)
+            for (int i0 = 0; i0 < rs;) {
+                if (rs - i0 > 4) {
+                    double acc8[8];
+                    smem_block<8, CB>(arows + tg, i0, rs, TG, x, acc8);
+                    const double s = treduce<8>(acc8, lane);
+                    const int i = lane >> 2;
+                    if ((lane & 3) == 0 && i0 + i < rs) dotp[wg * RM + lr0 + rr + rt + i0 + i] = s;
+                    i0 += 8;
+                } else {
+                    double acc4[4];
+                    smem_block<4, CB>(arows + tg, i0, rs, TG, x, acc4);
+                    const double s = treduce<4>(acc4, lane);
+                    const int i = lane >> 3;
+                    if ((lane & 7) == 0 && i0 + i < rs) dotp[wg * RM + lr0 + rr + rt + i0 + i] = s;
+                    i0 += 4;
                 }
             }
-            const double s = treduce<8>(acc8, lane);
-            const int i = lane >> 2;
-            if ((lane & 3) == 0 && i0 + i < rs) dotp[wg * RM + lr0 + rr + rt + i0 + i] = s;
         }
         // ---- S6 GEMV: streamed rows (L2/HBM), two rows per pass ----
         for (int i = rr + rt + rs; i < ng; i += 2) {
@@ -488,27 +585,15 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 cand[grp * 4 + 2] = bs;
             }
             if (RESMODE && lane == 0) cand[grp * 4 + 3] = rr2;
+            LP(0)
+            // ---- arrival: the LAST group to finish combines the CTA candidate and runs the
+            //      exchange (no CTA barrier before the publish) ----
         }
-        LP(0)
         __syncthreads();  // B1
-        LP(1)
-
-        // ---- S5 (last group, overlapping warp 0's exchange): RES_k = ||x_k - x*||^2/||x*||^2
-        //      (P:180); every CTA computes the same value, so all stop at the same k ----
-        if (!RESMODE && resgrp) {
-            if (cta == 0 && p.x_trace && k < p.trace_cap) {
-#pragma unroll
-                for (int q = 0; q < CB; ++q) {
-                    const int c = tg + TG * q;
-                    if (c < n) p.x_trace[k * n + c] = x[q];
-                }
-            }
-            double e2 = 0.0;
-#pragma unroll
-            for (int q = 0; q < CB; ++q) {
-                const double e = x[q] - xs[tg + TG * q];
-                e2 = __fma_rn(e, e, e2);
-            }
+        // ---- S5 (last group, beside warp 0's exchange): RES_k = ||x_k - x*||^2/||x*||^2;
+        //      every CTA computes the same value from its own copy of x, so all stop at the same k
+        // (RG = 1: warp 0 belongs to the only group and joins before its exchange)
+        if (!RESMODE && resgrp && (RG == 1 || warp != 0)) {
             e2 = lwarp_sum(e2);
             if (WPG > 1) {
                 if (lane == 0) resp[wg] = e2;
@@ -523,85 +608,106 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 if (cta == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = rk;
             }
         }
-        // ---- S7 exchange (warp 0) ----
         if (warp == 0) {
-            int stop = (!RESMODE && k == p.max_iters) ? CSK_MAX_ITERS : -1;
-            int64_t wrow = -1;
-            if (stop < 0) {
-                // CTA candidate: max key over the RG group candidates
-                const unsigned long long ck =
-                    lane < RG ? static_cast<unsigned long long>(__double_as_longlong(cand[lane * 4])) : 0ull;
-                unsigned long long km;
-                const int cl = warp_max_key_lane(ck, km);
-                const double cl_l = cand[cl * 4 + 1], cl_s = cand[cl * 4 + 2];
-                double crr = 0.0;
-                if (RESMODE)
-                    for (int g = 0; g < RG; ++g) crr = crr + cand[g * 4 + 3];
-                unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
-                unsigned long long *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotWords;
-                const uint32_t tag = static_cast<uint32_t>(k + 1);
-                if (lane == 0) {
-                    if (cta == 0) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
-                    red_max_u64(pair + 1, km);
-                    red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
-                    // the slot needs no ordering: readers validate its LL tags
-                    unsigned long long *my = slot_k + static_cast<size_t>(cta) * kSlotWords;
-                    unsigned long long h0, l0, h1, l1;
-                    ll_pack(cl_l, tag, h0, l0);
-                    ll_pack(cl_s, tag, h1, l1);
-                    st_relaxed_v2_u64(my, h0, l0);
-                    st_relaxed_v2_u64(my + 2, h1, l1);
-                    if (RESMODE) {
-                        ll_pack(crr, tag, h0, l0);
-                        st_relaxed_v2_u64(my + 4, h0, l0);
-                    }
-                }
-                LP(2)
-                unsigned long long c, mx;
-                do {  // relaxed polls (an acquire load would invalidate L1 on every poll) ...
-                    ld_relaxed_v2(pair, c, mx);
-                } while (c < static_cast<unsigned long long>(G));
-                // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the proxy
-                // fence orders this thread's generic view before its TMA reads
-                fence_proxy_async_global();
-                LP(3)
-                if (mx != 0ull) {
-                    wrow = static_cast<int64_t>(kmask - (mx & kmask));
+            {
+                LP(1)
+                int stop = (!RESMODE && k == p.max_iters) ? CSK_MAX_ITERS : -1;
+                int64_t wrow = -1;
+                if (stop < 0) {
+                    // CTA candidate: max key over the RG group candidates
+                    const unsigned long long ck =
+                        lane < RG ? static_cast<unsigned long long>(__double_as_longlong(cand[lane * 4])) : 0ull;
+                    unsigned long long kc;
+                    const int cl = warp_max_key_lane(ck, kc);
+                    const double cl_l = cand[cl * 4 + 1], cl_s = cand[cl * 4 + 2];
+                    double crr = 0.0;
+                    if (RESMODE)
+                        for (int g = 0; g < RG; ++g) crr = crr + cand[g * 4 + 3];
+                    unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
+                    unsigned long long *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotWords;
+                    const uint32_t tag = static_cast<uint32_t>(k + 1);
                     if (lane == 0) {
-                        const int own = static_cast<int>(static_cast<uint32_t>(wrow) / static_cast<uint32_t>(RM));
-                        // winner's (lambda, score) slot and A~^(ik) -> shared memory, one mbarrier
-                        // (odd n: the row is read with plain loads in the update)
-                        const uint32_t rb = even ? static_cast<uint32_t>(n) * 8u : 0u;
-                        mbar_arrive_expect_tx(mbar, rb + 32u);
-                        bulk_g2s(const_cast<unsigned long long *>(slotbuf), slot_k + static_cast<size_t>(own) * kSlotWords, 32u, mbar);
-                        if (even) bulk_g2s(rowbuf, p.At + wrow * n, rb, mbar);
-                        ctl[2] = own;
+                        if (cta == 0) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                        red_max_u64(pair + 1, kc);
+                        red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
+                        // the slot needs no ordering: readers validate its LL tags
+                        unsigned long long *my = slot_k + static_cast<size_t>(cta) * kSlotWords;
+                        unsigned long long h0, l0, h1, l1;
+                        ll_pack(cl_l, tag, h0, l0);
+                        ll_pack(cl_s, tag, h1, l1);
+                        st_relaxed_v2_u64(my, h0, l0);
+                        st_relaxed_v2_u64(my + 2, h1, l1);
+                        if (RESMODE) {
+                            ll_pack(crr, tag, h0, l0);
+                            st_relaxed_v2_u64(my + 4, h0, l0);
+                        }
                     }
+                    LP(2)
+#if CSK_PHASE_PROF
+                    if (p.skew && lane == 0 && k >= 8 && k < 72) {
+                        unsigned long long gt;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+                        p.skew[(k - 8) * 2 * G + cta] = static_cast<long long>(gt);
+                    }
+#endif
+                    unsigned long long c, mx;
+                    do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
+                        ld_relaxed_v2(pair, c, mx);
+                    } while (c < static_cast<unsigned long long>(G));
+                    // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the
+                    // proxy fence orders this thread's generic view before its TMA reads
+                    fence_proxy_async_global();
+                    LP(3)
+#if CSK_PHASE_PROF
+                    if (p.skew && lane == 0 && k >= 8 && k < 72) {
+                        unsigned long long gt;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+                        p.skew[(k - 8) * 2 * G + G + cta] = static_cast<long long>(gt);
+                    }
+#endif
+                    if (mx != 0ull) {
+                        wrow = static_cast<int64_t>(kmask - (mx & kmask));
+                        if (lane == 0) {
+                            const int own = static_cast<int>(static_cast<uint32_t>(wrow) / static_cast<uint32_t>(RM));
+                            // winner's (lambda, score) slot and A~^(ik) -> shared memory, one mbarrier
+                            // (odd n: the row is read with plain loads in the update)
+                            const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
+                            mbar_arrive_expect_tx(mbar, rbytes + 32u);
+                            bulk_g2s(const_cast<unsigned long long *>(slotbuf), slot_k + static_cast<size_t>(own) * kSlotWords, 32u, mbar);
+                            if (even) bulk_g2s(rowbuf, p.At + wrow * n, rbytes, mbar);
+                            ctl[2] = own;
+                        }
+                    }
+                    if (RESMODE) {
+                        // ||r_k||^2: the G CTA partials in fixed order
+                        double t = 0.0;
+                        for (int cc = lane; cc < G; cc += 32) t = t + ll_load(slot_k + static_cast<size_t>(cc) * kSlotWords + 4, tag);
+                        t = lwarp_sum(t);
+                        res = bb > 0.0 ? t / bb : t;
+                        if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                        if (res <= p.tol) stop = CSK_CONVERGED;
+                        else if (k == p.max_iters) stop = CSK_MAX_ITERS;
+                    }
+                    if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
+                    if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copies
                 }
-                if (RESMODE) {
-                    // ||r_k||^2: the G CTA partials in fixed order
-                    double t = 0.0;
-                    for (int cc = lane; cc < G; cc += 32) t = t + ll_load(slot_k + static_cast<size_t>(cc) * kSlotWords + 4, tag);
-                    t = lwarp_sum(t);
-                    res = bb > 0.0 ? t / bb : t;
-                    if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
-                    if (res <= p.tol) stop = CSK_CONVERGED;
-                    else if (k == p.max_iters) stop = CSK_MAX_ITERS;
+                if (lane == 0) {
+                    ctl[0] = stop;  // -1: copies in flight on mbar
+                    ctl[1] = wrow;
+                    ctl[3] = __double_as_longlong(res);
+                    *arrive = 0;
                 }
-                if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
-                if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copies
-            }
-            if (lane == 0) {
-                ctl[0] = stop;  // -1: copies in flight on mbar
-                ctl[1] = wrow;
-                ctl[3] = __double_as_longlong(res);
             }
         }
         LP(4)
         __syncthreads();  // B2
         LP(5)
         int stop = static_cast<int>(ctl[0]);
-        double lam = 0.0;
+        prow = -1;
+        if (!RESMODE && ctl[4] == CSK_CONVERGED) {  // RES_k <= tol: no update
+            if (stop == -1) mbar_wait(mbar, mphase);  // drain the copies of the exchange
+            stop = CSK_CONVERGED;
+        }
         if (stop == -1) {  // the winner's slot (and row) arrive on the mbarrier
             mbar_wait(mbar, mphase);
             mphase ^= 1u;
@@ -618,33 +724,16 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             if (sc == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
         }
         LP(6)
-        if (!RESMODE) {
-            res = __longlong_as_double(ctl[5]);
-            if (ctl[4] == CSK_CONVERGED) stop = CSK_CONVERGED;  // RES_k <= tol: no update
-        } else {
-            res = __longlong_as_double(ctl[3]);
-        }
+        if (!RESMODE) res = __longlong_as_double(ctl[5]);
+        else res = __longlong_as_double(ctl[3]);
         if (stop != -1) {
             term = stop;
             break;
         }
-        // ---- S8: x += lambda A~^(ik) ----
         const int64_t wrow = ctl[1];
         if (cta == 0 && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wrow;
         last = wrow;
-        if (even) {
-            const double *rb = reinterpret_cast<const double *>(smem + kRowbufOff) + tg;
-#pragma unroll
-            for (int q = 0; q < CB; ++q) x[q] = __fma_rn(lam, rb[TG * q], x[q]);  // zero-padded past n
-        } else {
-            const double *src = p.At + wrow * n;
-#pragma unroll
-            for (int q = 0; q < CB; ++q) {
-                const int c = tg + TG * q;
-                if (c < n) x[q] = __fma_rn(lam, ldg_stream1(src + c), x[q]);
-            }
-        }
-        LP(7)
+        prow = wrow;
     }
 #undef LP
 #if CSK_PHASE_PROF
@@ -702,7 +791,7 @@ const LoopVariant kVariants[] = {
     {16, 4, k_loop<16, 4, false, false>}, {16, 5, k_loop<16, 5, false, false>},
 };
 // TMEM tier variants (8 columns per thread, 8 register rows + 16 TMEM rows per thread)
-constexpr int kTmRegRows = 8, kTmRows = 16;
+constexpr int kTmRegRows = 6, kTmRows = 16;
 const LoopVariant kVariantTm = {8, kTmRegRows, k_loop<8, kTmRegRows, false, true>, true};
 const LoopVariant kVariantTmRes = {8, kTmRegRows, k_loop<8, kTmRegRows, true, true>, true};
 const LoopVariant kVariantsRes[] = {
@@ -826,6 +915,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.res_trace = opts ? opts->res_trace : nullptr;
     prm.x_trace = opts ? opts->x_trace : nullptr;
     prm.phase_cycles = opts ? opts->phase_cycles : nullptr;
+    prm.skew = (opts && opts->phase_cycles) ? reinterpret_cast<long long *>(opts->phase_cycles) + 32 : nullptr;
     if (prm.trace_cap <= 0) { prm.idx_trace = nullptr; prm.res_trace = nullptr; prm.x_trace = nullptr; prm.trace_cap = 0; }
 
     cudaLaunchConfig_t cfg = {};

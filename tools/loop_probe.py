@@ -15,7 +15,7 @@ import torch  # noqa: E402
 import paper_2004_02480_b200 as csk  # noqa: E402
 from csk_synth import CONFIGS, make_config  # noqa: E402
 
-NAMES = ["gemv+final", "B1", "combine+publish", "spin", "post", "B2", "rowwait", "upd"]
+NAMES = ["gemv+final", "arrive(leader)", "combine+publish", "spin", "post", "B2", "rowwait", "upd"]
 
 
 def main():
@@ -34,7 +34,7 @@ def main():
         cap = cfg.max_iters if nm != "C4" else 3000
         for G, wpg in [(g, w) for g in ctas for w in wpgs]:
             csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, group_warps=wpg)
-            ph = torch.zeros(32, dtype=torch.int64, device="cuda")
+            ph = torch.zeros(32 + 64 * 2 * 160, dtype=torch.int64, device="cuda")
             st = torch.cuda.Event(enable_timing=True)
             en = torch.cuda.Event(enable_timing=True)
             st.record()
@@ -46,6 +46,15 @@ def main():
             ms = st.elapsed_time(en)
             it = max(r.iterations, 1)
             c = ph.cpu().tolist()
+            geoG = csk.csk_last_solve_geometry()["num_ctas"]
+            sk = ph[32:32 + 64 * 2 * geoG].view(64, 2, geoG).cpu().double()
+            if r.iterations > 72:
+                pub, done = sk[:, 0, :], sk[:, 1, :]
+                spread = (pub.max(1).values - pub.min(1).values).mean().item()
+                lastpub_to_done = (done.min(1).values - pub.max(1).values).mean().item()
+                done_spread = (done.max(1).values - done.min(1).values).mean().item()
+                print(f"   skew (ns, mean over 64 iterations): publish spread {spread:.0f}, last publish -> first "
+                      f"spin exit {lastpub_to_done:.0f}, spin-exit spread {done_spread:.0f}")
             w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(8))
             w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(9) if c[16 + i])
             print(f"{nm} G={geo['num_ctas']} wpg={wpg} IT={r.iterations} {ms * 1e3 / it:.2f} us/it = "
