@@ -170,7 +170,11 @@ struct Pow2Ceil {
 };
 
 // Shared-memory carve-up (bytes), identical on host and device.
-constexpr size_t kRowbufOff = 640;
+constexpr int kCS = 16;               // cluster size of the cluster-exchange variant
+constexpr int64_t kCluMaxElems = 640 * 1024;  // d n up to which one 16-SM cluster beats 148 SMs
+constexpr size_t kInboxOff = 576;      // [2 parities][kCS][4] doubles: key, lambda, score, rr
+constexpr size_t kXbarOff = 1600;      // 2 mbarriers (one per parity), kCS arrivals each
+constexpr size_t kRowbufOff = 1664;
 struct LoopSmem {
     size_t ctl, mbar, slotbuf, cand, resp, btl, invl, dotp, xs, rowbuf, arows, total;
 };
@@ -261,12 +265,33 @@ __device__ __forceinline__ void smem_block(const double *ar_tg, int i0, int rs, 
     }
 }
 
+// ---- cluster (DSMEM) exchange helpers ----
+// 16-byte asynchronous store into a peer's shared memory that completes `bytes` on the peer's
+// mbarrier (no fence, no arrival: the receiver armed the barrier with expect_tx)
+__device__ __forceinline__ void st_async_v2_f64(uint32_t cluster_addr, double a, double b, uint32_t cluster_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(cluster_addr),
+                 "d"(a), "d"(b), "r"(cluster_mbar)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CB, int RRMAX, bool RESMODE, bool TM>
+template <int CB, int RRMAX, bool RESMODE, bool TM, bool CLU>
 __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
+    // CLU: the whole grid is one kCS-CTA thread-block cluster and the exchange is an
+    // all-to-all of the CTA candidates over DSMEM (no global atomics)
     static_assert(!TM || CB == 8, "the TMEM tier is laid out for 8 columns (16 TMEM columns) per row");
     constexpr int V = Pow2Ceil<RRMAX>::v;
     constexpr int LPR = 32 / V;  // lanes per row after the transposed tree
@@ -278,7 +303,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const int WPG = p.wpg, TG = 32 * WPG, RG = kLW / WPG;
     const int grp = warp / WPG, wg = warp - grp * WPG, tg = tid - grp * TG;
     // CTA c owns rows [c RM, min((c+1) RM, d)), RM = ceil(d/G): the owner of row i is i / RM
-    const int64_t r0 = static_cast<int64_t>(cta) * p.rows_max;
+    const int64_t r0 = (static_cast<int64_t>(cta) * p.rows_max < d) ? static_cast<int64_t>(cta) * p.rows_max : d;
     const int64_t r1 = (r0 + p.rows_max < d) ? r0 + p.rows_max : d;
     const int R = static_cast<int>(r1 - r0);
     const int lr0 = R * grp / RG, lr1 = R * (grp + 1) / RG;  // CTA-local rows of this group
@@ -307,8 +332,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
         if (L.total > dyn) __trap();
         mbar_init(mbar, 1);
+        if (CLU) {  // one local arrival (the expect_tx) per phase; the peers' st.async bring the bytes
+            mbar_init(reinterpret_cast<uint64_t *>(smem + kXbarOff), 1);
+            mbar_init(reinterpret_cast<uint64_t *>(smem + kXbarOff) + 1, 1);
+        }
         fence_mbar_init();
     }
+    if (CLU) cluster_sync_all();  // every peer's exchange barriers exist before the first arrival
     uint32_t tbase = 0;  // this thread's TMEM row area: lane 32 (warp & 3) + lane, 256 columns
     if constexpr (TM) {
         uint32_t *taddr_s = reinterpret_cast<uint32_t *>(const_cast<int64_t *>(ctl) + 6);
@@ -505,16 +535,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             }
         }
         // ---- S6 GEMV: shared-memory rows, blocks of 8, transposed tree ----
-        if constexpr (!TM) {
-            for (int i = 0; i < rs; ++i) {
-                const double *ar = arows + static_cast<size_t>(i) * CB * TG + tg;
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < CB; ++q) s = __fma_rn(ar[q * TG], x[q], s);
-                s = lwarp_sum(s);
-                if (lane == 0) dotp[wg * RM + lr0 + rr + i] = s;
-            }
-        } else {
+        {
             // blocks of 8 (a tail of <= 4 rows: a block of 4), columns outer so the block's rows
             // form independent fma chains; rows past rs re-read row rs-1 (never written back)
             for (int i0 = 0; i0 < rs;) {
@@ -623,9 +644,56 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     double crr = 0.0;
                     if (RESMODE)
                         for (int g = 0; g < RG; ++g) crr = crr + cand[g * 4 + 3];
+                    const uint32_t tag = static_cast<uint32_t>(k + 1);
+                    if constexpr (CLU) {
+                        // ---- all-to-all over DSMEM: this CTA arms its barrier of this parity for
+                        //      kCS x 32 bytes, then lane j st.async's the CTA candidate into rank j's
+                        //      inbox, completing the bytes on rank j's barrier ----
+                        const int par = static_cast<int>(k & 1);
+                        double *inbox = reinterpret_cast<double *>(smem + kInboxOff) + par * kCS * 4;
+                        uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + kXbarOff) + par;
+                        if (lane == 0) mbar_arrive_expect_tx(xbar, kCS * 32u);
+                        if (lane < kCS) {
+                            const uint32_t dst = mapa_shared(smem_u32(inbox + cta * 4), static_cast<uint32_t>(lane));
+                            const uint32_t rbar = mapa_shared(smem_u32(xbar), static_cast<uint32_t>(lane));
+                            st_async_v2_f64(dst, __longlong_as_double(static_cast<long long>(kc)), cl_l, rbar);
+                            st_async_v2_f64(dst + 16, cl_s, crr, rbar);
+                        }
+                        LP(2)
+                        while (!mbar_try_wait_cluster(xbar, static_cast<uint32_t>((k >> 1) & 1))) {
+                        }
+                        LP(3)
+                        const unsigned long long kj =
+                            lane < kCS ? static_cast<unsigned long long>(__double_as_longlong(inbox[lane * 4])) : 0ull;
+                        unsigned long long mx;
+                        const int wl = warp_max_key_lane(kj, mx);
+                        const double wlam = inbox[wl * 4 + 1], wsc = inbox[wl * 4 + 2];
+                        if (RESMODE) {
+                            double t = 0.0;
+                            for (int j = 0; j < kCS; ++j) t = t + inbox[j * 4 + 3];  // fixed order
+                            res = bb > 0.0 ? t / bb : t;
+                            if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                            if (res <= p.tol) stop = CSK_CONVERGED;
+                            else if (k == p.max_iters) stop = CSK_MAX_ITERS;
+                        }
+                        if (mx != 0ull) {
+                            wrow = static_cast<int64_t>(kmask - (mx & kmask));
+                            if (lane == 0) {
+                                // the winner's (lambda, score) go to the slot buffer, LL-tagged like
+                                // the global variant's; the row comes by TMA (odd n: plain loads)
+                                unsigned long long *sb = const_cast<unsigned long long *>(slotbuf);
+                                ll_pack(wlam, tag, sb[0], sb[1]);
+                                ll_pack(wsc, tag, sb[2], sb[3]);
+                                const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
+                                mbar_arrive_expect_tx(mbar, rbytes);
+                                if (even) bulk_g2s(rowbuf, p.At + wrow * n, rbytes, mbar);
+                            }
+                        }
+                        if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
+                        if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copy
+                    } else {
                     unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
                     unsigned long long *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotWords;
-                    const uint32_t tag = static_cast<uint32_t>(k + 1);
                     if (lane == 0) {
                         if (cta == 0) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
                         red_max_u64(pair + 1, kc);
@@ -690,6 +758,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
                     if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
                     if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copies
+                    }  // global exchange
                 }
                 if (lane == 0) {
                     ctl[0] = stop;  // -1: copies in flight on mbar
@@ -716,7 +785,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             if (ll_ok(slotbuf[0], slotbuf[1], tag) && ll_ok(slotbuf[2], slotbuf[3], tag)) {
                 lam = ll_val(slotbuf[0], slotbuf[1]);
                 sc = ll_val(slotbuf[2], slotbuf[3]);
-            } else {  // the copy raced the owner's slot store: re-read until the tags match
+            } else if (!CLU) {  // the copy raced the owner's slot store: re-read until the tags match
                 const unsigned long long *gs = p.slots + (static_cast<size_t>(k & 1) * G + ctl[2]) * kSlotWords;
                 lam = ll_load(gs, tag);
                 sc = ll_load(gs + 2, tag);
@@ -767,6 +836,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                              *reinterpret_cast<uint32_t *>(const_cast<int64_t *>(ctl) + 6))
                          : "memory");
     }
+    if (CLU) cluster_sync_all();  // no CTA leaves while a peer could still address its shared memory
 }
 
 using LoopFn = void (*)(const LoopParams);
@@ -781,22 +851,29 @@ struct LoopVariant {
     int cb, rrmax;
     LoopFn fn;
     bool tm = false;
+    bool clu = false;
 };
 const LoopVariant kVariants[] = {
-    {1, 2, k_loop<1, 2, false, false>},   {1, 8, k_loop<1, 8, false, false>},   {1, 32, k_loop<1, 32, false, false>},
-    {2, 2, k_loop<2, 2, false, false>},   {2, 8, k_loop<2, 8, false, false>},   {2, 32, k_loop<2, 32, false, false>},
-    {4, 2, k_loop<4, 2, false, false>},   {4, 4, k_loop<4, 4, false, false>},   {4, 8, k_loop<4, 8, false, false>},
-    {4, 20, k_loop<4, 20, false, false>}, {8, 2, k_loop<8, 2, false, false>},   {8, 4, k_loop<8, 4, false, false>},
-    {8, 8, k_loop<8, 8, false, false>},   {8, 10, k_loop<8, 10, false, false>}, {16, 2, k_loop<16, 2, false, false>},
-    {16, 4, k_loop<16, 4, false, false>}, {16, 5, k_loop<16, 5, false, false>},
+    {1, 2, k_loop<1, 2, false, false, false>},   {1, 8, k_loop<1, 8, false, false, false>},   {1, 32, k_loop<1, 32, false, false, false>},
+    {2, 2, k_loop<2, 2, false, false, false>},   {2, 8, k_loop<2, 8, false, false, false>},   {2, 32, k_loop<2, 32, false, false, false>},
+    {4, 2, k_loop<4, 2, false, false, false>},   {4, 4, k_loop<4, 4, false, false, false>},   {4, 8, k_loop<4, 8, false, false, false>},
+    {4, 20, k_loop<4, 20, false, false, false>}, {8, 2, k_loop<8, 2, false, false, false>},   {8, 4, k_loop<8, 4, false, false, false>},
+    {8, 8, k_loop<8, 8, false, false, false>},   {8, 10, k_loop<8, 10, false, false, false>}, {16, 2, k_loop<16, 2, false, false, false>},
+    {16, 4, k_loop<16, 4, false, false, false>}, {16, 5, k_loop<16, 5, false, false, false>},
 };
 // TMEM tier variants (8 columns per thread, 8 register rows + 16 TMEM rows per thread)
 constexpr int kTmRegRows = 6, kTmRows = 16;
-const LoopVariant kVariantTm = {8, kTmRegRows, k_loop<8, kTmRegRows, false, true>, true};
-const LoopVariant kVariantTmRes = {8, kTmRegRows, k_loop<8, kTmRegRows, true, true>, true};
+const LoopVariant kVariantTm = {8, kTmRegRows, k_loop<8, kTmRegRows, false, true, false>, true};
+const LoopVariant kVariantTmRes = {8, kTmRegRows, k_loop<8, kTmRegRows, true, true, false>, true};
+// single-cluster variants (the whole problem on kCS SMs, DSMEM exchange): C1/C2-sized systems
+const LoopVariant kVariantsClu[] = {
+    {1, 8, k_loop<1, 8, false, false, true>, false, true},   {2, 8, k_loop<2, 8, false, false, true>, false, true},
+    {4, 8, k_loop<4, 8, false, false, true>, false, true},   {8, 10, k_loop<8, 10, false, false, true>, false, true},
+    {16, 5, k_loop<16, 5, false, false, true>, false, true}, {8, kTmRegRows, k_loop<8, kTmRegRows, false, true, true>, true, true},
+};
 const LoopVariant kVariantsRes[] = {
-    {1, 32, k_loop<1, 32, true, false>}, {2, 32, k_loop<2, 32, true, false>}, {4, 20, k_loop<4, 20, true, false>},
-    {8, 10, k_loop<8, 10, true, false>}, {16, 5, k_loop<16, 5, true, false>},
+    {1, 32, k_loop<1, 32, true, false, false>}, {2, 32, k_loop<2, 32, true, false, false>}, {4, 20, k_loop<4, 20, true, false, false>},
+    {8, 10, k_loop<8, 10, true, false, false>}, {16, 5, k_loop<16, 5, true, false, false>},
 };
 // smallest instantiated RRMAX >= want for this CB (want <= rr_max_for(cb))
 const LoopVariant *pick_variant(int cb, int want, bool resmode) {
@@ -843,48 +920,97 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     if (32 * wpg * 16 < n) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n too large for the register GEMV");
     int cb = 1;
     while (32 * wpg * cb < n) cb *= 2;
-    int G = opts && opts->num_ctas > 0 ? opts->num_ctas : ctx->num_sms;
-    if (G > d) G = static_cast<int>(d);
-    const int rows_max = static_cast<int>((d + G - 1) / G);
-    G = static_cast<int>((d + rows_max - 1) / rows_max);  // every CTA owns >= 1 row
-    const int rg = kLW / wpg;
-    const int rb = (rows_max + rg - 1) / rg;  // max rows per group
-    // row tiers per group: registers, then TMEM (8 columns per thread only), then shared
-    // memory, then re-read from L2/HBM
     const int flags = opts ? opts->flags : 0;
-    auto reg_rows = [&](int cap) {
-        int r = cap;
-        if (opts && opts->reg_rows < 0) r = 0;
-        else if (opts && opts->reg_rows > 0 && opts->reg_rows < r) r = opts->reg_rows;
-        return r < rb ? r : rb;
+    const int rg = kLW / wpg;
+    // Geometry for G CTAs: row tiers per group -- registers, then TMEM (8 columns per thread
+    // only), then shared memory, then re-read from L2/HBM.
+    struct Geo {
+        int G, rows_max, rb, rr, rt, rs;
+        size_t smem;
+        const LoopVariant *var;
     };
-    auto smem_fit = [&](int rest) {
-        int f = 0;
-        while (f < rest && loop_smem(rows_max, wpg, cb, n, f + 1).total <= static_cast<size_t>(ctx->max_smem_optin)) ++f;
-        if (opts && opts->smem_rows < 0) f = 0;
-        else if (opts && opts->smem_rows > 0 && opts->smem_rows < f) f = opts->smem_rows;
-        return f;
+    auto geometry = [&](int Gw, bool clu, Geo &g) {
+        g.G = Gw;
+        g.rows_max = static_cast<int>((d + Gw - 1) / Gw);
+        if (!clu) g.G = static_cast<int>((d + g.rows_max - 1) / g.rows_max);  // every CTA owns >= 1 row
+        g.rb = (g.rows_max + rg - 1) / rg;  // max rows per group
+        auto reg_rows = [&](int cap) {
+            int r = cap;
+            if (opts && opts->reg_rows < 0) r = 0;
+            else if (opts && opts->reg_rows > 0 && opts->reg_rows < r) r = opts->reg_rows;
+            return r < g.rb ? r : g.rb;
+        };
+        auto smem_fit = [&](int rest) {
+            int f = 0;
+            while (f < rest && loop_smem(g.rows_max, wpg, cb, n, f + 1).total <= static_cast<size_t>(ctx->max_smem_optin)) ++f;
+            if (opts && opts->smem_rows < 0) f = 0;
+            else if (opts && opts->smem_rows > 0 && opts->smem_rows < f) f = opts->smem_rows;
+            return f;
+        };
+        int rcap = rr_max_for(cb);
+        if (clu) {  // the single-cluster variants carry <= 10 register rows (see kVariantsClu)
+            rcap = 0;
+            for (const auto &v : kVariantsClu)
+                if (v.cb == cb && !v.tm && v.rrmax > rcap) rcap = v.rrmax;
+        }
+        g.rr = reg_rows(rcap);
+        g.rt = 0;
+        g.rs = smem_fit(g.rb - g.rr);
+        const bool allow_tm = cb == 8 && !(flags & CSK_SOLVE_NO_TMEM);
+        if (allow_tm && ((flags & CSK_SOLVE_FORCE_TMEM) || g.rb - g.rr > 0)) {
+            g.rr = reg_rows(kTmRegRows);
+            g.rt = (g.rb - g.rr) < kTmRows ? (g.rb - g.rr) : kTmRows;
+            g.rs = smem_fit(g.rb - g.rr - g.rt);
+        }
+        g.var = nullptr;
+        if (clu) {
+            for (const auto &v : kVariantsClu)
+                if (v.cb == cb && v.tm == (g.rt > 0) && v.rrmax >= (g.rr > 0 ? g.rr : 1) &&
+                    (!g.var || v.rrmax < g.var->rrmax))
+                    g.var = &v;
+        } else {
+            g.var = g.rt > 0 ? (resmode ? &kVariantTmRes : &kVariantTm) : pick_variant(cb, g.rr > 0 ? g.rr : 1, resmode);
+        }
+        g.smem = loop_smem(g.rows_max, wpg, cb, n, g.rs).total;
+        return g.var != nullptr && g.smem <= static_cast<size_t>(ctx->max_smem_optin);
     };
-    int rr = reg_rows(rr_max_for(cb));
-    int rt = 0;
-    int rs = smem_fit(rb - rr);
-    const bool allow_tm = cb == 8 && !(flags & CSK_SOLVE_NO_TMEM);
-    if (allow_tm && ((flags & CSK_SOLVE_FORCE_TMEM) || rb - rr > rs)) {
-        rr = reg_rows(kTmRegRows);
-        rt = (rb - rr) < kTmRows ? (rb - rr) : kTmRows;
-        rs = smem_fit(rb - rr - rt);
+    Geo geo{};
+    bool clu = false;
+    // Single 16-CTA cluster with the DSMEM exchange when the whole system fits on 16 SMs with
+    // no streamed rows and is small enough that 16 SMs' GEMV beats the grid-wide exchange
+    // (cluster_size: 0 = auto, 16 = prefer the cluster, 1 = never).
+    const int want_cs = opts ? opts->cluster_size : 0;
+    if (!resmode && want_cs != 1 && (want_cs == kCS || (d * n <= kCluMaxElems && !(opts && opts->num_ctas > 0))) &&
+        d >= kCS) {
+        Geo g{};
+        if (geometry(kCS, true, g) && g.rr + g.rt + g.rs >= g.rb) {
+            CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(g.var->fn)));
+            int ncl = 0;
+            CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(g.var->fn), kCS, kLT, g.smem, &ncl));
+            if (ncl >= 1) {
+                geo = g;
+                clu = true;
+            }
+        }
     }
-    const LoopVariant *var = rt > 0 ? (resmode ? &kVariantTmRes : &kVariantTm)
-                                    : pick_variant(cb, rr > 0 ? rr : 1, resmode);
-    if (!var) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
+    if (!clu) {
+        int Gw = opts && opts->num_ctas > 0 ? opts->num_ctas : ctx->num_sms;
+        if (Gw > d) Gw = static_cast<int>(d);
+        if (!geometry(Gw, false, geo)) {
+            if (!geo.var) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
+            return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory (use more CTAs)");
+        }
+    }
+    const int G = geo.G, rows_max = geo.rows_max, rr = geo.rr, rt = geo.rt, rs = geo.rs;
+    const size_t smem = geo.smem;
+    const LoopVariant *var = geo.var;
     const LoopFn fn = var->fn;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
     int per = 0;
-    const size_t smem = loop_smem(rows_max, wpg, cb, n, rs).total;
-    if (smem > static_cast<size_t>(ctx->max_smem_optin))
-        return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory (use more CTAs)");
-    CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, smem, &per));
-    if (per < G) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
+    if (!clu) {
+        CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, smem, &per));
+        if (per < G) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
+    }
     int kb = 1;
     while ((1ll << kb) < d + 1) ++kb;
 
@@ -920,8 +1046,15 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
 
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    if (clu) {  // one 16-CTA cluster: co-scheduled by construction, no cooperative launch needed
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = kCS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+    } else {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+    }
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(kLT);
     cfg.dynamicSmemBytes = smem;
@@ -930,14 +1063,14 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     cfg.numAttrs = 1;
     // Profiling only (ncu cannot replay cooperative launches): same kernel without the attribute.
     static const bool noncoop = getenv("CSK_PROFILE_NONCOOP") != nullptr;
-    if (noncoop) cfg.numAttrs = 0;
+    if (noncoop && !clu) cfg.numAttrs = 0;
     CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, prm));
     static const bool dbg = getenv("CSK_DEBUG") != nullptr;
     if (dbg)
-        fprintf(stderr, "[csk] loop: d=%lld n=%lld G=%d wpg=%d cb=%d rrmax=%d tm=%d rr=%d rt=%d rs=%d rows/CTA=%d smem=%zu\n",
-                (long long)d, (long long)n, G, wpg, cb, var->rrmax, (int)var->tm, rr, rt, rs, rows_max, smem);
+        fprintf(stderr, "[csk] loop: d=%lld n=%lld G=%d cluster=%d wpg=%d cb=%d rrmax=%d tm=%d rr=%d rt=%d rs=%d rows/CTA=%d smem=%zu\n",
+                (long long)d, (long long)n, G, clu ? kCS : 0, wpg, cb, var->rrmax, (int)var->tm, rr, rt, rs, rows_max, smem);
     ctx->last_solve_geom[0] = G;
-    ctx->last_solve_geom[1] = 1;
+    ctx->last_solve_geom[1] = clu ? kCS : 1;
     ctx->last_solve_geom[2] = rs;
     ctx->last_solve_geom[3] = rr;
     ctx->last_solve_geom[4] = wpg;
