@@ -249,6 +249,39 @@ __device__ __forceinline__ double dbl_of(uint32_t lo, uint32_t hi) {
     return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
 }
 
+// NB TMEM rows (NB/2 tcgen05.ld of two rows each) folded against x: the next pair's load is in
+// flight while the current pair is folded; each row folds its two column halves in separate
+// chains (4 chains per pair), added at the end.
+template <int NB, int CB>
+__device__ __forceinline__ void tmem_block(uint32_t taddr, const double (&x)[CB], double (&acc)[NB]) {
+    double lo[NB], hi[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) lo[j] = hi[j] = 0.0;
+    uint32_t v[32];
+    tmem_ld32_async(taddr, v);
+    tmem_wait_ld(v);
+#pragma unroll
+    for (int j = 0; j < NB; j += 2) {
+        uint32_t w[32];
+        if (j + 2 < NB) tmem_ld32_async(taddr + 16u * (j + 2), w);
+#pragma unroll
+        for (int q = 0; q < CB / 2; ++q) {
+            const int q2 = q + CB / 2;
+            lo[j] = __fma_rn(dbl_of(v[2 * q], v[2 * q + 1]), x[q], lo[j]);
+            lo[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q], v[16 + 2 * q + 1]), x[q], lo[j + 1]);
+            hi[j] = __fma_rn(dbl_of(v[2 * q2], v[2 * q2 + 1]), x[q2], hi[j]);
+            hi[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q2], v[16 + 2 * q2 + 1]), x[q2], hi[j + 1]);
+        }
+        if (j + 2 < NB) {
+            tmem_wait_ld(w);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) v[t] = w[t];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = lo[j] + hi[j];
+}
+
 // NB shared-memory rows (from i0, clamped to rs-1) folded against x: columns outer, rows inner.
 template <int NB, int CB>
 __device__ __forceinline__ void smem_block(const double *ar_tg, int i0, int rs, int TG, const double (&x)[CB],
@@ -498,40 +531,31 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         }
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
         if constexpr (TM) {
-            // 8-row blocks; rows past rt read unused columns of this thread's TMEM area (never
-            // written back).  The next pair's tcgen05.ld is in flight while the current pair is
-            // folded; each row folds its two column halves in separate chains (4 chains/pair).
-            for (int j0 = 0; j0 < rt; j0 += 8) {
-                double lo[8], hi[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) lo[j] = hi[j] = 0.0;
-                uint32_t v[32];
-                tmem_ld32_async(tbase + 16u * j0, v);
-                tmem_wait_ld(v);
-#pragma unroll
-                for (int j = 0; j < 8; j += 2) {
-                    uint32_t w[32];
-                    if (j + 2 < 8) tmem_ld32_async(tbase + 16u * (j0 + j + 2), w);
-#pragma unroll
-                    for (int q = 0; q < CB / 2; ++q) {
-                        const int q2 = q + CB / 2;
-                        lo[j] = __fma_rn(dbl_of(v[2 * q], v[2 * q + 1]), x[q], lo[j]);
-                        lo[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q], v[16 + 2 * q + 1]), x[q], lo[j + 1]);
-                        hi[j] = __fma_rn(dbl_of(v[2 * q2], v[2 * q2 + 1]), x[q2], hi[j]);
-                        hi[j + 1] = __fma_rn(dbl_of(v[16 + 2 * q2], v[16 + 2 * q2 + 1]), x[q2], hi[j + 1]);
-                    }
-                    if (j + 2 < 8) {
-                        tmem_wait_ld(w);
-#pragma unroll
-                        for (int t = 0; t < 32; ++t) v[t] = w[t];
-                    }
+            // blocks of 8 / 4 / 2 rows (a block may run one row past rt, reading an unused row
+            // of this thread's TMEM area that is never written back)
+            for (int j0 = 0; j0 < rt;) {
+                if (rt - j0 > 4) {
+                    double acc8[8];
+                    tmem_block<8, CB>(tbase + 16u * j0, x, acc8);
+                    const double s = treduce<8>(acc8, lane);
+                    const int i = lane >> 2;
+                    if ((lane & 3) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
+                    j0 += 8;
+                } else if (rt - j0 > 2) {
+                    double acc4[4];
+                    tmem_block<4, CB>(tbase + 16u * j0, x, acc4);
+                    const double s = treduce<4>(acc4, lane);
+                    const int i = lane >> 3;
+                    if ((lane & 7) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
+                    j0 += 4;
+                } else {
+                    double acc2[2];
+                    tmem_block<2, CB>(tbase + 16u * j0, x, acc2);
+                    const double s = treduce<2>(acc2, lane);
+                    const int i = lane >> 4;
+                    if ((lane & 15) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
+                    j0 += 2;
                 }
-                double acc8[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc8[j] = lo[j] + hi[j];
-                const double s = treduce<8>(acc8, lane);
-                const int i = lane >> 2;
-                if ((lane & 3) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
             }
         }
         // ---- S6 GEMV: shared-memory rows, blocks of 8, transposed tree ----
