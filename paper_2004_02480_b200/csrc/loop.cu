@@ -459,6 +459,12 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const bool even = (n & 1) == 0;
     const unsigned long long kmask = (1ull << b) - 1ull;
 
+    // finalize lanes keep their row's b~ and 1/nsq in registers (groups of <= 32 rows)
+    const bool fast_fin = ng <= 32;
+    const double fin_b = (fast_fin && lane < ng) ? btl[lr0 + lane] : 0.0;
+    const double fin_i = (fast_fin && lane < ng) ? invl[lr0 + lane] : 0.0;
+    const bool all_reg = rr == ng;  // every row of the group in registers: own partial by shuffle
+
     int64_t k = 0, last = -1;
     int term = -1;
     double res = 0.0;
@@ -516,6 +522,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             }
         }
         // ---- S6 GEMV: register rows (transposed tree: row i ends in lanes [i LPR, (i+1) LPR)) ----
+        double sreg;
         {
             double acc[V];
 #pragma unroll
@@ -526,8 +533,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 for (int i = 0; i < RRMAX; ++i) acc[i] = __fma_rn(a[i][q], x[q], acc[i]);
             }
             const double s = treduce<V>(acc, lane);
+            sreg = s;
             const int i = lane / LPR;
-            if ((lane % LPR) == 0 && i < rr) dotp[wg * RM + lr0 + i] = s;
+            if ((lane % LPR) == 0 && i < rr && !(all_reg && wg == 0)) dotp[wg * RM + lr0 + i] = s;
         }
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
         if constexpr (TM) {
@@ -607,7 +615,22 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         if (wg == 0) {
             unsigned long long bk = 0ull;
             double bl = 0.0, bs = -1.0, rr2 = 0.0;
-            for (int l0 = 0; l0 < ng; l0 += 32) {
+            if (fast_fin) {
+                // one row per lane; the warp's own partial of row `lane` comes by shuffle when all
+                // rows are register rows, the other warps' partials from shared memory
+                const double own = __shfl_sync(0xffffffffu, sreg, (lane * LPR) & 31);
+                if (lane < ng) {
+                    const int l = lr0 + lane;
+                    double dot = all_reg ? own : dotp[l];
+                    for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
+                    const double ri = fin_b - dot;
+                    const double sc = fin_i > 0.0 ? (ri * ri) * fin_i : -1.0;
+                    if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
+                    bk = row_key(sc, r0 + l, b);
+                    bl = ri * fin_i;
+                    bs = sc;
+                }
+            } else for (int l0 = 0; l0 < ng; l0 += 32) {
                 const int l = lr0 + l0 + lane;
                 if (l0 + lane < ng) {
                     double dot = dotp[l];
@@ -882,7 +905,7 @@ const LoopVariant kVariants[] = {
     {2, 2, k_loop<2, 2, false, false, false>},   {2, 8, k_loop<2, 8, false, false, false>},   {2, 32, k_loop<2, 32, false, false, false>},
     {4, 2, k_loop<4, 2, false, false, false>},   {4, 4, k_loop<4, 4, false, false, false>},   {4, 8, k_loop<4, 8, false, false, false>},
     {4, 20, k_loop<4, 20, false, false, false>}, {8, 2, k_loop<8, 2, false, false, false>},   {8, 4, k_loop<8, 4, false, false, false>},
-    {8, 8, k_loop<8, 8, false, false, false>},   {8, 10, k_loop<8, 10, false, false, false>}, {16, 2, k_loop<16, 2, false, false, false>},
+    {8, 8, k_loop<8, 8, false, false, false>},   {8, 9, k_loop<8, 9, false, false, false>}, {8, 10, k_loop<8, 10, false, false, false>}, {16, 2, k_loop<16, 2, false, false, false>},
     {16, 4, k_loop<16, 4, false, false, false>}, {16, 5, k_loop<16, 5, false, false, false>},
 };
 // TMEM tier variants (8 columns per thread, 8 register rows + 16 TMEM rows per thread)

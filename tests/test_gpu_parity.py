@@ -165,6 +165,27 @@ def test_solve_launch_shapes_and_streamed_rows(csk, num_ctas, smem_rows, cluster
     _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 300)
 
 
+@pytest.mark.parametrize("name,cluster,tmem", [("C1", 16, None), ("C1", 1, None), ("C2", 16, None),
+                                               ("C2", 1, None), ("C2", 16, False), ("C2", 16, True)])
+def test_solve_cluster_and_grid_exchange(csk, name, cluster, tmem):
+    """The single-cluster DSMEM exchange (cluster_size=16) and the grid-wide atomic exchange
+    (cluster_size=1) on the same sketched system: identical i_k sequences against the oracle."""
+    cfg = CONFIGS[name]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters,
+                      cluster_size=cluster, tmem=tmem, trace=4000, trace_x=True)
+    geo = csk.csk_last_solve_geometry()
+    assert geo["cluster_size"] == (16 if cluster == 16 else 1)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star),
+                     tol=cfg.tol, max_iters=cfg.max_iters, trace=4000)
+    assert g.termination == csk.CONVERGED
+    _free_running(g, o)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000)
+    n_same = min(len(g.idx_trace), len(o.idx_trace))
+    assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
+
+
 @pytest.mark.parametrize("n,d,num_ctas,reg_rows,group_warps", [
     (200, 1500, 12, 0, 0),    # 8 register + 8 TMEM rows per group
     (200, 1500, 12, 2, 0),    # 2 register + 14 TMEM rows
