@@ -21,8 +21,13 @@
 // on one GPU, with the gather done by the candidate kernels writing straight into the
 // gathered buffer -- the 1-GPU test of the sharded decomposition.
 #include <nccl.h>
+#include <stdlib.h>
 #include <string.h>
 
+#include <cuda.h>
+
+#include <map>
+#include <string>
 #include <vector>
 
 #include "csk_internal.cuh"
@@ -32,6 +37,8 @@ namespace csk {
 struct Comm {
     ncclComm_t nccl = nullptr;
     int nranks = 1, rank = 0;
+    // peer mappings (cudaIpcOpenMemHandle) of the other ranks' allocations, by handle bytes
+    std::map<std::string, void *> peer_open;
 };
 
 namespace {
@@ -448,6 +455,141 @@ csk_status_t csk_sketch_sharded(csk_ctx_t ctx, const double *A_local, int64_t ld
     return CSK_OK;
 }
 
+// ---- S10 fused across GPUs: every rank runs the persistent k_loop on its rows; all P x Gr
+//      CTAs take part in ONE exchange whose {count, max} pair lives in rank 0's memory and is
+//      updated with system-scope atomics over NVLink; the winner's slot and row are read from
+//      the owner's memory through peer mappings (CUDA IPC handles swapped with ncclAllGather).
+struct IpcRec {
+    cudaIpcMemHandle_t a;  // allocation holding this rank's A~ rows
+    long long a_off;       // offset of A~_local inside it
+    cudaIpcMemHandle_t x;  // this rank's exchange buffer (ctx->slots)
+    long long pad;
+};
+
+static csk_status_t ipc_handle(csk_ctx_t ctx, const void *ptr, cudaIpcMemHandle_t *h, long long *off) {
+    // driver entry point through the runtime (no link-time dependency on libcuda)
+    using GetRange = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(ctx, CSK_E_CUDA, "cudaGetDriverEntryPoint(cuMemGetAddressRange) failed");
+        get_range = reinterpret_cast<GetRange>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+        return fail(ctx, CSK_E_CUDA, "cuMemGetAddressRange failed");
+    CSK_CUDA(ctx, cudaIpcGetMemHandle(h, reinterpret_cast<void *>(base)));
+    *off = static_cast<long long>(reinterpret_cast<uintptr_t>(ptr) - static_cast<uintptr_t>(base));
+    return CSK_OK;
+}
+
+static csk_status_t ipc_open(csk_ctx_t ctx, const cudaIpcMemHandle_t &h, void **out) {
+    const std::string key(reinterpret_cast<const char *>(&h), sizeof(h));
+    auto it = ctx->comm->peer_open.find(key);
+    if (it != ctx->comm->peer_open.end()) {
+        *out = it->second;
+        return CSK_OK;
+    }
+    void *p = nullptr;
+    CSK_CUDA(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->comm->peer_open[key] = p;
+    *out = p;
+    return CSK_OK;
+}
+
+__global__ void k_sumsq_shard(const double *v, int64_t len, double *out) {
+    // single CTA, fixed order: thread-strided fma, warp butterfly, warps in order
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) a = __fma_rn(v[i], v[i], a);
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = red[0];
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = t + red[w];
+        *out = t;
+    }
+}
+
+static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_local, const double *b_tilde_local,
+                                        const double *nsq_local, int64_t d_lo, int64_t d_hi, int64_t d, int64_t n,
+                                        double *x, const double *x_star, double tol, int64_t max_iters,
+                                        csk_report_t *report, cudaStream_t s) {
+    Comm *cm = ctx->comm;
+    const int P = cm->nranks, me = cm->rank;
+    if (P > kMaxRanks) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve_sharded: more than 8 ranks");
+    RankSetup rs;
+    rs.P = P;
+    rs.rank = me;
+    rs.Gr = ctx->num_sms;
+    rs.sys = 1;
+    for (int r = 0; r < P; ++r) {
+        int64_t lo, hi;
+        csk_shard_range(d, P, r, &lo, &hi);
+        rs.dlo[r] = lo;
+        rs.dlo[r + 1] = hi;
+    }
+    if (rs.dlo[me] != d_lo || rs.dlo[me + 1] != d_hi)
+        return fail(ctx, CSK_E_ARG, "csk_solve_sharded: [d_lo, d_hi) must be csk_shard_range(d, P, rank)");
+    for (int r = 0; r < P; ++r)
+        if (rs.dlo[r + 1] <= rs.dlo[r]) return fail(ctx, CSK_E_ARG, "csk_solve_sharded: a rank owns no rows (d < P)");
+    // this rank's exchange buffer: [3 pairs][2][Gr] LL slots (rank 0's pairs are the global ones)
+    const size_t ex = loop_exchange_bytes(rs.Gr);
+    CSK_CHECK(ensure(ctx, ctx->slots, ex));
+    CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
+    const size_t xch_bytes = ex - static_cast<size_t>(2) * rs.Gr * 8 * 8;
+    // swap IPC handles (A~ rows, exchange buffer) through NCCL
+    IpcRec mine{};
+    CSK_CHECK(ipc_handle(ctx, A_tilde_local, &mine.a, &mine.a_off));
+    long long xoff = 0;
+    CSK_CHECK(ipc_handle(ctx, ctx->slots.ptr, &mine.x, &xoff));
+    std::vector<IpcRec> all(P);
+    void *dbuf = nullptr;
+    CSK_CUDA(ctx, cudaMallocAsync(&dbuf, sizeof(IpcRec) * (P + 1), s));
+    CSK_CUDA(ctx, cudaMemcpyAsync(static_cast<char *>(dbuf) + sizeof(IpcRec) * P, &mine, sizeof(IpcRec),
+                                  cudaMemcpyHostToDevice, s));
+    CSK_NCCL(ctx, ncclAllGather(static_cast<char *>(dbuf) + sizeof(IpcRec) * P, dbuf, sizeof(IpcRec), ncclUint8,
+                                cm->nccl, s));
+    CSK_CUDA(ctx, cudaMemcpyAsync(all.data(), dbuf, sizeof(IpcRec) * P, cudaMemcpyDeviceToHost, s));
+    CSK_CUDA(ctx, cudaStreamSynchronize(s));
+    for (int r = 0; r < P; ++r) {
+        unsigned char *xb = nullptr;
+        if (r == me) {
+            rs.At_r[r] = A_tilde_local;
+            xb = static_cast<unsigned char *>(ctx->slots.ptr);
+        } else {
+            void *a = nullptr, *xp = nullptr;
+            CSK_CHECK(ipc_open(ctx, all[r].a, &a));
+            CSK_CHECK(ipc_open(ctx, all[r].x, &xp));
+            rs.At_r[r] = reinterpret_cast<const double *>(static_cast<unsigned char *>(a) + all[r].a_off);
+            xb = static_cast<unsigned char *>(xp) + xoff;  // same ctx workspace layout on every rank
+        }
+        rs.slots_r[r] = reinterpret_cast<unsigned long long *>(xb + xch_bytes);
+        if (r == 0) rs.xch = reinterpret_cast<unsigned long long *>(xb);
+    }
+    rs.bt_r[me] = b_tilde_local;
+    rs.nsq_r[me] = nsq_local;
+    rs.x_r[me] = x;
+    // zero the exchange memory, and the global ||b~||^2 for residual mode; the all-reduce is
+    // also the barrier that keeps every rank's kernel behind rank 0's zeroed pairs
+    CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, ex, s));
+    double *bb = static_cast<double *>(ctx->scalars.ptr);
+    CSK_CUDA(ctx, cudaMemsetAsync(bb, 0, 8, s));
+    if (x_star == nullptr) {
+        k_sumsq_shard<<<1, 1024, 0, s>>>(b_tilde_local, d_hi - d_lo, bb);
+        rs.bb = bb;
+    }
+    CSK_NCCL(ctx, ncclAllReduce(bb, bb, 1, ncclFloat64, ncclSum, cm->nccl, s));
+    CSK_CUDA(ctx, cudaFreeAsync(dbuf, s));
+    rs.exchange_zeroed = true;
+    return run_loop(ctx, A_tilde_local, b_tilde_local, nsq_local, d_hi - d_lo, n, x, x_star, tol, max_iters, nullptr,
+                    report, s, &rs);
+}
+
 csk_status_t csk_solve_sharded(csk_ctx_t ctx, const double *A_tilde_local, const double *b_tilde_local,
                                const double *nsq_local, int64_t d_lo, int64_t d_hi, int64_t d, int64_t n,
                                double *x, const double *x_star, double tol, int64_t max_iters,
@@ -458,6 +600,11 @@ csk_status_t csk_solve_sharded(csk_ctx_t ctx, const double *A_tilde_local, const
         return fail(ctx, CSK_E_ARG, "csk_solve_sharded: bad arguments");
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = as_stream(stream);
+    // default: the fused persistent loop over peer memory; CSK_SHARDED_NCCL=1 selects the
+    // host-driven loop (local candidate kernel + ncclAllGather + apply kernel per iteration)
+    static const bool host_nccl = getenv("CSK_SHARDED_NCCL") != nullptr;
+    if (!host_nccl) return solve_sharded_fused(ctx, A_tilde_local, b_tilde_local, nsq_local, d_lo, d_hi, d, n, x,
+                                               x_star, tol, max_iters, report, s);
     std::vector<void *> owned;
     std::vector<RankView> rv(1);
     rv[0] = RankView{A_tilde_local, b_tilde_local, nsq_local, d_hi - d_lo, d_lo, x, {}};
@@ -477,35 +624,43 @@ csk_status_t csk_solve_virtual_ranks(csk_ctx_t ctx, const double *A_tilde, const
     if (!ctx || !A_tilde || !b_tilde || !nsq || !x || !report || nranks < 1 || d < 1 || n < 1 || !(tol > 0.0) ||
         max_iters < 0)
         return ctx ? fail(ctx, CSK_E_ARG, "csk_solve_virtual_ranks: bad arguments") : CSK_E_ARG;
+    if (nranks > kMaxRanks)
+        return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve_virtual_ranks: more than 8 ranks");
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = as_stream(stream);
-    std::vector<void *> owned;
-    std::vector<RankView> rv(nranks);
-    csk_status_t st = CSK_OK;
-    for (int p = 0; p < nranks && st == CSK_OK; ++p) {
+    // The fused S10 loop with P virtual ranks in ONE cooperative launch: rank r's CTAs own the
+    // rows of csk_shard_range(d, P, r) and run the same grid-wide exchange the P-GPU launch runs
+    // (there with peer-mapped memory); every virtual rank writes its own copy of x.
+    void *tmp = nullptr;
+    double *copies = x_copies;
+    if (!copies) {
+        if (cudaMalloc(&tmp, static_cast<size_t>(nranks) * n * 8) != cudaSuccess)
+            return fail(ctx, CSK_E_NOMEM, "csk_solve_virtual_ranks: cudaMalloc");
+        copies = static_cast<double *>(tmp);
+    }
+    RankSetup rs;
+    rs.P = nranks;
+    rs.rank = -1;
+    rs.Gr = ctx->num_sms / nranks;
+    rs.sys = 0;
+    for (int p = 0; p < nranks; ++p) {
         int64_t lo, hi;
         csk_shard_range(d, nranks, p, &lo, &hi);
-        double *xp = nullptr;
-        if (p == 0) {
-            xp = x;
-        } else {
-            void *q = nullptr;
-            if (cudaMalloc(&q, static_cast<size_t>(n) * 8) != cudaSuccess) { st = CSK_E_NOMEM; break; }
-            owned.push_back(q);
-            xp = static_cast<double *>(q);
-            cudaMemcpyAsync(xp, x, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s);
-        }
-        rv[p] = RankView{A_tilde + lo * n, b_tilde + lo, nsq + lo, hi - lo, lo, xp, {}};
-        st = alloc_shard_bufs(ctx, n, nranks, cand_grid(ctx, hi - lo), rv[p].b, owned);
+        rs.dlo[p] = lo;
+        rs.dlo[p + 1] = hi;
+        rs.At_r[p] = A_tilde + lo * n;
+        rs.bt_r[p] = b_tilde + lo;
+        rs.nsq_r[p] = nsq + lo;
+        rs.x_r[p] = copies + static_cast<size_t>(p) * n;
+        cudaMemcpyAsync(rs.x_r[p], x, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s);
     }
-    if (st == CSK_OK) st = run_sharded_loop(ctx, rv, nullptr, n, x_star, tol, max_iters, report, s);
-    if (st == CSK_OK && x_copies) {
-        for (int p = 0; p < nranks; ++p)
-            cudaMemcpyAsync(x_copies + static_cast<size_t>(p) * n, rv[p].x, static_cast<size_t>(n) * 8,
-                            cudaMemcpyDeviceToDevice, s);
-    }
+    for (int p = 0; p < nranks; ++p)
+        if (rs.dlo[p + 1] <= rs.dlo[p])
+            return fail(ctx, CSK_E_ARG, "csk_solve_virtual_ranks: a rank owns no rows (d < P)");
+    csk_status_t st = run_loop(ctx, A_tilde, b_tilde, nsq, d, n, x, x_star, tol, max_iters, nullptr, report, s, &rs);
+    if (st == CSK_OK) cudaMemcpyAsync(x, copies, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s);
     cudaStreamSynchronize(s);
-    for (void *p : owned) cudaFree(p);
+    if (tmp) cudaFree(tmp);
     return st;
 }
 

@@ -101,10 +101,29 @@ csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const 
                        int64_t d, int64_t n, double *x, const double *x_star, double tol,
                        int64_t max_iters, const csk_solve_opts_t *opts, csk_report_t *report,
                        cudaStream_t stream);
-// (loop.cu) register-resident loop with the flat atomic exchange (default)
+// (loop.cu) register-resident loop with the flat atomic exchange (default).
+// RankSetup (optional) shards the rows of A~ over P ranks for the same persistent kernel:
+//   rank = -1: P virtual ranks in ONE cooperative launch on this GPU (the 1-GPU test of S10);
+//   rank >= 0: this process is rank `rank` of P GPUs; the other ranks' A~ rows and slots are
+//              peer-mapped (sys = 1: system-scope exchange over NVLink).
+constexpr int kMaxRanks = 8;
+struct RankSetup {
+    int P = 1, rank = 0, Gr = 0, sys = 0;
+    int64_t dlo[kMaxRanks + 1] = {};
+    const double *At_r[kMaxRanks] = {};
+    const double *bt_r[kMaxRanks] = {};
+    const double *nsq_r[kMaxRanks] = {};
+    unsigned long long *slots_r[kMaxRanks] = {};  // null: carved from ctx->slots (virtual ranks)
+    unsigned long long *xch = nullptr;            // null: ctx->slots
+    double *x_r[kMaxRanks] = {};
+    const double *bb = nullptr;                   // residual mode: global ||b~||^2 (device), null: computed
+    bool exchange_zeroed = false;                 // the caller zeroed xch/slots (and synchronised the ranks)
+};
+size_t loop_exchange_bytes(int total_ctas);  // bytes of ctx->slots a launch of total_ctas needs
 csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq, int64_t d,
                       int64_t n, double *x, const double *x_star, double tol, int64_t max_iters,
-                      const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream);
+                      const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream,
+                      const RankSetup *ranks = nullptr);
 csk_status_t ensure_host_report(csk_ctx_t ctx);
 csk_status_t finish_solve(csk_ctx_t ctx, csk_report_t *report);
 

@@ -32,6 +32,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "csk_internal.cuh"
 
 namespace csk {
@@ -68,6 +70,17 @@ struct LoopParams {
     double *x_trace;
     int64_t *phase_cycles;    // debug (libcsk_prof.so only): [2 warps][16] SM-cycle totals of CTA 0
     long long *skew;          // debug (libcsk_prof.so only): [64 iterations][2][G] globaltimer ns
+    // ---- row sharding over P ranks (S10).  P = 1: one GPU.  rank >= 0: this launch is rank
+    //      `rank` of P GPUs (the other ranks' arrays are peer-mapped; sys = 1).  rank = -1: P
+    //      virtual ranks in ONE launch (rank = cta / Gr), the 1-GPU test of the decomposition.
+    int P, rank, Gr, sys;
+    int64_t dlo[kMaxRanks + 1];             // rank r owns the global rows [dlo[r], dlo[r+1])
+    int RMr[kMaxRanks];                     // rank r's rows per CTA, ceil((dlo[r+1]-dlo[r]) / Gr)
+    const double *At_r[kMaxRanks];          // rank r's rows of A~ (row dlo[r] first)
+    const double *bt_r[kMaxRanks];
+    const double *nsq_r[kMaxRanks];
+    unsigned long long *slots_r[kMaxRanks];  // rank r's LL slots [2][Gr][kSlotWords]
+    double *x_r[kMaxRanks];                 // rank r's output x (virtual: per-rank copies)
 };
 
 // ---- PTX helpers specific to the exchange ----
@@ -76,6 +89,21 @@ __device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long
 }
 __device__ __forceinline__ void red_add_release_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// system-scope variants for the cross-GPU exchange (peer memory over NVLink)
+__device__ __forceinline__ void red_max_u64_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release_u64_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v2_sys(const unsigned long long *p, unsigned long long &a,
+                                                  unsigned long long &b) {
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2_u64_sys(unsigned long long *p, unsigned long long a,
+                                                      unsigned long long b) {
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_v2_u64(unsigned long long *p, unsigned long long a,
                                                   unsigned long long b) {
@@ -99,11 +127,12 @@ __device__ __forceinline__ void ld_relaxed_v2_u64(const unsigned long long *p, u
                                                   unsigned long long &b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
-// spin until the LL-tagged double at p (2 words) carries `tag`
-__device__ __forceinline__ double ll_load(const unsigned long long *p, uint32_t tag) {
+// spin until the LL-tagged double at p (2 words) carries `tag` (sys: a peer GPU's memory)
+__device__ __forceinline__ double ll_load(const unsigned long long *p, uint32_t tag, bool sys = false) {
     unsigned long long hi, lo;
     do {
-        ld_relaxed_v2_u64(p, hi, lo);
+        if (sys) ld_relaxed_v2_sys(p, hi, lo);
+        else ld_relaxed_v2_u64(p, hi, lo);
     } while (!ll_ok(hi, lo, tag));
     return ll_val(hi, lo);
 }
@@ -330,14 +359,22 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     constexpr int LPR = 32 / V;  // lanes per row after the transposed tree
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = gridDim.x, cta = blockIdx.x;
+    const int cta = blockIdx.x;
     const int64_t d = p.d;
     const int n = static_cast<int>(p.n);
     const int WPG = p.wpg, TG = 32 * WPG, RG = kLW / WPG;
     const int grp = warp / WPG, wg = warp - grp * WPG, tg = tid - grp * TG;
-    // CTA c owns rows [c RM, min((c+1) RM, d)), RM = ceil(d/G): the owner of row i is i / RM
-    const int64_t r0 = (static_cast<int64_t>(cta) * p.rows_max < d) ? static_cast<int64_t>(cta) * p.rows_max : d;
-    const int64_t r1 = (r0 + p.rows_max < d) ? r0 + p.rows_max : d;
+    // rank rk owns the rows [dlo[rk], dlo[rk+1]); its CTA lc the rows [dlo + lc RMr, ...),
+    // RMr = ceil(rank rows / Gr): the owner of global row i is (rank of i, (i - dlo) / RMr)
+    const int rk = p.rank >= 0 ? p.rank : cta / p.Gr;
+    const int lc = p.rank >= 0 ? cta : cta - rk * p.Gr;
+    const int G = p.P * p.Gr;  // CTAs in the exchange (all ranks)
+    const bool lead = rk == 0 && lc == 0;
+    const int64_t dlo_r = p.dlo[rk], nsh = p.dlo[rk + 1] - dlo_r;
+    const int64_t RMr = p.RMr[rk];
+    const int64_t r0 = dlo_r + ((lc * RMr < nsh) ? lc * RMr : nsh);
+    const int64_t r1 = (r0 + RMr < dlo_r + nsh) ? r0 + RMr : dlo_r + nsh;
+    const double *Ash = p.At_r[rk];  // row dlo_r of A~ (this rank's rows)
     const int R = static_cast<int>(r1 - r0);
     const int lr0 = R * grp / RG, lr1 = R * (grp + 1) / RG;  // CTA-local rows of this group
     const int ng = lr1 - lr0;
@@ -391,21 +428,21 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
 #pragma unroll
     for (int q = 0; q < CB; ++q) {
         const int c = tg + TG * q;
-        x[q] = c < n ? p.x[c] : 0.0;
+        x[q] = c < n ? p.x_r[rk][c] : 0.0;
     }
     for (int c = tid; c < TG * CB; c += kLT) {
         xs[c] = (!RESMODE && c < n) ? p.x_star[c] : 0.0;
         if (c >= n) rowbuf[c] = 0.0;  // the TMA writes [0, n); x_q += lambda * 0 past n
     }
     for (int l = tid; l < R; l += kLT) {
-        btl[l] = p.bt[r0 + l];
-        const double ns = p.nsq[r0 + l];
+        btl[l] = p.bt_r[rk][r0 - dlo_r + l];
+        const double ns = p.nsq_r[rk][r0 - dlo_r + l];
         invl[l] = ns > 0.0 ? 1.0 / ns : 0.0;
     }
     double a[RRMAX][CB];
 #pragma unroll
     for (int i = 0; i < RRMAX; ++i) {
-        const double *src = p.At + (r0 + lr0 + i) * n;
+        const double *src = Ash + (r0 - dlo_r + lr0 + i) * n;
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
             const int c = tg + TG * q;
@@ -414,7 +451,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     }
     if constexpr (TM) {
         for (int j = 0; j < rt; ++j) {  // warp-uniform
-            const double *src = p.At + (r0 + lr0 + rr + j) * n;
+            const double *src = Ash + (r0 - dlo_r + lr0 + rr + j) * n;
             uint32_t v[16];
 #pragma unroll
             for (int q = 0; q < CB; ++q) {
@@ -428,7 +465,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     for (int i = 0; i < rs; ++i) {
-        const double *src = p.At + (r0 + lr0 + rr + rt + i) * n;
+        const double *src = Ash + (r0 - dlo_r + lr0 + rr + rt + i) * n;
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
             const int c = tg + TG * q;
@@ -471,11 +508,12 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     uint32_t mphase = 0;
     double lam = 0.0;      // lambda of the pending update x += lam A~^(prow)
     int64_t prow = -1;     // row of the pending update (-1: none)
+    const double *prow_ptr = nullptr;  // its A~ row (owner rank's memory: peer-mapped across GPUs)
     int *arrive = reinterpret_cast<int *>(const_cast<int64_t *>(ctl) + 7);  // group arrivals (smem)
     if (tid == 0) *arrive = 0;
     __syncthreads();
 #if CSK_PHASE_PROF
-    const bool prof = p.phase_cycles != nullptr && cta == 0 && lane == 0 && (warp == 0 || warp == kLW - 1);
+    const bool prof = p.phase_cycles != nullptr && lead && lane == 0 && (warp == 0 || warp == kLW - 1);
     long long ph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tp = clock64();
 #define LP(i)                           \
@@ -491,12 +529,12 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S8 of iteration k-1, fused at the top of iteration k: x_q += lambda a_{i_{k-1}}[c_q]
         //      (the row is in the fixed-offset row buffer, zero past n; odd n: from L2) ----
         if (prow >= 0) {
-            if (even) {
+            if (even && !p.sys) {
                 const double *rb = reinterpret_cast<const double *>(smem + kRowbufOff) + tg;
 #pragma unroll
                 for (int q = 0; q < CB; ++q) x[q] = __fma_rn(lam, rb[TG * q], x[q]);
             } else {
-                const double *src = p.At + prow * n;
+                const double *src = prow_ptr;
 #pragma unroll
                 for (int q = 0; q < CB; ++q) {
                     const int c = tg + TG * q;
@@ -508,7 +546,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S5 partial (last group): ||x_k - x*||^2, combined by the group's finalize warp ----
         double e2 = 0.0;
         if (!RESMODE && resgrp) {
-            if (cta == 0 && p.x_trace && k < p.trace_cap) {
+            if (lead && p.x_trace && k < p.trace_cap) {
 #pragma unroll
                 for (int q = 0; q < CB; ++q) {
                     const int c = tg + TG * q;
@@ -591,7 +629,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S6 GEMV: streamed rows (L2/HBM), two rows per pass ----
         for (int i = rr + rt + rs; i < ng; i += 2) {
             const bool two = i + 1 < ng;
-            const double *s0 = p.At + (r0 + lr0 + i) * n;
+            const double *s0 = Ash + (r0 - dlo_r + lr0 + i) * n;
             const double *s1 = two ? s0 + n : s0;
             double u0 = 0.0, u1 = 0.0;
 #pragma unroll
@@ -670,10 +708,10 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 for (int w = 1; w < WPG; ++w) e2 = e2 + resp[w];
             }
             if (wg == 0 && lane == 0) {
-                const double rk = xs_nrm > 0.0 ? e2 / xs_nrm : e2;
-                ctl[4] = rk <= p.tol ? CSK_CONVERGED : -1;
-                ctl[5] = __double_as_longlong(rk);
-                if (cta == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = rk;
+                const double resk = xs_nrm > 0.0 ? e2 / xs_nrm : e2;
+                ctl[4] = resk <= p.tol ? CSK_CONVERGED : -1;
+                ctl[5] = __double_as_longlong(resk);
+                if (lead && p.res_trace && k < p.trace_cap) p.res_trace[k] = resk;
             }
         }
         if (warp == 0) {
@@ -719,7 +757,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             double t = 0.0;
                             for (int j = 0; j < kCS; ++j) t = t + inbox[j * 4 + 3];  // fixed order
                             res = bb > 0.0 ? t / bb : t;
-                            if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                            if (lead && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
                             if (res <= p.tol) stop = CSK_CONVERGED;
                             else if (k == p.max_iters) stop = CSK_MAX_ITERS;
                         }
@@ -733,28 +771,38 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                                 ll_pack(wsc, tag, sb[2], sb[3]);
                                 const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
                                 mbar_arrive_expect_tx(mbar, rbytes);
-                                if (even) bulk_g2s(rowbuf, p.At + wrow * n, rbytes, mbar);
+                                if (even) bulk_g2s(rowbuf, Ash + (wrow - dlo_r) * n, rbytes, mbar);
+                                sb[4] = reinterpret_cast<unsigned long long>(Ash + (wrow - dlo_r) * n);
                             }
                         }
                         if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
                         if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copy
                     } else {
                     unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
-                    unsigned long long *slot_k = p.slots + static_cast<size_t>(k & 1) * G * kSlotWords;
+                    const size_t par_off = static_cast<size_t>(k & 1) * p.Gr * kSlotWords;
                     if (lane == 0) {
-                        if (cta == 0) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
-                        red_max_u64(pair + 1, kc);
-                        red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
-                        // the slot needs no ordering: readers validate its LL tags
-                        unsigned long long *my = slot_k + static_cast<size_t>(cta) * kSlotWords;
-                        unsigned long long h0, l0, h1, l1;
+                        // (sys: the pair lives in rank 0's memory and the slots are read by the
+                        //  other GPUs -- system-scope atomics, polls and stores over NVLink)
+                        unsigned long long *my = p.slots_r[rk] + par_off + static_cast<size_t>(lc) * kSlotWords;
+                        unsigned long long h0, l0, h1, l1, h2 = 0, l2 = 0;
                         ll_pack(cl_l, tag, h0, l0);
                         ll_pack(cl_s, tag, h1, l1);
-                        st_relaxed_v2_u64(my, h0, l0);
-                        st_relaxed_v2_u64(my + 2, h1, l1);
-                        if (RESMODE) {
-                            ll_pack(crr, tag, h0, l0);
-                            st_relaxed_v2_u64(my + 4, h0, l0);
+                        if (RESMODE) ll_pack(crr, tag, h2, l2);
+                        if (!p.sys) {
+                            if (lead) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                            red_max_u64(pair + 1, kc);
+                            red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
+                            // the slot needs no ordering: readers validate its LL tags
+                            st_relaxed_v2_u64(my, h0, l0);
+                            st_relaxed_v2_u64(my + 2, h1, l1);
+                            if (RESMODE) st_relaxed_v2_u64(my + 4, h2, l2);
+                        } else {
+                            if (lead) st_relaxed_v2_u64_sys(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                            red_max_u64_sys(pair + 1, kc);
+                            red_add_release_u64_sys(pair, 1ull);
+                            st_relaxed_v2_u64_sys(my, h0, l0);
+                            st_relaxed_v2_u64_sys(my + 2, h1, l1);
+                            if (RESMODE) st_relaxed_v2_u64_sys(my + 4, h2, l2);
                         }
                     }
                     LP(2)
@@ -767,7 +815,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
 #endif
                     unsigned long long c, mx;
                     do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
-                        ld_relaxed_v2(pair, c, mx);
+                        if (p.sys) ld_relaxed_v2_sys(pair, c, mx);
+                        else ld_relaxed_v2(pair, c, mx);
                     } while (c < static_cast<unsigned long long>(G));
                     // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the
                     // proxy fence orders this thread's generic view before its TMA reads
@@ -783,23 +832,44 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     if (mx != 0ull) {
                         wrow = static_cast<int64_t>(kmask - (mx & kmask));
                         if (lane == 0) {
-                            const int own = static_cast<int>(static_cast<uint32_t>(wrow) / static_cast<uint32_t>(RM));
-                            // winner's (lambda, score) slot and A~^(ik) -> shared memory, one mbarrier
-                            // (odd n: the row is read with plain loads in the update)
-                            const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
-                            mbar_arrive_expect_tx(mbar, rbytes + 32u);
-                            bulk_g2s(const_cast<unsigned long long *>(slotbuf), slot_k + static_cast<size_t>(own) * kSlotWords, 32u, mbar);
-                            if (even) bulk_g2s(rowbuf, p.At + wrow * n, rbytes, mbar);
-                            ctl[2] = own;
+                            // owner: rank by the row ranges, then its CTA
+                            int orank = 0;
+                            if (p.P > 1)
+                                while (orank + 1 < p.P && p.dlo[orank + 1] <= wrow) ++orank;
+                            const uint32_t olrow = static_cast<uint32_t>(wrow - p.dlo[orank]);
+                            const int olc = static_cast<int>(olrow / static_cast<uint32_t>(p.RMr[orank]));
+                            const unsigned long long *oslot = p.slots_r[orank] + par_off + static_cast<size_t>(olc) * kSlotWords;
+                            const double *orow = p.At_r[orank] + (wrow - p.dlo[orank]) * n;
+                            unsigned long long *sb = const_cast<unsigned long long *>(slotbuf);
+                            sb[4] = reinterpret_cast<unsigned long long>(orow);
+                            sb[7] = reinterpret_cast<unsigned long long>(oslot);
+                            if (!p.sys) {
+                                // winner's (lambda, score) slot and A~^(ik) -> shared memory, one
+                                // mbarrier (odd n: the row is read with plain loads in the update)
+                                const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
+                                mbar_arrive_expect_tx(mbar, rbytes + 32u);
+                                bulk_g2s(sb, oslot, 32u, mbar);
+                                if (even) bulk_g2s(rowbuf, orow, rbytes, mbar);
+                            } else {
+                                // across GPUs: the slot by system-scope loads (LL-validated), the
+                                // row by plain loads from the peer's memory in the update
+                                const double wl = ll_load(oslot, tag, true), ws = ll_load(oslot + 2, tag, true);
+                                ll_pack(wl, tag, sb[0], sb[1]);
+                                ll_pack(ws, tag, sb[2], sb[3]);
+                                mbar_arrive_expect_tx(mbar, 0u);
+                            }
                         }
                     }
                     if (RESMODE) {
-                        // ||r_k||^2: the G CTA partials in fixed order
+                        // ||r_k||^2: the G CTA partials in fixed order (rank-major)
                         double t = 0.0;
-                        for (int cc = lane; cc < G; cc += 32) t = t + ll_load(slot_k + static_cast<size_t>(cc) * kSlotWords + 4, tag);
+                        for (int cc = lane; cc < G; cc += 32) {
+                            const int cr = cc / p.Gr, cl2 = cc - cr * p.Gr;
+                            t = t + ll_load(p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4, tag, p.sys != 0);
+                        }
                         t = lwarp_sum(t);
                         res = bb > 0.0 ? t / bb : t;
-                        if (cta == 0 && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
+                        if (lead && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
                         if (res <= p.tol) stop = CSK_CONVERGED;
                         else if (k == p.max_iters) stop = CSK_MAX_ITERS;
                     }
@@ -833,9 +903,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 lam = ll_val(slotbuf[0], slotbuf[1]);
                 sc = ll_val(slotbuf[2], slotbuf[3]);
             } else if (!CLU) {  // the copy raced the owner's slot store: re-read until the tags match
-                const unsigned long long *gs = p.slots + (static_cast<size_t>(k & 1) * G + ctl[2]) * kSlotWords;
-                lam = ll_load(gs, tag);
-                sc = ll_load(gs + 2, tag);
+                const unsigned long long *gs = reinterpret_cast<const unsigned long long *>(slotbuf[7]);
+                lam = ll_load(gs, tag, p.sys != 0);
+                sc = ll_load(gs + 2, tag, p.sys != 0);
             }
             if (sc == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
         }
@@ -847,9 +917,10 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             break;
         }
         const int64_t wrow = ctl[1];
-        if (cta == 0 && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wrow;
+        if (lead && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wrow;
         last = wrow;
         prow = wrow;
+        prow_ptr = reinterpret_cast<const double *>(slotbuf[4]);
     }
 #undef LP
 #if CSK_PHASE_PROF
@@ -857,17 +928,17 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         for (int i = 0; i < 16; ++i) p.phase_cycles[(warp == 0 ? 0 : 1) * 16 + i] = ph[i];
 #endif
     // ---- epilogue: CTA 0's last group writes x (and the trace of the final iterate) ----
-    if (cta == 0 && resgrp) {
+    if (lc == 0 && resgrp) {  // every rank (virtual: every copy) writes its x
         const bool tr = p.x_trace && k < p.trace_cap;
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
             const int c = tg + TG * q;
             if (c < n) {
-                p.x[c] = x[q];
-                if (tr) p.x_trace[k * n + c] = x[q];
+                p.x_r[rk][c] = x[q];
+                if (tr && lead) p.x_trace[k * n + c] = x[q];
             }
         }
-        if (tid == (RG - 1) * TG) {
+        if (tid == (RG - 1) * TG && (p.rank >= 0 || rk == 0)) {
             p.report[0] = k;
             p.report[1] = __double_as_longlong(res);
             p.report[2] = term;
@@ -951,9 +1022,15 @@ __global__ void k_sumsq_loop(const double *v, int64_t len, double *out) {
 
 }  // namespace
 
+size_t loop_exchange_bytes(int total_ctas) {
+    return static_cast<size_t>(3) * kXchWords * 8 + static_cast<size_t>(2) * total_ctas * kSlotWords * 8;
+}
+
 csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq, int64_t d,
                       int64_t n, double *x, const double *x_star, double tol, int64_t max_iters,
-                      const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream) {
+                      const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream,
+                      const RankSetup *ranks) {
+    const bool multi = ranks != nullptr;
     const bool resmode = (x_star == nullptr);
     // group width: the fewest warps per group with n <= 256 WPG (<= 8 columns per thread:
     // fewer copies of x to update than 16 columns, still one warp per group for n <= 256)
@@ -976,10 +1053,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         size_t smem;
         const LoopVariant *var;
     };
-    auto geometry = [&](int Gw, bool clu, Geo &g) {
+    auto geometry = [&](int Gw, bool clu, Geo &g, int rm_fixed = 0) {
         g.G = Gw;
-        g.rows_max = static_cast<int>((d + Gw - 1) / Gw);
-        if (!clu) g.G = static_cast<int>((d + g.rows_max - 1) / g.rows_max);  // every CTA owns >= 1 row
+        g.rows_max = rm_fixed > 0 ? rm_fixed : static_cast<int>((d + Gw - 1) / Gw);
+        if (!clu && rm_fixed == 0) g.G = static_cast<int>((d + g.rows_max - 1) / g.rows_max);  // every CTA owns >= 1 row
         g.rb = (g.rows_max + rg - 1) / rg;  // max rows per group
         auto reg_rows = [&](int cap) {
             int r = cap;
@@ -1027,7 +1104,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     // no streamed rows and is small enough that 16 SMs' GEMV beats the grid-wide exchange
     // (cluster_size: 0 = auto, 16 = prefer the cluster, 1 = never).
     const int want_cs = opts ? opts->cluster_size : 0;
-    if (!resmode && want_cs != 1 && (want_cs == kCS || (d * n <= kCluMaxElems && !(opts && opts->num_ctas > 0))) &&
+    if (!multi && !resmode && want_cs != 1 && (want_cs == kCS || (d * n <= kCluMaxElems && !(opts && opts->num_ctas > 0))) &&
         d >= kCS) {
         Geo g{};
         if (geometry(kCS, true, g) && g.rr + g.rt + g.rs >= g.rb) {
@@ -1040,7 +1117,18 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
             }
         }
     }
-    if (!clu) {
+    if (multi) {
+        // P ranks x Gr CTAs; the carve-up is sized by the largest rank's rows per CTA
+        int64_t rm = 1;
+        for (int r = 0; r < ranks->P; ++r) {
+            const int64_t sz = ranks->dlo[r + 1] - ranks->dlo[r];
+            rm = std::max<int64_t>(rm, (sz + ranks->Gr - 1) / ranks->Gr);
+        }
+        if (!geometry(ranks->Gr, false, geo, static_cast<int>(rm))) {
+            if (!geo.var) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: no kernel for this n");
+            return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: too many rows per CTA for shared memory");
+        }
+    } else if (!clu) {
         int Gw = opts && opts->num_ctas > 0 ? opts->num_ctas : ctx->num_sms;
         if (Gw > d) Gw = static_cast<int>(d);
         if (!geometry(Gw, false, geo)) {
@@ -1054,27 +1142,55 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     const LoopFn fn = var->fn;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
     int per = 0;
+    // CTAs of this launch (virtual ranks: all of them) and of the whole exchange
+    const int grid = multi ? (ranks->rank < 0 ? ranks->P * ranks->Gr : ranks->Gr) : G;
+    const int gtotal = multi ? ranks->P * ranks->Gr : G;
     if (!clu) {
         CSK_CHECK(max_resident(ctx, reinterpret_cast<const void *>(fn), 1, kLT, smem, &per));
-        if (per < G) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
+        if (per < grid) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: grid cannot be co-resident");
     }
     int kb = 1;
     while ((1ll << kb) < d + 1) ++kb;
 
     const size_t xch_bytes = 3 * kXchWords * 8;
-    const size_t slot_bytes = static_cast<size_t>(2) * G * kSlotWords * 8;
-    CSK_CHECK(ensure(ctx, ctx->slots, xch_bytes + slot_bytes));
+    const size_t ex_bytes = loop_exchange_bytes(gtotal);
+    CSK_CHECK(ensure(ctx, ctx->slots, ex_bytes));
     CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
-    CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, xch_bytes + slot_bytes, stream));
-    double *bb = static_cast<double *>(ctx->scalars.ptr);
-    if (resmode) k_sumsq_loop<<<1, 1024, 0, stream>>>(bt, d, bb);
+    if (!(multi && ranks->exchange_zeroed)) CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, ex_bytes, stream));
+    const double *bb = static_cast<double *>(ctx->scalars.ptr);
+    if (resmode) {
+        if (multi && ranks->bb) bb = ranks->bb;
+        else k_sumsq_loop<<<1, 1024, 0, stream>>>(bt, d, static_cast<double *>(ctx->scalars.ptr));
+    }
 
     LoopParams prm{};
     prm.At = At; prm.bt = bt; prm.nsq = nsq; prm.d = d; prm.n = n; prm.x = x;
+    if (!multi) {  // one GPU: one rank owning every row
+        prm.P = 1; prm.rank = 0; prm.Gr = G; prm.sys = 0;
+        prm.dlo[0] = 0; prm.dlo[1] = d;
+        prm.RMr[0] = rows_max;
+        prm.At_r[0] = At; prm.bt_r[0] = bt; prm.nsq_r[0] = nsq; prm.x_r[0] = x;
+    } else {
+        prm.P = ranks->P; prm.rank = ranks->rank; prm.Gr = ranks->Gr; prm.sys = ranks->sys;
+        for (int r = 0; r <= ranks->P; ++r) prm.dlo[r] = ranks->dlo[r];
+        for (int r = 0; r < ranks->P; ++r)
+            prm.RMr[r] = static_cast<int>((ranks->dlo[r + 1] - ranks->dlo[r] + ranks->Gr - 1) / ranks->Gr);
+        for (int r = 0; r < ranks->P; ++r) {
+            prm.At_r[r] = ranks->At_r[r]; prm.bt_r[r] = ranks->bt_r[r]; prm.nsq_r[r] = ranks->nsq_r[r];
+            prm.x_r[r] = ranks->x_r[r];
+        }
+    }
     prm.x_star = x_star; prm.tol = tol; prm.max_iters = max_iters;
     prm.xch = static_cast<unsigned long long *>(ctx->slots.ptr);
     prm.slots = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(ctx->slots.ptr) + xch_bytes);
+    prm.slots_r[0] = prm.slots;
+    if (multi) {
+        if (ranks->xch) prm.xch = ranks->xch;
+        for (int r = 0; r < ranks->P; ++r)  // virtual ranks: slices of this ctx's slots
+            prm.slots_r[r] = ranks->slots_r[r] ? ranks->slots_r[r]
+                                               : prm.slots + static_cast<size_t>(r) * 2 * ranks->Gr * kSlotWords;
+    }
     prm.report = static_cast<int64_t *>(ctx->report.ptr);
     prm.bb = bb;
     prm.wpg = wpg;
@@ -1102,7 +1218,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
     }
-    cfg.gridDim = dim3(G);
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kLT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
