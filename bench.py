@@ -12,7 +12,8 @@ is flushed by writing a 256 MiB buffer (untimed).
 
 N > 1 (torchrun): ONE problem, row-sharded across the ranks (strong scaling): the sketch
 with csk_sketch_sharded (NCCL reduce-scatter of partial A~ by bucket range, S9) and the loop
-with csk_solve_sharded (per-iteration NCCL all-gather max-loc + winning row, S10).
+with csk_solve_sharded (S10: the persistent loop on every GPU, one exchange over NVLink peer
+memory per iteration).
 """
 from __future__ import annotations
 
@@ -492,9 +493,9 @@ def run_sharded(args, dist, rank, ws):
         "iterations_per_s": round(it / (sv * 1e-3), 1), "sketch_ms": round(sk, 5), "solve_ms": round(sv, 4),
         "sketch_hbm_gbs": round(alg_bytes_sketch(cfg) / (sk * 1e-3) / 1e9, 1),
         "clocks": sampler.summary(t0, t1),
-        "gpu_launches": args.steps * (4 + 3 * ((it // 16) + 1) * 16),
-        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_row_norms + per iteration "
-                             "k_shard_candidate, k_shard_apply (+ NCCL kernels)",
+        "gpu_launches": args.steps * 4,
+        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB radix-sort kernels, "
+                             "the NCCL reduce-scatter of S9 and the NCCL handle/barrier collectives of S10)",
     }
     csk.comm_destroy(ctx)
     return out
