@@ -267,6 +267,20 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
                  :
                  : "memory");
 }
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+                 :
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
@@ -283,6 +297,38 @@ __device__ __forceinline__ double dbl_of(uint32_t lo, uint32_t hi) {
 // chains (4 chains per pair), added at the end.
 template <int NB, int CB>
 __device__ __forceinline__ void tmem_block(uint32_t taddr, const double (&x)[CB], double (&acc)[NB]) {
+    // one row (CB doubles = 16 TMEM columns) per tcgen05.ld; the next row's load is in flight
+    // while the current row is folded in two chains (column halves), added at the end
+    double lo[NB], hi[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) lo[j] = hi[j] = 0.0;
+    uint32_t v[16];
+    tmem_ld16_async(taddr, v);
+    tmem_wait_ld16(v);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        uint32_t w[16];
+        if (j + 1 < NB) tmem_ld16_async(taddr + 16u * (j + 1), w);
+#pragma unroll
+        for (int q = 0; q < CB / 2; ++q) {
+            const int q2 = q + CB / 2;
+            lo[j] = __fma_rn(dbl_of(v[2 * q], v[2 * q + 1]), x[q], lo[j]);
+            hi[j] = __fma_rn(dbl_of(v[2 * q2], v[2 * q2 + 1]), x[q2], hi[j]);
+        }
+        if (j + 1 < NB) {
+            tmem_wait_ld16(w);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] = w[t];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = lo[j] + hi[j];
+}
+
+// Wide variant: two rows per tcgen05.ld (x32), the next pair in flight while the current pair is
+// folded (4 chains per pair) -- half the waits of the one-row form, 64 staging registers.
+template <int NB, int CB>
+__device__ __forceinline__ void tmem_block_wide(uint32_t taddr, const double (&x)[CB], double (&acc)[NB]) {
     double lo[NB], hi[NB];
 #pragma unroll
     for (int j = 0; j < NB; ++j) lo[j] = hi[j] = 0.0;
@@ -312,17 +358,30 @@ __device__ __forceinline__ void tmem_block(uint32_t taddr, const double (&x)[CB]
 }
 
 // NB shared-memory rows (from i0, clamped to rs-1) folded against x: columns outer, rows inner.
+// Layout [row][q/2][thread][2]: a thread's columns c_q, c_{q+1} sit in one 16-byte word.
 template <int NB, int CB>
-__device__ __forceinline__ void smem_block(const double *ar_tg, int i0, int rs, int TG, const double (&x)[CB],
+__device__ __forceinline__ void smem_block(const double *arows, int tg, int i0, int rs, int TG, const double (&x)[CB],
                                            double (&acc)[NB]) {
+    static_assert(CB % 2 == 0 || CB == 1, "pairs of columns");
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[j] = 0.0;
-#pragma unroll
-    for (int q = 0; q < CB; ++q) {
+    if constexpr (CB == 1) {
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
             const int jj = (i0 + j < rs) ? i0 + j : rs - 1;
-            acc[j] = __fma_rn(ar_tg[(static_cast<size_t>(jj) * CB + q) * TG], x[q], acc[j]);
+            acc[j] = __fma_rn(arows[static_cast<size_t>(jj) * TG + tg], x[0], acc[j]);
+        }
+    } else {
+        const double2 *a2 = reinterpret_cast<const double2 *>(arows) + tg;
+#pragma unroll
+        for (int qp = 0; qp < CB / 2; ++qp) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const int jj = (i0 + j < rs) ? i0 + j : rs - 1;
+                const double2 v = a2[(static_cast<size_t>(jj) * (CB / 2) + qp) * TG];
+                acc[j] = __fma_rn(v.x, x[2 * qp], acc[j]);
+                acc[j] = __fma_rn(v.y, x[2 * qp + 1], acc[j]);
+            }
         }
     }
 }
@@ -350,11 +409,13 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CB, int RRMAX, bool RESMODE, bool TM, bool CLU>
+template <int CB, int RRMAX, bool RESMODE, int TM, bool CLU>
 __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     // CLU: the whole grid is one kCS-CTA thread-block cluster and the exchange is an
     // all-to-all of the CTA candidates over DSMEM (no global atomics)
-    static_assert(!TM || CB == 8, "the TMEM tier is laid out for 8 columns (16 TMEM columns) per row");
+    // TM: 0 no TMEM tier; 1 wide (two rows per tcgen05.ld); 2 narrow (one row per load, more
+    // register rows).  The TMEM tier is laid out for 8 columns (16 TMEM columns) per row.
+    static_assert(TM == 0 || CB == 8, "TMEM rows hold 8 columns per thread");
     constexpr int V = Pow2Ceil<RRMAX>::v;
     constexpr int LPR = 32 / V;  // lanes per row after the transposed tree
     extern __shared__ __align__(128) unsigned char smem[];
@@ -379,7 +440,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const int lr0 = R * grp / RG, lr1 = R * (grp + 1) / RG;  // CTA-local rows of this group
     const int ng = lr1 - lr0;
     const int rr = ng < p.rr ? ng : p.rr;
-    const int rt = TM ? ((ng - rr) < p.rt ? (ng - rr) : p.rt) : 0;   // rows in TMEM
+    const int rt = TM != 0 ? ((ng - rr) < p.rt ? (ng - rr) : p.rt) : 0;   // rows in TMEM
     const int rs = (ng - rr - rt) < p.rs ? (ng - rr - rt) : p.rs;
     const int b = p.key_bits;
     const int RM = p.rows_max;
@@ -410,7 +471,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     }
     if (CLU) cluster_sync_all();  // every peer's exchange barriers exist before the first arrival
     uint32_t tbase = 0;  // this thread's TMEM row area: lane 32 (warp & 3) + lane, 256 columns
-    if constexpr (TM) {
+    if constexpr (TM != 0) {
         uint32_t *taddr_s = reinterpret_cast<uint32_t *>(const_cast<int64_t *>(ctl) + 6);
         if (warp == 0) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(taddr_s))
@@ -449,7 +510,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             a[i][q] = (i < rr && c < n) ? src[c] : 0.0;
         }
     }
-    if constexpr (TM) {
+    if constexpr (TM != 0) {
         for (int j = 0; j < rt; ++j) {  // warp-uniform
             const double *src = Ash + (r0 - dlo_r + lr0 + rr + j) * n;
             uint32_t v[16];
@@ -469,7 +530,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
             const int c = tg + TG * q;
-            arows[(static_cast<size_t>(i) * CB + q) * TG + tg] = c < n ? src[c] : 0.0;
+            const double v = c < n ? src[c] : 0.0;
+            if (CB == 1) arows[static_cast<size_t>(i) * TG + tg] = v;
+            else arows[((static_cast<size_t>(i) * (CB / 2) + q / 2) * TG + tg) * 2 + (q & 1)] = v;
         }
     }
     __syncthreads();
@@ -576,27 +639,30 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             if ((lane % LPR) == 0 && i < rr && !(all_reg && wg == 0)) dotp[wg * RM + lr0 + i] = s;
         }
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
-        if constexpr (TM) {
+        if constexpr (TM != 0) {
             // blocks of 8 / 4 / 2 rows (a block may run one row past rt, reading an unused row
             // of this thread's TMEM area that is never written back)
             for (int j0 = 0; j0 < rt;) {
                 if (rt - j0 > 4) {
                     double acc8[8];
-                    tmem_block<8, CB>(tbase + 16u * j0, x, acc8);
+                    if constexpr (TM == 1) tmem_block_wide<8, CB>(tbase + 16u * j0, x, acc8);
+                    else tmem_block<8, CB>(tbase + 16u * j0, x, acc8);
                     const double s = treduce<8>(acc8, lane);
                     const int i = lane >> 2;
                     if ((lane & 3) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
                     j0 += 8;
                 } else if (rt - j0 > 2) {
                     double acc4[4];
-                    tmem_block<4, CB>(tbase + 16u * j0, x, acc4);
+                    if constexpr (TM == 1) tmem_block_wide<4, CB>(tbase + 16u * j0, x, acc4);
+                    else tmem_block<4, CB>(tbase + 16u * j0, x, acc4);
                     const double s = treduce<4>(acc4, lane);
                     const int i = lane >> 3;
                     if ((lane & 7) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
                     j0 += 4;
                 } else {
                     double acc2[2];
-                    tmem_block<2, CB>(tbase + 16u * j0, x, acc2);
+                    if constexpr (TM == 1) tmem_block_wide<2, CB>(tbase + 16u * j0, x, acc2);
+                    else tmem_block<2, CB>(tbase + 16u * j0, x, acc2);
                     const double s = treduce<2>(acc2, lane);
                     const int i = lane >> 4;
                     if ((lane & 15) == 0 && j0 + i < rt) dotp[wg * RM + lr0 + rr + j0 + i] = s;
@@ -611,14 +677,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             for (int i0 = 0; i0 < rs;) {
                 if (rs - i0 > 4) {
                     double acc8[8];
-                    smem_block<8, CB>(arows + tg, i0, rs, TG, x, acc8);
+                    smem_block<8, CB>(arows, tg, i0, rs, TG, x, acc8);
                     const double s = treduce<8>(acc8, lane);
                     const int i = lane >> 2;
                     if ((lane & 3) == 0 && i0 + i < rs) dotp[wg * RM + lr0 + rr + rt + i0 + i] = s;
                     i0 += 8;
                 } else {
                     double acc4[4];
-                    smem_block<4, CB>(arows + tg, i0, rs, TG, x, acc4);
+                    smem_block<4, CB>(arows, tg, i0, rs, TG, x, acc4);
                     const double s = treduce<4>(acc4, lane);
                     const int i = lane >> 3;
                     if ((lane & 7) == 0 && i0 + i < rs) dotp[wg * RM + lr0 + rr + rt + i0 + i] = s;
@@ -945,7 +1011,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             p.report[3] = last;
         }
     }
-    if constexpr (TM) {
+    if constexpr (TM != 0) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -972,26 +1038,30 @@ struct LoopVariant {
     bool clu = false;
 };
 const LoopVariant kVariants[] = {
-    {1, 2, k_loop<1, 2, false, false, false>},   {1, 8, k_loop<1, 8, false, false, false>},   {1, 32, k_loop<1, 32, false, false, false>},
-    {2, 2, k_loop<2, 2, false, false, false>},   {2, 8, k_loop<2, 8, false, false, false>},   {2, 32, k_loop<2, 32, false, false, false>},
-    {4, 2, k_loop<4, 2, false, false, false>},   {4, 4, k_loop<4, 4, false, false, false>},   {4, 8, k_loop<4, 8, false, false, false>},
-    {4, 20, k_loop<4, 20, false, false, false>}, {8, 2, k_loop<8, 2, false, false, false>},   {8, 4, k_loop<8, 4, false, false, false>},
-    {8, 8, k_loop<8, 8, false, false, false>},   {8, 9, k_loop<8, 9, false, false, false>}, {8, 10, k_loop<8, 10, false, false, false>}, {16, 2, k_loop<16, 2, false, false, false>},
-    {16, 4, k_loop<16, 4, false, false, false>}, {16, 5, k_loop<16, 5, false, false, false>},
+    {1, 2, k_loop<1, 2, false, 0, false>},   {1, 8, k_loop<1, 8, false, 0, false>},   {1, 32, k_loop<1, 32, false, 0, false>},
+    {2, 2, k_loop<2, 2, false, 0, false>},   {2, 8, k_loop<2, 8, false, 0, false>},   {2, 32, k_loop<2, 32, false, 0, false>},
+    {4, 2, k_loop<4, 2, false, 0, false>},   {4, 4, k_loop<4, 4, false, 0, false>},   {4, 8, k_loop<4, 8, false, 0, false>},
+    {4, 20, k_loop<4, 20, false, 0, false>}, {8, 2, k_loop<8, 2, false, 0, false>},   {8, 4, k_loop<8, 4, false, 0, false>},
+    {8, 8, k_loop<8, 8, false, 0, false>},   {8, 9, k_loop<8, 9, false, 0, false>}, {8, 10, k_loop<8, 10, false, 0, false>}, {16, 2, k_loop<16, 2, false, 0, false>},
+    {16, 4, k_loop<16, 4, false, 0, false>}, {16, 5, k_loop<16, 5, false, 0, false>},
 };
 // TMEM tier variants (8 columns per thread, 8 register rows + 16 TMEM rows per thread)
-constexpr int kTmRegRows = 6, kTmRows = 16;
-const LoopVariant kVariantTm = {8, kTmRegRows, k_loop<8, kTmRegRows, false, true, false>, true};
-const LoopVariant kVariantTmRes = {8, kTmRegRows, k_loop<8, kTmRegRows, true, true, false>, true};
+constexpr int kTmRows = 16;
+constexpr int kTmRegRowsWide = 6, kTmRegRowsNarrow = 8;
+const LoopVariant kVariantTm = {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, false, 1, false>, true};
+const LoopVariant kVariantTmRes = {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, true, 1, false>, true};
+const LoopVariant kVariantTmN = {8, kTmRegRowsNarrow, k_loop<8, kTmRegRowsNarrow, false, 2, false>, true};
+const LoopVariant kVariantTmNRes = {8, kTmRegRowsNarrow, k_loop<8, kTmRegRowsNarrow, true, 2, false>, true};
 // single-cluster variants (the whole problem on kCS SMs, DSMEM exchange): C1/C2-sized systems
 const LoopVariant kVariantsClu[] = {
-    {1, 8, k_loop<1, 8, false, false, true>, false, true},   {2, 8, k_loop<2, 8, false, false, true>, false, true},
-    {4, 8, k_loop<4, 8, false, false, true>, false, true},   {8, 10, k_loop<8, 10, false, false, true>, false, true},
-    {16, 5, k_loop<16, 5, false, false, true>, false, true}, {8, kTmRegRows, k_loop<8, kTmRegRows, false, true, true>, true, true},
+    {1, 8, k_loop<1, 8, false, 0, true>, false, true},   {2, 8, k_loop<2, 8, false, 0, true>, false, true},
+    {4, 8, k_loop<4, 8, false, 0, true>, false, true},   {8, 10, k_loop<8, 10, false, 0, true>, false, true},
+    {16, 5, k_loop<16, 5, false, 0, true>, false, true}, {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, false, 1, true>, true, true},
+    {8, kTmRegRowsNarrow, k_loop<8, kTmRegRowsNarrow, false, 2, true>, true, true},
 };
 const LoopVariant kVariantsRes[] = {
-    {1, 32, k_loop<1, 32, true, false, false>}, {2, 32, k_loop<2, 32, true, false, false>}, {4, 20, k_loop<4, 20, true, false, false>},
-    {8, 10, k_loop<8, 10, true, false, false>}, {16, 5, k_loop<16, 5, true, false, false>},
+    {1, 32, k_loop<1, 32, true, 0, false>}, {2, 32, k_loop<2, 32, true, 0, false>}, {4, 20, k_loop<4, 20, true, 0, false>},
+    {8, 10, k_loop<8, 10, true, 0, false>}, {16, 5, k_loop<16, 5, true, 0, false>},
 };
 // smallest instantiated RRMAX >= want for this CB (want <= rr_max_for(cb))
 const LoopVariant *pick_variant(int cb, int want, bool resmode) {
@@ -1081,19 +1151,28 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         g.rt = 0;
         g.rs = smem_fit(g.rb - g.rr);
         const bool allow_tm = cb == 8 && !(flags & CSK_SOLVE_NO_TMEM);
+        int tmk = 0;  // 1: wide TMEM loads (6 register rows), 2: narrow (8 register rows)
         if (allow_tm && ((flags & CSK_SOLVE_FORCE_TMEM) || g.rb - g.rr > 0)) {
-            g.rr = reg_rows(kTmRegRows);
+            // narrow when every row past 8 register rows fits in TMEM (no shared-memory tier)
+            tmk = (g.rb - kTmRegRowsNarrow <= kTmRows) ? 2 : 1;
+            g.rr = reg_rows(tmk == 2 ? kTmRegRowsNarrow : kTmRegRowsWide);
             g.rt = (g.rb - g.rr) < kTmRows ? (g.rb - g.rr) : kTmRows;
             g.rs = smem_fit(g.rb - g.rr - g.rt);
+            if (g.rt == 0) tmk = 0;
         }
         g.var = nullptr;
         if (clu) {
+            const int want_rr = tmk == 2 ? kTmRegRowsNarrow : tmk == 1 ? kTmRegRowsWide : (g.rr > 0 ? g.rr : 1);
             for (const auto &v : kVariantsClu)
-                if (v.cb == cb && v.tm == (g.rt > 0) && v.rrmax >= (g.rr > 0 ? g.rr : 1) &&
+                if (v.cb == cb && v.tm == (tmk != 0) && v.rrmax >= want_rr && (tmk == 0 || v.rrmax == want_rr) &&
                     (!g.var || v.rrmax < g.var->rrmax))
                     g.var = &v;
+        } else if (tmk == 1) {
+            g.var = resmode ? &kVariantTmRes : &kVariantTm;
+        } else if (tmk == 2) {
+            g.var = resmode ? &kVariantTmNRes : &kVariantTmN;
         } else {
-            g.var = g.rt > 0 ? (resmode ? &kVariantTmRes : &kVariantTm) : pick_variant(cb, g.rr > 0 ? g.rr : 1, resmode);
+            g.var = pick_variant(cb, g.rr > 0 ? g.rr : 1, resmode);
         }
         g.smem = loop_smem(g.rows_max, wpg, cb, n, g.rs).total;
         return g.var != nullptr && g.smem <= static_cast<size_t>(ctx->max_smem_optin);
