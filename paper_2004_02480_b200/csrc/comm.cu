@@ -459,6 +459,8 @@ csk_status_t csk_sketch_sharded(csk_ctx_t ctx, const double *A_local, int64_t ld
 //      CTAs take part in ONE exchange whose {count, max} pair lives in rank 0's memory and is
 //      updated with system-scope atomics over NVLink; the winner's slot and row are read from
 //      the owner's memory through peer mappings (CUDA IPC handles swapped with ncclAllGather).
+constexpr int kXchWordsComm = 16;  // mirrors loop.cu's exchange layout (one 128-B line per pair)
+
 struct IpcRec {
     cudaIpcMemHandle_t a;  // allocation holding this rank's A~ rows
     long long a_off;       // offset of A~_local inside it
@@ -512,6 +514,17 @@ __global__ void k_sumsq_shard(const double *v, int64_t len, double *out) {
         double t = red[0];
         for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = t + red[w];
         *out = t;
+    }
+}
+
+// P2P sanity probe: rank r's word (r+1) * gamma must be readable by every rank through its
+// peer mapping (system-scope loads).  bad = 1 on any mismatch.
+__global__ void k_peer_probe(const unsigned long long *const *words, int P, int *bad) {
+    const int r = threadIdx.x;
+    if (r < P) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(words[r]) : "memory");
+        if (v != static_cast<unsigned long long>(r + 1) * 0x9E3779B97F4A7C15ull) atomicExch(bad, 1);
     }
 }
 
@@ -574,6 +587,32 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
     rs.bt_r[me] = b_tilde_local;
     rs.nsq_r[me] = nsq_local;
     rs.x_r[me] = x;
+    // probe the peer mappings once per solve: every rank writes a word into its exchange buffer,
+    // reads every rank's word through the mappings, and all ranks agree (all-reduce max) on the
+    // outcome; a failure selects the host-driven NCCL loop on every rank
+    {
+        const size_t probe_off = (2 * kXchWordsComm + 8) * 8;  // unused word of the third pair line
+        const unsigned long long mine_w = static_cast<unsigned long long>(me + 1) * 0x9E3779B97F4A7C15ull;
+        CSK_CUDA(ctx, cudaMemcpyAsync(static_cast<unsigned char *>(ctx->slots.ptr) + probe_off, &mine_w, 8,
+                                      cudaMemcpyHostToDevice, s));
+        const unsigned long long *words[kMaxRanks];
+        for (int r = 0; r < P; ++r)
+            words[r] = reinterpret_cast<const unsigned long long *>(
+                reinterpret_cast<const unsigned char *>(rs.slots_r[r]) - xch_bytes + probe_off);
+        void *pb = nullptr;
+        CSK_CUDA(ctx, cudaMallocAsync(&pb, sizeof(words) + 16, s));
+        CSK_CUDA(ctx, cudaMemcpyAsync(pb, words, sizeof(words), cudaMemcpyHostToDevice, s));
+        int *bad = reinterpret_cast<int *>(static_cast<unsigned char *>(pb) + sizeof(words));
+        CSK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), s));
+        CSK_NCCL(ctx, ncclAllReduce(bad, bad, 1, ncclInt32, ncclMax, cm->nccl, s));  // barrier: all words written
+        k_peer_probe<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned long long *const *>(pb), P, bad);
+        CSK_NCCL(ctx, ncclAllReduce(bad, bad, 1, ncclInt32, ncclMax, cm->nccl, s));
+        int bad_h = 0;
+        CSK_CUDA(ctx, cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CSK_CUDA(ctx, cudaStreamSynchronize(s));
+        CSK_CUDA(ctx, cudaFreeAsync(pb, s));
+        if (bad_h) return CSK_E_UNSUPPORTED;  // caller falls back to the host-driven loop
+    }
     // zero the exchange memory, and the global ||b~||^2 for residual mode; the all-reduce is
     // also the barrier that keeps every rank's kernel behind rank 0's zeroed pairs
     CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, ex, s));
@@ -603,8 +642,12 @@ csk_status_t csk_solve_sharded(csk_ctx_t ctx, const double *A_tilde_local, const
     // default: the fused persistent loop over peer memory; CSK_SHARDED_NCCL=1 selects the
     // host-driven loop (local candidate kernel + ncclAllGather + apply kernel per iteration)
     static const bool host_nccl = getenv("CSK_SHARDED_NCCL") != nullptr;
-    if (!host_nccl) return solve_sharded_fused(ctx, A_tilde_local, b_tilde_local, nsq_local, d_lo, d_hi, d, n, x,
-                                               x_star, tol, max_iters, report, s);
+    if (!host_nccl) {
+        const csk_status_t fst = solve_sharded_fused(ctx, A_tilde_local, b_tilde_local, nsq_local, d_lo, d_hi, d, n,
+                                                     x, x_star, tol, max_iters, report, s);
+        if (fst != CSK_E_UNSUPPORTED) return fst;
+        // peer memory unusable (probe failed / no P2P): the host-driven NCCL loop below
+    }
     std::vector<void *> owned;
     std::vector<RankView> rv(1);
     rv[0] = RankView{A_tilde_local, b_tilde_local, nsq_local, d_hi - d_lo, d_lo, x, {}};

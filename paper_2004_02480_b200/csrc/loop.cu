@@ -74,6 +74,7 @@ struct LoopParams {
     //      `rank` of P GPUs (the other ranks' arrays are peer-mapped; sys = 1).  rank = -1: P
     //      virtual ranks in ONE launch (rank = cta / Gr), the 1-GPU test of the decomposition.
     int P, rank, Gr, sys;
+    unsigned long long timeout_ns;          // exchange watchdog
     int64_t dlo[kMaxRanks + 1];             // rank r owns the global rows [dlo[r], dlo[r+1])
     int RMr[kMaxRanks];                     // rank r's rows per CTA, ceil((dlo[r+1]-dlo[r]) / Gr)
     const double *At_r[kMaxRanks];          // rank r's rows of A~ (row dlo[r] first)
@@ -142,6 +143,12 @@ __device__ __forceinline__ void ld_relaxed_v2(const unsigned long long *p, unsig
 }
 // order this thread's generic-proxy view of global memory before its later async-proxy (TMA) reads
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ double lwarp_sum(double v) {
 #pragma unroll
@@ -880,10 +887,22 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
 #endif
                     unsigned long long c, mx;
+                    const unsigned long long t_spin = globaltimer_ns();
+                    bool timed_out = false;
                     do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
                         if (p.sys) ld_relaxed_v2_sys(pair, c, mx);
                         else ld_relaxed_v2(pair, c, mx);
+                        // watchdog: a rank that never arrives (a peer that failed to launch) turns
+                        // into an error instead of a hang
+                        if (c < static_cast<unsigned long long>(G) && globaltimer_ns() - t_spin > p.timeout_ns) {
+                            timed_out = true;
+                            break;
+                        }
                     } while (c < static_cast<unsigned long long>(G));
+                    if (timed_out) {
+                        stop = -3;
+                        mx = 0ull;
+                    }
                     // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the
                     // proxy fence orders this thread's generic view before its TMA reads
                     fence_proxy_async_global();
@@ -939,7 +958,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         if (res <= p.tol) stop = CSK_CONVERGED;
                         else if (k == p.max_iters) stop = CSK_MAX_ITERS;
                     }
-                    if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
+                    if (stop == -1 && mx == 0ull) stop = -2;  // every row masked: zero sketch
                     if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copies
                     }  // global exchange
                 }
@@ -1283,6 +1302,8 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.res_trace = opts ? opts->res_trace : nullptr;
     prm.x_trace = opts ? opts->x_trace : nullptr;
     prm.phase_cycles = opts ? opts->phase_cycles : nullptr;
+    static const double tmo_s = getenv("CSK_EXCHANGE_TIMEOUT_S") ? atof(getenv("CSK_EXCHANGE_TIMEOUT_S")) : 30.0;
+    prm.timeout_ns = static_cast<unsigned long long>(tmo_s * 1e9);
     prm.skew = (opts && opts->phase_cycles) ? reinterpret_cast<long long *>(opts->phase_cycles) + 32 : nullptr;
     if (prm.trace_cap <= 0) { prm.idx_trace = nullptr; prm.res_trace = nullptr; prm.x_trace = nullptr; prm.trace_cap = 0; }
 

@@ -962,6 +962,9 @@ csk_status_t finish_solve(csk_ctx_t ctx, csk_report_t *report) {
     CSK_CUDA(ctx, cudaStreamSynchronize(ctx->pending_stream));
     const int64_t *rep = ctx->report_host;
     if (rep[2] == -2) return fail(ctx, CSK_E_ZERO_SKETCH, "csk_solve: every row of A~ is zero");
+    if (rep[2] == -3)
+        return fail(ctx, CSK_E_CUDA, "csk_solve: exchange watchdog -- not every CTA / rank arrived within "
+                                     "CSK_EXCHANGE_TIMEOUT_S (default 30 s)");
     if (!report) return CSK_OK;
     report->iterations = rep[0];
     double fr;
