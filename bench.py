@@ -6,7 +6,8 @@ One "step" = one pass of the whole hot path over one synthetic problem resident 
 HBM: plan (S1/S2) + sketch with fused norms (S3/S4) + the persistent Algorithm 1
 loop (S5-S8) until RES <= 1e-6 or the iteration cap.
 Default workload: config C3 (see DESIGN.md §7 for why C3).  Between timed steps L2
-is flushed by writing a 256 MiB buffer (untimed).
+is flushed by writing a 256 MiB buffer (untimed) unless A is larger than L2 (C3: 400 MB), the
+timing rules' other option.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
@@ -175,12 +176,18 @@ def run_ours(args, dist, rank, ws):
     dev = torch.device("cuda", torch.cuda.current_device())
     p = make_config(cfg, dev)
     ctx = csk.Context()
+    csk.csk_ctx_set_timing(True, ctx=ctx)  # events right around k_sketch_dense / k_loop (roofline)
     d, n = cfg.d, cfg.n
     At = torch.empty(d, n, dtype=torch.float64, device=dev)
     bt = torch.empty(d, dtype=torch.float64, device=dev)
     nsq = torch.empty(d, dtype=torch.float64, device=dev)
     x = torch.zeros(n, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # timing rule: flush L2 between steps OR use inputs larger than L2.  When A exceeds L2
+    # (C3: 400 MB vs 126 MB) nothing of A survives a step, and a write-flush would only leave L2
+    # full of dirty lines whose write-backs then compete with the sketch's HBM reads.
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    do_flush = cfg.bytes_A <= 2 * l2_bytes
     stream = torch.cuda.current_stream()
 
     def step(ev=None):
@@ -204,12 +211,16 @@ def run_ours(args, dist, rank, ws):
     sampler.start()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     reps = []
+    kern_ms = {"sketch": [], "loop": []}
     _barrier(dist)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(args.steps):
-        flush.fill_(1.0)  # untimed: outside the events of step k
+        if do_flush:
+            flush.fill_(1.0)  # untimed: outside the events of step k
         reps.append(step(evs[k]))
+        for w in kern_ms:  # the step already synchronised (csk_solve_wait)
+            kern_ms[w].append(csk.csk_last_kernel_ms(w, ctx=ctx))
     torch.cuda.synchronize()
     _barrier(dist)
     t1 = time.perf_counter()
@@ -229,9 +240,11 @@ def run_ours(args, dist, rank, ws):
     # C1-C3; registers + TMEM + shared memory at C4).  north_star frames it as the bytes of A~
     # per iteration over the on-chip (SMEM/L2) bandwidth; the FP64 FMA bound is reported beside.
     loop_bytes = alg_bytes_iter(cfg) * it
-    loop_gbs = loop_bytes / (sv_ms * 1e-3) / 1e9
+    k_loop_ms = sum(kern_ms["loop"]) / len(kern_ms["loop"])
+    k_sketch_ms = sum(kern_ms["sketch"]) / len(kern_ms["sketch"])
+    loop_gbs = loop_bytes / (k_loop_ms * 1e-3) / 1e9
     smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
-    loop_tflops = 2.0 * cfg.d * cfg.n * it / (sv_ms * 1e-3) / 1e12
+    loop_tflops = 2.0 * cfg.d * cfg.n * it / (k_loop_ms * 1e-3) / 1e12
     fp64_peak = 148 * DFMA_PER_CLK_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
     sketch_gbs = alg_bytes_sketch(cfg) / (sk_ms * 1e-3) / 1e9
     out = {
@@ -250,7 +263,8 @@ def run_ours(args, dist, rank, ws):
         "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "kind": cfg.kind,
                    "tol": cfg.tol, "max_iters": cfg.max_iters, "sketch_seed": cfg.sketch_seed,
                    "per_rank": "independent problem per rank" if ws > 1 else "single problem",
-                   "l2": "flushed between steps (256 MiB write, untimed); A (%.0f MB) > L2" % (cfg.bytes_A / 1e6)},
+                   "l2": ("flushed between steps (256 MiB write, untimed)" if do_flush else
+                          "input larger than L2 (A = %.0f MB > %.0f MB L2): no flush" % (cfg.bytes_A / 1e6, l2_bytes / 1e6))},
         "iterations": it,
         "final_res": reps[-1].final_res,
         "termination": ["converged", "max_iters", "stagnated"][reps[-1].termination],
@@ -266,7 +280,10 @@ def run_ours(args, dist, rank, ws):
                      "traffic_note": "DRAM bytes of the whole k_loop launch (one launch = the whole loop): "
                                      "A~ is read once into registers/TMEM/shared memory and stays on chip",
                      "peak_source": f"derived: 148 SM x {SMEM_BYTES_PER_CLK_PER_SM} B/clk x {sm_max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                     "alg_bytes_per_iteration": alg_bytes_iter(cfg)},
+                     "alg_bytes_per_iteration": alg_bytes_iter(cfg),
+                     "kernel_ms": round(k_loop_ms, 5),
+                     "timing": "CUDA events recorded by libcsk on the launching stream right around k_loop "
+                               "(csk_ctx_set_timing), mean over the timed steps"},
         "roofline_fp64": {"kernel": "k_loop", "bound": "alu", "achieved": round(loop_tflops, 3),
                           "peak": round(fp64_peak, 2), "unit": "TFLOP/s", "frac": round(loop_tflops / fp64_peak, 4),
                           "peak_source": f"derived: 148 SM x {DFMA_PER_CLK_PER_SM} DFMA/clk x 2 x {sm_max_mhz:.0f} MHz "
@@ -274,11 +291,16 @@ def run_ours(args, dist, rank, ws):
                           "alg_flops_per_iteration": 2 * cfg.d * cfg.n,
                           "note": "the loop is latency-bound: one grid-wide exchange (atomic max-key + count, "
                                   "~2.3k cycles floor measured) per iteration"},
-        "roofline_sketch": {"kernel": "plan + k_sketch_dense", "bound": "hbm",
-                            "achieved": round(sketch_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                            "frac": round(sketch_gbs / hbm_peak, 4), "peak_source": peak_src,
-                            "alg_bytes": alg_bytes_sketch(cfg),
-                            "traffic": _ncu_traffic(f"r01_ncu_sketch_{cfg.name}.txt")},
+        "roofline_sketch": {"kernel": "k_sketch_dense", "bound": "hbm",
+                            "achieved": round(alg_bytes_sketch(cfg) / (k_sketch_ms * 1e-3) / 1e9, 1),
+                            "peak": hbm_peak, "unit": "GB/s",
+                            "frac": round(alg_bytes_sketch(cfg) / (k_sketch_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                            "peak_source": peak_src, "alg_bytes": alg_bytes_sketch(cfg),
+                            "kernel_ms": round(k_sketch_ms, 5),
+                            "traffic": _ncu_traffic(f"r01_ncu_sketch_{cfg.name}.txt"),
+                            "with_plan": {"ms": round(sk_ms, 5), "achieved": round(sketch_gbs, 1),
+                                          "frac": round(sketch_gbs / hbm_peak, 4),
+                                          "note": "whole csk_sketch call: hash + CUB radix-sort plan + sketch"}},
         "clocks": clocks,
         "gpu_launches": 4 * args.steps,
         "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB onesweep radix-sort kernels and one memset)",

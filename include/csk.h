@@ -188,6 +188,13 @@ CSK_API csk_status_t csk_solve_ex(csk_ctx_t ctx, const double *A_tilde, const do
  * (e.g. CSK_E_ZERO_SKETCH).  x is valid only after this returns. */
 CSK_API csk_status_t csk_solve_wait(csk_ctx_t ctx, csk_report_t *report);
 
+/* Per-kernel timing for the roofline (bench.py): with timing on, the library records CUDA
+ * events on the launching stream right around the sketch kernel (k_sketch_dense, which = 0) and
+ * the loop kernel (k_loop, which = 1).  csk_last_kernel_ms synchronises on the end event and
+ * returns the last launch's duration in ms.  Off by default (no events recorded). */
+CSK_API csk_status_t csk_ctx_set_timing(csk_ctx_t ctx, int32_t on);
+CSK_API csk_status_t csk_last_kernel_ms(csk_ctx_t ctx, int32_t which, float *ms);
+
 /* Launch geometry the last csk_solve* on this ctx used: CTAs, CTAs per cluster, rows of
  * A~ kept in shared memory per CTA (any pointer may be NULL). */
 CSK_API csk_status_t csk_last_solve_geometry(csk_ctx_t ctx, int32_t *num_ctas, int32_t *cluster_size,

@@ -86,6 +86,8 @@ def _load():
         "csk_solve_ex": ([P, P, P, P, i64, i64, P, P, dbl, i64, ctypes.POINTER(SolveOpts),
                           ctypes.POINTER(Report), P], i32),
         "csk_solve_wait": ([P, ctypes.POINTER(Report)], i32),
+        "csk_ctx_set_timing": ([P, i32], i32),
+        "csk_last_kernel_ms": ([P, i32, ctypes.POINTER(ctypes.c_float)], i32),
         "csk_last_solve_geometry": ([P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_int32)], i32),
         "csk_run": ([P, P, i64, P, i64, i64, i64, u64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
@@ -339,6 +341,20 @@ def csk_solve_async(At, bt, nsq, x, x_star=None, tol: float = 1e-6, max_iters: i
     opts.flags = SOLVE_ASYNC
     ctx.check(lib.csk_solve_ex(ctx.handle, _ptr(At), _ptr(bt), _ptr(nsq), d, n, _ptr(x), _ptr(x_star),
                                float(tol), int(max_iters), ctypes.byref(opts), None, _stream()))
+
+
+def csk_ctx_set_timing(on: bool = True, ctx: Context | None = None):
+    """Record CUDA events around the sketch and loop kernels of later calls on `ctx`."""
+    ctx = ctx or default_context()
+    ctx.check(lib.csk_ctx_set_timing(ctx.handle, 1 if on else 0))
+
+
+def csk_last_kernel_ms(which: str, ctx: Context | None = None) -> float:
+    """Duration (ms) of the last timed 'sketch' (k_sketch_dense) or 'loop' (k_loop) launch."""
+    ctx = ctx or default_context()
+    ms = ctypes.c_float()
+    ctx.check(lib.csk_last_kernel_ms(ctx.handle, {"sketch": 0, "loop": 1}[which], ctypes.byref(ms)))
+    return ms.value
 
 
 def csk_last_solve_geometry(ctx: Context | None = None) -> dict:

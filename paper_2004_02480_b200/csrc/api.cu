@@ -156,6 +156,8 @@ csk_status_t csk_ctx_destroy(csk_ctx_t ctx) {
                         &ctx->report, &ctx->scalars};
     for (Workspace *w : all) release(*w);
     if (ctx->report_host) cudaFreeHost(ctx->report_host);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
     return CSK_OK;
 }
@@ -232,6 +234,24 @@ csk_status_t csk_solve_wait(csk_ctx_t ctx, csk_report_t *report) {
     if (!ctx) return CSK_E_ARG;
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     return finish_solve(ctx, report);
+}
+
+csk_status_t csk_ctx_set_timing(csk_ctx_t ctx, int32_t on) {
+    if (!ctx) return CSK_E_ARG;
+    CSK_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (on && !ctx->ev[0])
+        for (auto &e : ctx->ev) CSK_CUDA(ctx, cudaEventCreate(&e));
+    ctx->timing = on != 0;
+    ctx->ev_recorded[0] = ctx->ev_recorded[1] = false;
+    return CSK_OK;
+}
+
+csk_status_t csk_last_kernel_ms(csk_ctx_t ctx, int32_t which, float *ms) {
+    if (!ctx || !ms || which < 0 || which > 1) return ctx ? fail(ctx, CSK_E_ARG, "csk_last_kernel_ms: bad arguments") : CSK_E_ARG;
+    if (!ctx->ev_recorded[which]) return fail(ctx, CSK_E_ARG, "csk_last_kernel_ms: no timed launch yet (csk_ctx_set_timing)");
+    CSK_CUDA(ctx, cudaEventSynchronize(ctx->ev[2 * which + 1]));
+    CSK_CUDA(ctx, cudaEventElapsedTime(ms, ctx->ev[2 * which], ctx->ev[2 * which + 1]));
+    return CSK_OK;
 }
 
 csk_status_t csk_last_solve_geometry(csk_ctx_t ctx, int32_t *num_ctas, int32_t *cluster_size,

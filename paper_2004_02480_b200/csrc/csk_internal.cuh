@@ -47,6 +47,10 @@ struct csk_ctx_s {
     std::map<std::tuple<const void *, int, size_t>, int> occ_cache;  // (fn, cluster, smem) -> n
     int64_t cub_key_m = -1, cub_key_bits = -1;
     size_t cub_bytes = 0;
+    // per-kernel CUDA-event timing (csk_ctx_set_timing): [0,1] sketch kernel, [2,3] loop kernel
+    bool timing = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool ev_recorded[2] = {false, false};
 };
 
 namespace csk {
@@ -59,6 +63,12 @@ csk_status_t ensure(csk_ctx_t ctx, Workspace &w, size_t bytes);
 csk_status_t raise_smem(csk_ctx_t ctx, const void *fn);
 // cudaOccupancyMaxActiveClusters (cs > 1) or blocks-per-SM x SMs (cs == 1), memoised.
 csk_status_t max_resident(csk_ctx_t ctx, const void *fn, int cs, int threads, size_t smem, int *out);
+// Kernel timing hooks: record event 2*which (before) / 2*which+1 (after) when timing is on.
+inline void time_mark(csk_ctx_t ctx, int which, bool after, cudaStream_t s) {
+    if (!ctx->timing) return;
+    cudaEventRecord(ctx->ev[2 * which + (after ? 1 : 0)], s);
+    if (after) ctx->ev_recorded[which] = true;
+}
 
 #define CSK_CUDA(ctx, call)                                   \
     do {                                                      \

@@ -1327,7 +1327,9 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     // Profiling only (ncu cannot replay cooperative launches): same kernel without the attribute.
     static const bool noncoop = getenv("CSK_PROFILE_NONCOOP") != nullptr;
     if (noncoop && !clu) cfg.numAttrs = 0;
+    time_mark(ctx, 1, false, stream);
     CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, prm));
+    time_mark(ctx, 1, true, stream);
     static const bool dbg = getenv("CSK_DEBUG") != nullptr;
     if (dbg)
         fprintf(stderr, "[csk] loop: d=%lld n=%lld G=%d cluster=%d wpg=%d cb=%d rrmax=%d tm=%d rr=%d rt=%d rs=%d rows/CTA=%d smem=%zu\n",

@@ -451,6 +451,7 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
 #define CSK_LAUNCH_DENSE_RB(PP, T, R)                                                                   \
     {                                                                                                   \
         CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_dense<PP, T, R>)));           \
+        time_mark(ctx, 0, false, stream);                                                              \
         k_sketch_dense<PP, T, R><<<grid, threads, g.smem, stream>>>(                                    \
             A, lda, b, m, n, d, perm, offsets, At, bt, nsq, g.tc, g.chunk_cols, g.chunks,               \
             g.slot_bytes, g.rb, g.stages, static_cast<int>(g.header));                                  \
@@ -473,6 +474,7 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
     }
 #undef CSK_LAUNCH_DENSE
 #undef CSK_LAUNCH_DENSE_RB
+    time_mark(ctx, 0, true, stream);
     CSK_CUDA(ctx, cudaGetLastError());
     return CSK_OK;
 }
