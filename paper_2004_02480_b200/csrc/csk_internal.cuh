@@ -47,6 +47,11 @@ struct csk_ctx_s {
     std::map<std::tuple<const void *, int, size_t>, int> occ_cache;  // (fn, cluster, smem) -> n
     int64_t cub_key_m = -1, cub_key_bits = -1;
     size_t cub_bytes = 0;
+    // csk_sketch as a replayed CUDA graph (hash, radix-sort plan, offsets, sketch: one submit)
+    // per argument tuple: the first call runs eagerly (sizes the workspaces), the second captures
+    std::map<std::string, cudaGraphExec_t> sketch_graphs;
+    std::set<std::string> sketch_seen;
+    cudaStream_t cap_stream = nullptr;  // private stream the graph is captured on
     // per-kernel CUDA-event timing (csk_ctx_set_timing): [0,1] sketch kernel, [2,3] loop kernel
     bool timing = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
