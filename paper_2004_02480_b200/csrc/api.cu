@@ -24,7 +24,7 @@ csk_status_t ensure(csk_ctx_t ctx, Workspace &w, size_t bytes) {
     if (w.bytes >= bytes) return CSK_OK;
     if (w.ptr) {
         // captured sketch graphs hold the old workspace pointers
-        for (auto &kv : ctx->sketch_graphs) cudaGraphExecDestroy(kv.second);
+        for (auto &kv : ctx->sketch_graphs) cudaGraphExecDestroy(kv.second.exec);
         ctx->sketch_graphs.clear();
         ctx->sketch_seen.clear();
         // the old buffer may still be in use by queued work on any stream
@@ -163,7 +163,7 @@ csk_status_t csk_ctx_destroy(csk_ctx_t ctx) {
     if (ctx->report_host) cudaFreeHost(ctx->report_host);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    for (auto &kv : ctx->sketch_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto &kv : ctx->sketch_graphs) cudaGraphExecDestroy(kv.second.exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
     return CSK_OK;
@@ -178,53 +178,50 @@ csk_status_t csk_sketch(csk_ctx_t ctx, const double *A, int64_t lda, const doubl
     CSK_CHECK(check_dense(ctx, "csk_sketch", A, lda, b, m, n, d, false, A_tilde, b_tilde));
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = as_stream(stream);
-    auto eager = [&](cudaStream_t st) -> csk_status_t {
-        int32_t *perm = nullptr, *offsets = nullptr;
-        CSK_CHECK(build_plan(ctx, seed, 0, m, d, nullptr, nullptr, &perm, &offsets, st));
-        return launch_sketch_dense(ctx, A, lda, b, m, n, d, perm, offsets, A_tilde, b_tilde, nsq, st);
-    };
     static const bool no_graph = getenv("CSK_NO_GRAPH") != nullptr;
-    if (no_graph) return eager(s);
-    // the same call again: replay its graph (one submit instead of ~6 launches + host gaps)
-    char kb[256];
-    snprintf(kb, sizeof(kb), "%p,%lld,%p,%lld,%lld,%lld,%llu,%p,%p,%p,%p,%d", static_cast<const void *>(A),
-             static_cast<long long>(lda), static_cast<const void *>(b), static_cast<long long>(m),
-             static_cast<long long>(n), static_cast<long long>(d), static_cast<unsigned long long>(seed),
-             static_cast<void *>(A_tilde), static_cast<void *>(b_tilde), static_cast<void *>(nsq),
-             static_cast<void *>(s), ctx->timing ? 1 : 0);
+    int32_t *perm = nullptr, *offsets = nullptr;
+    if (no_graph) {
+        CSK_CHECK(build_plan(ctx, seed, 0, m, d, nullptr, nullptr, &perm, &offsets, s));
+        return launch_sketch_dense(ctx, A, lda, b, m, n, d, perm, offsets, A_tilde, b_tilde, nsq, s);
+    }
+    // The plan (hash + CUB radix sort + bucket offsets, ~6 launches) depends only on (seed, m, d):
+    // from the second identical call on it is replayed as a CUDA graph (one submit, no host gaps
+    // between its kernels); the sketch kernel is launched after it on `s` as usual
+    char kb[128];
+    snprintf(kb, sizeof(kb), "%lld,%lld,%llu,%p", static_cast<long long>(m), static_cast<long long>(d),
+             static_cast<unsigned long long>(seed), static_cast<void *>(s));
     const std::string key(kb);
     auto it = ctx->sketch_graphs.find(key);
-    if (it != ctx->sketch_graphs.end()) {
-        CSK_CUDA(ctx, cudaGraphLaunch(it->second, s));
-        if (ctx->timing) ctx->ev_recorded[0] = true;
-        return CSK_OK;
-    }
-    if (!ctx->sketch_seen.count(key)) {  // first time: eager (sizes every workspace)
-        ctx->sketch_seen.insert(key);
-        return eager(s);
-    }
     cudaStreamCaptureStatus cs;
     CSK_CUDA(ctx, cudaStreamIsCapturing(s, &cs));
-    if (cs != cudaStreamCaptureStatusNone) return eager(s);  // the caller is capturing: stay inline
-    // capture on a private stream (the legacy default stream cannot capture); launch on `s`
-    if (!ctx->cap_stream) CSK_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
-    CSK_CUDA(ctx, cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-    const csk_status_t st = eager(ctx->cap_stream);
-    cudaGraph_t g = nullptr;
-    const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
-    if (st != CSK_OK) {
-        if (g) cudaGraphDestroy(g);
-        return st;
+    if (it != ctx->sketch_graphs.end()) {
+        CSK_CUDA(ctx, cudaGraphLaunch(it->second.exec, s));
+        perm = it->second.perm;
+        offsets = it->second.offsets;
+    } else if (!ctx->sketch_seen.count(key) || cs != cudaStreamCaptureStatusNone) {
+        // first time (sizes every workspace), or the caller is capturing: inline
+        ctx->sketch_seen.insert(key);
+        CSK_CHECK(build_plan(ctx, seed, 0, m, d, nullptr, nullptr, &perm, &offsets, s));
+    } else {
+        // capture on a private stream (the legacy default stream cannot capture); launch on `s`
+        if (!ctx->cap_stream) CSK_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        CSK_CUDA(ctx, cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+        const csk_status_t st = build_plan(ctx, seed, 0, m, d, nullptr, nullptr, &perm, &offsets, ctx->cap_stream);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
+        if (st != CSK_OK) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (ce != cudaSuccess) return cuda_fail(ctx, ce, "cudaStreamEndCapture(csk_sketch plan)");
+        cudaGraphExec_t ex = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) return cuda_fail(ctx, ie, "cudaGraphInstantiate(csk_sketch plan)");
+        ctx->sketch_graphs[key] = {ex, perm, offsets};
+        CSK_CUDA(ctx, cudaGraphLaunch(ex, s));
     }
-    if (ce != cudaSuccess) return cuda_fail(ctx, ce, "cudaStreamEndCapture(csk_sketch)");
-    cudaGraphExec_t ex = nullptr;
-    const cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
-    cudaGraphDestroy(g);
-    if (ie != cudaSuccess) return cuda_fail(ctx, ie, "cudaGraphInstantiate(csk_sketch)");
-    ctx->sketch_graphs[key] = ex;
-    CSK_CUDA(ctx, cudaGraphLaunch(ex, s));
-    if (ctx->timing) ctx->ev_recorded[0] = true;
-    return CSK_OK;
+    return launch_sketch_dense(ctx, A, lda, b, m, n, d, perm, offsets, A_tilde, b_tilde, nsq, s);
 }
 
 csk_status_t csk_sketch_with_map(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,

@@ -49,7 +49,11 @@ struct csk_ctx_s {
     size_t cub_bytes = 0;
     // csk_sketch as a replayed CUDA graph (hash, radix-sort plan, offsets, sketch: one submit)
     // per argument tuple: the first call runs eagerly (sizes the workspaces), the second captures
-    std::map<std::string, cudaGraphExec_t> sketch_graphs;
+    struct PlanGraph {  // a captured plan (S2) and the workspaces it writes
+        cudaGraphExec_t exec;
+        int32_t *perm, *offsets;
+    };
+    std::map<std::string, PlanGraph> sketch_graphs;
     std::set<std::string> sketch_seen;
     cudaStream_t cap_stream = nullptr;  // private stream the graph is captured on
     // per-kernel CUDA-event timing (csk_ctx_set_timing): [0,1] sketch kernel, [2,3] loop kernel

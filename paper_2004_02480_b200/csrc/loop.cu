@@ -77,6 +77,7 @@ struct LoopParams {
     unsigned long long timeout_ns;          // exchange watchdog
     int64_t dlo[kMaxRanks + 1];             // rank r owns the global rows [dlo[r], dlo[r+1])
     int RMr[kMaxRanks];                     // rank r's rows per CTA, ceil((dlo[r+1]-dlo[r]) / Gr)
+    unsigned long long rm_magic;            // P = 1: ceil(2^40 / RM) if (d-1) RM < 2^40 (row -> CTA by a multiply), else 0
     const double *At_r[kMaxRanks];          // rank r's rows of A~ (row dlo[r] first)
     const double *bt_r[kMaxRanks];
     const double *nsq_r[kMaxRanks];
@@ -271,8 +272,7 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
                    "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
                    "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
                    "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
-                 :
-                 : "memory");
+                 :);
 }
 __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
@@ -285,8 +285,7 @@ __device__ __forceinline__ void tmem_wait_ld16(uint32_t (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
                    "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
-                 :
-                 : "memory");
+                 :);
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
@@ -887,16 +886,22 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
 #endif
                     unsigned long long c, mx;
-                    const unsigned long long t_spin = globaltimer_ns();
+                    unsigned long long t_spin = 0ull;
+                    uint32_t spins = 0u;
                     bool timed_out = false;
                     do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
                         if (p.sys) ld_relaxed_v2_sys(pair, c, mx);
                         else ld_relaxed_v2(pair, c, mx);
                         // watchdog: a rank that never arrives (a peer that failed to launch) turns
-                        // into an error instead of a hang
-                        if (c < static_cast<unsigned long long>(G) && globaltimer_ns() - t_spin > p.timeout_ns) {
-                            timed_out = true;
-                            break;
+                        // into an error instead of a hang; the clock is read only every 4096 polls
+                        // (a normal exchange ends after a few), so it is off the fast path
+                        if (((++spins) & 4095u) == 0u && c < static_cast<unsigned long long>(G)) {
+                            const unsigned long long now = globaltimer_ns();
+                            if (t_spin == 0ull) t_spin = now;
+                            else if (now - t_spin > p.timeout_ns) {
+                                timed_out = true;
+                                break;
+                            }
                         }
                     } while (c < static_cast<unsigned long long>(G));
                     if (timed_out) {
@@ -914,17 +919,27 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         p.skew[(k - 8) * 2 * G + G + cta] = static_cast<long long>(gt);
                     }
 #endif
+                    LP(8)
                     if (mx != 0ull) {
                         wrow = static_cast<int64_t>(kmask - (mx & kmask));
                         if (lane == 0) {
                             // owner: rank by the row ranges, then its CTA
-                            int orank = 0;
-                            if (p.P > 1)
-                                while (orank + 1 < p.P && p.dlo[orank + 1] <= wrow) ++orank;
-                            const uint32_t olrow = static_cast<uint32_t>(wrow - p.dlo[orank]);
-                            const int olc = static_cast<int>(olrow / static_cast<uint32_t>(p.RMr[orank]));
-                            const unsigned long long *oslot = p.slots_r[orank] + par_off + static_cast<size_t>(olc) * kSlotWords;
-                            const double *orow = p.At_r[orank] + (wrow - p.dlo[orank]) * n;
+                            const unsigned long long *oslot;
+                            const double *orow;
+                            if (p.rm_magic != 0ull) {  // one rank: CTA = row / RM by a multiply-shift
+                                const uint32_t olc = static_cast<uint32_t>((static_cast<unsigned long long>(wrow) * p.rm_magic) >> 40);
+                                oslot = p.slots + par_off + static_cast<size_t>(olc) * kSlotWords;
+                                orow = p.At + wrow * n;
+                            } else {
+                                int orank = 0;
+                                if (p.P > 1)
+                                    while (orank + 1 < p.P && p.dlo[orank + 1] <= wrow) ++orank;
+                                const uint32_t olrow = static_cast<uint32_t>(wrow - p.dlo[orank]);
+                                const int olc = static_cast<int>(olrow / static_cast<uint32_t>(p.RMr[orank]));
+                                oslot = p.slots_r[orank] + par_off + static_cast<size_t>(olc) * kSlotWords;
+                                orow = p.At_r[orank] + (wrow - p.dlo[orank]) * n;
+                            }
+                            LP(11)
                             unsigned long long *sb = const_cast<unsigned long long *>(slotbuf);
                             sb[4] = reinterpret_cast<unsigned long long>(orow);
                             sb[7] = reinterpret_cast<unsigned long long>(oslot);
@@ -933,8 +948,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                                 // mbarrier (odd n: the row is read with plain loads in the update)
                                 const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
                                 mbar_arrive_expect_tx(mbar, rbytes + 32u);
+                                LP(12)
                                 bulk_g2s(sb, oslot, 32u, mbar);
+                                LP(13)
                                 if (even) bulk_g2s(rowbuf, orow, rbytes, mbar);
+                                LP(14)
                             } else {
                                 // across GPUs: the slot by system-scope loads (LL-validated), the
                                 // row by plain loads from the peer's memory in the update
@@ -945,6 +963,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             }
                         }
                     }
+                    LP(9)
                     if (RESMODE) {
                         // ||r_k||^2: the G CTA partials in fixed order (rank-major)
                         double t = 0.0;
@@ -962,6 +981,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copies
                     }  // global exchange
                 }
+                LP(10)
                 if (lane == 0) {
                     ctl[0] = stop;  // -1: copies in flight on mbar
                     ctl[1] = wrow;
@@ -1268,6 +1288,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         prm.P = 1; prm.rank = 0; prm.Gr = G; prm.sys = 0;
         prm.dlo[0] = 0; prm.dlo[1] = d;
         prm.RMr[0] = rows_max;
+        // floor(i / RM) = (i M) >> 40 with M = ceil(2^40 / RM) for every i with i RM < 2^40
+        // (the error i (M RM - 2^40) / 2^40 < i RM / 2^40 < 1 stays below the gap to the next multiple)
+        const unsigned long long M = ((1ull << 40) + static_cast<unsigned long long>(rows_max) - 1) / static_cast<unsigned long long>(rows_max);
+        if (static_cast<double>(d) * rows_max < 1099511627776.0 && static_cast<double>(d) * M < 1.8e19) prm.rm_magic = M;
         prm.At_r[0] = At; prm.bt_r[0] = bt; prm.nsq_r[0] = nsq; prm.x_r[0] = x;
     } else {
         prm.P = ranks->P; prm.rank = ranks->rank; prm.Gr = ranks->Gr; prm.sys = ranks->sys;

@@ -112,6 +112,30 @@ def test_sketch_argument_errors(csk):
         csk.csk_sketch(p.A.cpu(), p.b.cpu(), 10)
 
 
+@pytest.mark.parametrize("timing", [False, True])
+def test_sketch_graph_replay(csk, timing):
+    """Repeated identical csk_sketch calls replay a captured CUDA graph (api.cu): every replay is
+    bit-exact, a grown workspace re-captures, and with timing on the kernel events are recorded
+    inside the graph (csk_last_kernel_ms of a replay is a real duration)."""
+    ctx = csk.Context()
+    if timing:
+        csk.csk_ctx_set_timing(True, ctx=ctx)
+    for m, n, d in [(3000, 64, 500), (3000, 64, 500), (3000, 64, 500), (9000, 96, 800), (9000, 96, 800),
+                    (9000, 96, 800), (3000, 64, 500)]:
+        p = make_dense(m, n, "gauss", m + n, "cuda")
+        out = (torch.full((d, n), float("nan"), dtype=torch.float64, device="cuda"),
+               torch.full((d,), float("nan"), dtype=torch.float64, device="cuda"),
+               torch.full((d,), float("nan"), dtype=torch.float64, device="cuda"))
+        for _ in range(4):  # eager, capture, replay, replay
+            At, bt, _ = csk.csk_sketch(p.A, p.b, d, seed=4, ctx=ctx, out=out)
+            torch.cuda.synchronize()
+            At_o, bt_o = oracle.sketch_dense(_np(p.A), _np(p.b), d, seed=4)
+            assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+            if timing:
+                assert csk.csk_last_kernel_ms("sketch", ctx=ctx) > 0.0
+            out[0].fill_(float("nan"))
+
+
 # ---------------------------------------------------------------- S5-S8 loop
 def _lockstep(At, bt, nsq, xtr, itr, k_max):
     At, bt, nsq = _np(At), _np(bt), _np(nsq)

@@ -15,7 +15,8 @@ import torch  # noqa: E402
 import paper_2004_02480_b200 as csk  # noqa: E402
 from csk_synth import CONFIGS, make_config  # noqa: E402
 
-NAMES = ["gemv+final", "arrive(leader)", "combine+publish", "spin", "post", "B2", "rowwait", "upd"]
+NAMES = ["gemv+final", "arrive(leader)", "combine+publish", "spin", "post", "B2", "rowwait", "upd", "fence",
+         "owner+tma", "stopchk", "owner", "sb+expect", "slotcp", "rowcp"]
 
 
 def main():
@@ -55,8 +56,8 @@ def main():
                 done_spread = (done.max(1).values - done.min(1).values).mean().item()
                 print(f"   skew (ns, mean over 64 iterations): publish spread {spread:.0f}, last publish -> first "
                       f"spin exit {lastpub_to_done:.0f}, spin-exit spread {done_spread:.0f}")
-            w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(8))
-            w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(9) if c[16 + i])
+            w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(15))
+            w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(15) if c[16 + i])
             print(f"{nm} G={geo['num_ctas']} wpg={wpg} IT={r.iterations} {ms * 1e3 / it:.2f} us/it = "
                   f"{ms * 1e6 / it * 1.965:.0f} cyc/it | w0 cyc/it: {w0} | w7: {w7}", flush=True)
 

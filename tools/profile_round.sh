@@ -15,4 +15,7 @@ CSK_PROFILE_NONCOOP=1 timeout 600 ncu --set full --clock-control none --import-s
 python tools/run_solve_once.py C4 2000 > /dev/null 2>&1 && \
 CSK_PROFILE_NONCOOP=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_loop -c 1 \
     -o gpurun_out/${R}_loop_C4 python tools/run_solve_once.py C4 2000 > gpurun_out/${R}_ncu_loop_C4.log 2>&1
+python tools/sketch_time.py C3 > /dev/null 2>&1 && \
+CSK_NO_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sketch_dense -s 2 -c 1 \
+    -o gpurun_out/${R}_sketch_C3 python tools/sketch_time.py C3 > gpurun_out/${R}_ncu_sketch_C3.log 2>&1
 ls -la gpurun_out
