@@ -565,10 +565,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const bool even = (n & 1) == 0;
     const unsigned long long kmask = (1ull << b) - 1ull;
 
-    // finalize lanes keep their row's b~ and 1/nsq in registers (groups of <= 32 rows)
-    const bool fast_fin = ng <= 32;
+    // finalize lanes keep their rows' b~ and 1/nsq in registers (groups of <= 32 rows; with the
+    // TMEM tier <= 64: rows lane and lane + 32)
+    const bool fast_fin = ng <= (TM != 0 ? 64 : 32);
     const double fin_b = (fast_fin && lane < ng) ? btl[lr0 + lane] : 0.0;
     const double fin_i = (fast_fin && lane < ng) ? invl[lr0 + lane] : 0.0;
+    const double fin_b2 = (TM != 0 && fast_fin && lane + 32 < ng) ? btl[lr0 + 32 + lane] : 0.0;
+    const double fin_i2 = (TM != 0 && fast_fin && lane + 32 < ng) ? invl[lr0 + 32 + lane] : 0.0;
     const bool all_reg = rr == ng;  // every row of the group in registers: own partial by shuffle
 
     int64_t k = 0, last = -1;
@@ -739,6 +742,16 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     bk = row_key(sc, r0 + l, b);
                     bl = ri * fin_i;
                     bs = sc;
+                }
+                if (TM != 0 && lane + 32 < ng) {  // second row of the lane (groups of 33..64 rows)
+                    const int l = lr0 + 32 + lane;
+                    double dot = dotp[l];
+                    for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
+                    const double ri = fin_b2 - dot;
+                    const double sc = fin_i2 > 0.0 ? (ri * ri) * fin_i2 : -1.0;
+                    if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
+                    const unsigned long long kk = row_key(sc, r0 + l, b);
+                    if (kk > bk) { bk = kk; bl = ri * fin_i2; bs = sc; }
                 }
             } else for (int l0 = 0; l0 < ng; l0 += 32) {
                 const int l = lr0 + l0 + lane;
