@@ -335,7 +335,40 @@ def run_ours(args, dist, rank, ws):
     # ---- other configs (rank 0, N = 1): evidence for every §8(a) regime
     if rank == 0 and ws == 1 and not args.no_extras:
         out["per_config"] = extras(csk, ctx, [c for c in ("C1", "C2", "C4") if c != cfg.name], flush)
+        # the paper's comparison (Table 1 columns): MWRK on the unsketched system
+        out["vs_mwrk"] = mwrk_compare(csk, ctx, cfg, p, ms_step, it)
     return out
+
+
+def mwrk_compare(csk, ctx, cfg, p, csk_ms, csk_it):
+    """MWRK (Remark 1) on (A, b) itself: row norms of A + the same persistent loop with
+    d = m rows (those that do not fit on chip are re-read from HBM every iteration).  IT speedup
+    and time speedup as defined at P:178 (MWRK over CSK; CSK time = sketch + loop)."""
+    x = torch.zeros(cfg.n, dtype=torch.float64, device="cuda")
+
+    def run(ev=None):
+        x.zero_()
+        if ev:
+            ev[0].record()
+        nsq = csk.csk_row_norms(p.A, ctx=ctx)
+        csk.csk_solve_async(p.A, p.b, nsq, x, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters, ctx=ctx)
+        if ev:
+            ev[1].record()
+        return csk.csk_solve_wait(ctx)
+
+    run()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    rep = run(ev)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1])
+    geo = csk.csk_last_solve_geometry(ctx=ctx)
+    return {"config": cfg.name, "method": "MWRK on the unsketched system (P:69 Remark 1), same loop kernel, d = m",
+            "iterations": rep.iterations, "termination": ["converged", "max_iters", "stagnated"][rep.termination],
+            "final_res": rep.final_res, "ms": round(ms, 4), "us_per_iteration": round(ms * 1e3 / max(rep.iterations, 1), 3),
+            "it_speedup": round(rep.iterations / max(csk_it, 1), 4), "time_speedup": round(ms / csk_ms, 3),
+            "resident_rows_per_cta": geo["smem_rows"],
+            "note": "IT speedup = IT(MWRK)/IT(CSK), time speedup = time(MWRK)/time(CSK) (P:178); "
+                    "MWRK time = row norms + loop, CSK time = sketch + loop"}
 
 
 def extras(csk, ctx, names, flush):

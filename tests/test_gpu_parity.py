@@ -327,6 +327,19 @@ def test_identity_map_solve_is_mwrk(csk):
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
 
 
+@pytest.mark.parametrize("smem_rows,tmem", [(0, None), (-1, False)])
+def test_mwrk_unsketched_parity(csk, smem_rows, tmem):
+    """MWRK on the unsketched system (Remark 1) = the same loop
+    kernel on (A, b, ||A_i||^2) with d = m rows (tmem=False, smem_rows=-1: every row past the
+    register tier re-read from L2/HBM each iteration)."""
+    p = make_dense(12000, 200, "lognormal_rows", 23, "cuda")
+    nsq = csk.csk_row_norms(p.A)
+    g = csk.csk_solve(p.A, p.b, nsq, x_star=p.x_star, smem_rows=smem_rows, tmem=tmem, trace=300, trace_x=True)
+    o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), trace=300)
+    _free_running(g, o)
+    _lockstep(p.A, p.b, nsq, g.x_trace, g.idx_trace, 300)
+
+
 def test_run_and_run_host(csk):
     cfg = CONFIGS["C2"]
     p = make_config(cfg, "cuda")
