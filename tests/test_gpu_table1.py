@@ -1,0 +1,61 @@
+"""Table 1 protocol on the GPU: d = n^2, A, x* ~ randn,
+b = A x*, RES <= 1e-6, cap 20 000.  The GPU's mean IT of CSK and MWRK over seeded trials match
+the paper's printed means (tests/golden/table1_full.txt), and one trial per size runs the same
+number of iterations as the oracle on the same input (same sketch, bit-exact; same i_k)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "table1_full.txt")
+
+
+def _paper():
+    rows = {}
+    for line in open(GOLDEN):
+        if line.startswith("#") or not line.strip():
+            continue
+        m, n, d, ci, mi, _, _ = line.split()
+        rows[(int(m), int(n))] = (int(d), float(ci), float(mi))
+    return rows
+
+
+@pytest.fixture(scope="module")
+def csk():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2004_02480_b200 as m
+    return m
+
+
+def _trial(m, n, t):
+    g = torch.Generator(device="cuda").manual_seed(4242 + 1000 * t + n)
+    xs = torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
+    A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    return A, A @ xs, xs
+
+
+@pytest.mark.parametrize("m,n,trials", [(300000, 50, 24), (300000, 100, 12)])
+def test_table1_iteration_means_on_gpu(csk, m, n, trials):
+    d, csk_it, mwrk_it = _paper()[(m, n)]
+    its, mws = [], []
+    for t in range(trials):
+        A, b, xs = _trial(m, n, t)
+        x, rep = csk.csk_run(A, b, d, seed=t, x_star=xs, max_iters=20000)
+        assert rep.termination == csk.CONVERGED and rep.final_res <= 1e-6
+        its.append(rep.iterations)
+        if t < trials // 2:
+            r = csk.csk_solve(A, b, csk.csk_row_norms(A), x_star=xs, max_iters=20000)
+            assert r.termination == csk.CONVERGED
+            mws.append(r.iterations)
+        if t == 0:  # the oracle on the same input: same iteration count
+            o = oracle.csk(A.cpu().numpy(), b.cpu().numpy(), d, seed=0, x_star=xs.cpu().numpy(), max_iters=20000)
+            assert abs(o.iterations - rep.iterations) <= 1, (o.iterations, rep.iterations)
+    # the printed means are over 50 trials; the trial-to-trial spread of IT is a few iterations
+    assert abs(np.mean(its) - csk_it) <= 0.03 * csk_it, (np.mean(its), csk_it, its)
+    assert abs(np.mean(mws) - mwrk_it) <= 2.5, (np.mean(mws), mwrk_it, mws)
