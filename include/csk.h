@@ -81,6 +81,8 @@ typedef struct {
 #define CSK_SOLVE_LEGACY 2 /* opts->flags: the round-1 cluster/DSMEM kernel (shared-memory rows; A/B only) */
 #define CSK_SOLVE_NO_TMEM 4    /* opts->flags: never keep A~ rows in tensor memory */
 #define CSK_SOLVE_FORCE_TMEM 8 /* opts->flags: use the TMEM row tier whenever the layout allows (tests) */
+#define CSK_SOLVE_NO_STREAM_RING 16 /* opts->flags: rows that do not fit on chip are re-read with plain loads
+                                        instead of the TMA stream ring (tests, A/B) */
 
 typedef struct {
     int32_t num_ctas;      /* persistent CTAs (<= co-resident limit); 0 = auto */

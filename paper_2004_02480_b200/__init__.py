@@ -33,6 +33,7 @@ SOLVE_ASYNC = 1
 SOLVE_LEGACY = 2
 SOLVE_NO_TMEM = 4
 SOLVE_FORCE_TMEM = 8
+SOLVE_NO_STREAM_RING = 16
 
 
 class CskError(RuntimeError):
@@ -285,7 +286,7 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
               num_ctas: int = 0, smem_rows: int = 0, cluster_size: int = 0, trace: int = 0,
               trace_x: bool = False, phase_cycles: torch.Tensor | None = None,
               reg_rows: int = 0, group_warps: int = 0, legacy: bool = False, tmem: bool | None = None,
-              ctx: Context | None = None) -> SolveResult:
+              stream_ring: bool = True, ctx: Context | None = None) -> SolveResult:
     """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel."""
     ctx = ctx or default_context()
     _need(At, torch.float64, "A_tilde", 2)
@@ -302,7 +303,7 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
     opts.reg_rows = reg_rows
     opts.group_warps = group_warps
     opts.flags = ((SOLVE_LEGACY if legacy else 0) | (SOLVE_NO_TMEM if tmem is False else 0)
-                  | (SOLVE_FORCE_TMEM if tmem is True else 0))
+                  | (SOLVE_FORCE_TMEM if tmem is True else 0) | (0 if stream_ring else SOLVE_NO_STREAM_RING))
     idx_t = res_t = x_t = None
     if trace:
         idx_t = torch.full((trace,), -1, dtype=torch.int64, device=At.device)

@@ -77,6 +77,7 @@ struct LoopParams {
     unsigned long long timeout_ns;          // exchange watchdog
     int64_t dlo[kMaxRanks + 1];             // rank r owns the global rows [dlo[r], dlo[r+1])
     int RMr[kMaxRanks];                     // rank r's rows per CTA, ceil((dlo[r+1]-dlo[r]) / Gr)
+    int st_rows, st_stages;                 // ST variants: rows per stream-ring stage, stages per row group
     unsigned long long rm_magic;            // P = 1: ceil(2^40 / RM) if (d-1) RM < 2^40 (row -> CTA by a multiply), else 0
     const double *At_r[kMaxRanks];          // rank r's rows of A~ (row dlo[r] first)
     const double *bt_r[kMaxRanks];
@@ -213,9 +214,14 @@ constexpr size_t kInboxOff = 576;      // [2 parities][kCS][4] doubles: key, lam
 constexpr size_t kXbarOff = 1600;      // 2 mbarriers (one per parity), kCS arrivals each
 constexpr size_t kRowbufOff = 1664;
 struct LoopSmem {
-    size_t ctl, mbar, slotbuf, cand, resp, btl, invl, dotp, xs, rowbuf, arows, total;
+    size_t ctl, mbar, slotbuf, cand, resp, btl, invl, dotp, xs, rowbuf, arows, ring, rbar, total;
 };
-__host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs) {
+// Bytes of one stream-ring stage: st_rows whole rows of A~ (a 128-B multiple)
+__host__ __device__ inline size_t st_stage_bytes(int64_t n, int st_rows) {
+    return (static_cast<size_t>(st_rows) * static_cast<size_t>(n) * 8 + 127) & ~size_t(127);
+}
+__host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int64_t n, int rs, int st_stages = 0,
+                                              int st_rows = 0) {
     // The fixed-size control words and the winner-row buffer come first, at compile-time
     // offsets: the hot loop then addresses them from the shared-memory base without keeping
     // (or rematerialising) pointers in registers.
@@ -236,6 +242,11 @@ __host__ __device__ inline LoopSmem loop_smem(int rows_max, int wpg, int cb, int
     L.dotp = take(static_cast<size_t>(wpg) * rows_max * 8);
     L.xs = take(np * 8);
     L.arows = take(static_cast<size_t>(rs) * cb * kLT * 8);
+    // streamed rows (ST variants): per row group st_stages stages of st_rows rows, and a
+    // full / empty mbarrier pair per stage
+    const int rg = kLW / wpg;
+    L.ring = take(static_cast<size_t>(rg) * st_stages * st_stage_bytes(n, st_rows));
+    L.rbar = take(static_cast<size_t>(rg) * st_stages * 16);
     L.total = o;
     return L;
 }
@@ -415,7 +426,7 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CB, int RRMAX, bool RESMODE, int TM, bool CLU>
+template <int CB, int RRMAX, bool RESMODE, int TM, bool CLU, bool ST = false>
 __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     // CLU: the whole grid is one kCS-CTA thread-block cluster and the exchange is an
     // all-to-all of the CTA candidates over DSMEM (no global atomics)
@@ -450,8 +461,17 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const int rs = (ng - rr - rt) < p.rs ? (ng - rr - rt) : p.rs;
     const int b = p.key_bits;
     const int RM = p.rows_max;
+    // ---- ST: the rows past the on-chip tiers stream through a per-group ring of shared-memory
+    //      stages filled by TMA bulk copies (whole rows, contiguous in A~).  Chunk g (of SC per
+    //      iteration, g counted over the whole loop) holds rows s0 + (g mod SC) SR ... and lives in
+    //      stage g mod SS; the copies of the next iteration's first chunks are issued as soon as
+    //      their stages are drained, so they load during the exchange. ----
+    const int s0 = rr + rt + rs;
+    const int SR = ST ? p.st_rows : 1, SS = ST ? p.st_stages : 1;
+    const int SC = ST ? (ng - s0 + SR - 1) / SR : 0;
+    const bool producer = ST && wg == 0 && lane == 0;
 
-    const LoopSmem L = loop_smem(RM, WPG, CB, n, p.rs);
+    const LoopSmem L = loop_smem(RM, WPG, CB, n, p.rs, ST ? p.st_stages : 0, ST ? p.st_rows : 0);
     volatile int64_t *ctl = reinterpret_cast<volatile int64_t *>(smem + L.ctl);  // [0..3] B2, [4..5] RES
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L.mbar);
     const unsigned long long *slotbuf = reinterpret_cast<const unsigned long long *>(smem + L.slotbuf);  // winner's slot (TMA)
@@ -463,6 +483,17 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     double *xs = reinterpret_cast<double *>(smem + L.xs);      // x* by padded column
     double *rowbuf = reinterpret_cast<double *>(smem + L.rowbuf);
     double *arows = reinterpret_cast<double *>(smem + L.arows) + static_cast<size_t>(grp) * p.rs * CB * TG;
+    const size_t st_stride = ST ? st_stage_bytes(n, SR) / 8 : 0;  // doubles per ring stage
+    double *ring = reinterpret_cast<double *>(smem + L.ring) + static_cast<size_t>(grp) * SS * st_stride;
+    uint64_t *rbar = reinterpret_cast<uint64_t *>(smem + L.rbar) + 2 * grp * SS;  // [SS][full, empty]
+    auto st_issue = [&](uint32_t g) {  // producer: chunk g -> stage g mod SS
+        const int c = static_cast<int>(g % static_cast<uint32_t>(SC));
+        const int st = static_cast<int>(g % static_cast<uint32_t>(SS));
+        const int nr = min(SR, ng - s0 - c * SR);
+        const uint32_t by = static_cast<uint32_t>(nr) * static_cast<uint32_t>(n) * 8u;
+        mbar_arrive_expect_tx(rbar + 2 * st, by);
+        bulk_g2s(ring + st * st_stride, Ash + (r0 - dlo_r + lr0 + s0 + c * SR) * n, by, rbar + 2 * st);
+    };
 
     if (tid == 0) {
         uint32_t dyn;
@@ -472,6 +503,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         if (CLU) {  // one local arrival (the expect_tx) per phase; the peers' st.async bring the bytes
             mbar_init(reinterpret_cast<uint64_t *>(smem + kXbarOff), 1);
             mbar_init(reinterpret_cast<uint64_t *>(smem + kXbarOff) + 1, 1);
+        }
+        if constexpr (ST) {  // per stage: full (the producer's expect_tx + the bytes), empty (the group's warps)
+            uint64_t *rb = reinterpret_cast<uint64_t *>(smem + L.rbar);
+            for (int i = 0; i < RG * p.st_stages; ++i) {
+                mbar_init(rb + 2 * i, 1);
+                mbar_init(rb + 2 * i + 1, static_cast<uint32_t>(WPG));
+            }
         }
         fence_mbar_init();
     }
@@ -542,6 +580,10 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         }
     }
     __syncthreads();
+    if constexpr (ST) {  // the first SS chunks (barrier inits are visible after the CTA barrier)
+        if (producer && SC > 0)
+            for (int g = 0; g < SS; ++g) st_issue(static_cast<uint32_t>(g));
+    }
 
     // ||x*||^2 by the last row group (every group holds all of x; fixed order: thread q-order
     // fma, warp butterfly, warps in order).  The last group also owns the RES test and the
@@ -701,25 +743,59 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 }
             }
         }
-        // ---- S6 GEMV: streamed rows (L2/HBM), two rows per pass ----
-        for (int i = rr + rt + rs; i < ng; i += 2) {
-            const bool two = i + 1 < ng;
-            const double *s0 = Ash + (r0 - dlo_r + lr0 + i) * n;
-            const double *s1 = two ? s0 + n : s0;
-            double u0 = 0.0, u1 = 0.0;
+        if constexpr (ST) {
+            // ---- S6 GEMV: streamed rows from the TMA ring, SR (<= 4) rows per stage, transposed
+            //      tree (row j of a stage ends in lanes [8j, 8j + 8)) ----
+            for (int c = 0; c < SC; ++c) {
+                const uint32_t g = static_cast<uint32_t>(k) * static_cast<uint32_t>(SC) + static_cast<uint32_t>(c);
+                const int st = static_cast<int>(g % static_cast<uint32_t>(SS));
+                const uint32_t par = (g / static_cast<uint32_t>(SS)) & 1u;
+                const int nr = min(SR, ng - s0 - c * SR);
+                mbar_wait(rbar + 2 * st, par);
+                const double *rp = ring + st * st_stride;
+                double u[4];
 #pragma unroll
-            for (int q = 0; q < CB; ++q) {
-                const int c = tg + TG * q;
-                const double v0 = c < n ? ldg_stream1(s0 + c) : 0.0;
-                const double v1 = c < n ? ldg_stream1(s1 + c) : 0.0;
-                u0 = __fma_rn(v0, x[q], u0);
-                u1 = __fma_rn(v1, x[q], u1);
+                for (int j = 0; j < 4; ++j) u[j] = 0.0;
+#pragma unroll
+                for (int q = 0; q < CB; ++q) {
+                    const int col = tg + TG * q;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double v = (j < nr && col < n) ? rp[j * n + col] : 0.0;
+                        u[j] = __fma_rn(v, x[q], u[j]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(rbar + 2 * st + 1);  // this warp is done with the stage
+                const double sj = treduce<4>(u, lane);
+                const int j = lane >> 3;
+                if ((lane & 7) == 0 && j < nr) dotp[wg * RM + lr0 + s0 + c * SR + j] = sj;
+                if (producer) {  // refill the stage with chunk g + SS once every warp has read it
+                    mbar_wait(rbar + 2 * st + 1, par);
+                    st_issue(g + static_cast<uint32_t>(SS));
+                }
             }
-            u0 = lwarp_sum(u0);
-            u1 = lwarp_sum(u1);
-            if (lane == 0) {
-                dotp[wg * RM + lr0 + i] = u0;
-                if (two) dotp[wg * RM + lr0 + i + 1] = u1;
+        } else {
+            // ---- S6 GEMV: streamed rows (L2/HBM), two rows per pass ----
+            for (int i = rr + rt + rs; i < ng; i += 2) {
+                const bool two = i + 1 < ng;
+                const double *s0 = Ash + (r0 - dlo_r + lr0 + i) * n;
+                const double *s1 = two ? s0 + n : s0;
+                double u0 = 0.0, u1 = 0.0;
+    #pragma unroll
+                for (int q = 0; q < CB; ++q) {
+                    const int c = tg + TG * q;
+                    const double v0 = c < n ? ldg_stream1(s0 + c) : 0.0;
+                    const double v1 = c < n ? ldg_stream1(s1 + c) : 0.0;
+                    u0 = __fma_rn(v0, x[q], u0);
+                    u1 = __fma_rn(v1, x[q], u1);
+                }
+                u0 = lwarp_sum(u0);
+                u1 = lwarp_sum(u1);
+                if (lane == 0) {
+                    dotp[wg * RM + lr0 + i] = u0;
+                    if (two) dotp[wg * RM + lr0 + i + 1] = u1;
+                }
             }
         }
         // ---- S7 (group): r_i = b~_i - dot, score, lambda, key; group argmax -> cand[grp] ----
@@ -1041,6 +1117,15 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         prow_ptr = reinterpret_cast<const double *>(slotbuf[4]);
     }
 #undef LP
+    if constexpr (ST) {  // drain the copies already issued for the iteration that never ran
+        if (producer && SC > 0) {
+            const uint32_t g0 = static_cast<uint32_t>(k + 1) * static_cast<uint32_t>(SC);
+            for (int i = 0; i < SS; ++i) {
+                const uint32_t g = g0 + static_cast<uint32_t>(i);
+                mbar_wait(rbar + 2 * (g % static_cast<uint32_t>(SS)), (g / static_cast<uint32_t>(SS)) & 1u);
+            }
+        }
+    }
 #if CSK_PHASE_PROF
     if (prof)
         for (int i = 0; i < 16; ++i) p.phase_cycles[(warp == 0 ? 0 : 1) * 16 + i] = ph[i];
@@ -1111,6 +1196,14 @@ const LoopVariant kVariantsClu[] = {
     {16, 5, k_loop<16, 5, false, 0, true>, false, true}, {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, false, 1, true>, true, true},
     {8, kTmRegRowsNarrow, k_loop<8, kTmRegRowsNarrow, false, 2, true>, true, true},
 };
+// Stream-ring variants (rows past the on-chip tiers through TMA stages; x* stop rule only):
+// few register rows, so the registers go to the streamed chunk's loads
+const LoopVariant kVariantsSt[] = {
+    {1, 8, k_loop<1, 8, false, 0, false, true>},  {2, 8, k_loop<2, 8, false, 0, false, true>},
+    {4, 8, k_loop<4, 8, false, 0, false, true>},  {8, 8, k_loop<8, 8, false, 0, false, true>},
+    {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, false, 1, false, true>, true},
+};
+constexpr size_t kRingMaxBytes = 128 * 1024;  // per CTA, all groups' stages
 const LoopVariant kVariantsRes[] = {
     {1, 32, k_loop<1, 32, true, 0, false>}, {2, 32, k_loop<2, 32, true, 0, false>}, {4, 20, k_loop<4, 20, true, 0, false>},
     {8, 10, k_loop<8, 10, true, 0, false>}, {16, 5, k_loop<16, 5, true, 0, false>},
@@ -1170,8 +1263,12 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     const int rg = kLW / wpg;
     // Geometry for G CTAs: row tiers per group -- registers, then TMEM (8 columns per thread
     // only), then shared memory, then re-read from L2/HBM.
+    // the ring's TMA copies need 16-B aligned rows: every rank's A~ base aligned, n even
+    bool st_aligned = (reinterpret_cast<uintptr_t>(At) & 15) == 0;
+    if (multi)
+        for (int r = 0; r < ranks->P; ++r) st_aligned = st_aligned && (reinterpret_cast<uintptr_t>(ranks->At_r[r]) & 15) == 0;
     struct Geo {
-        int G, rows_max, rb, rr, rt, rs;
+        int G, rows_max, rb, rr, rt, rs, st_rows, st_stages;
         size_t smem;
         const LoopVariant *var;
     };
@@ -1186,9 +1283,13 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
             else if (opts && opts->reg_rows > 0 && opts->reg_rows < r) r = opts->reg_rows;
             return r < g.rb ? r : g.rb;
         };
+        g.st_rows = 0;
+        g.st_stages = 0;
         auto smem_fit = [&](int rest) {
             int f = 0;
-            while (f < rest && loop_smem(g.rows_max, wpg, cb, n, f + 1).total <= static_cast<size_t>(ctx->max_smem_optin)) ++f;
+            while (f < rest && loop_smem(g.rows_max, wpg, cb, n, f + 1, g.st_stages, g.st_rows).total <=
+                                   static_cast<size_t>(ctx->max_smem_optin))
+                ++f;
             if (opts && opts->smem_rows < 0) f = 0;
             else if (opts && opts->smem_rows > 0 && opts->smem_rows < f) f = opts->smem_rows;
             return f;
@@ -1226,7 +1327,29 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         } else {
             g.var = pick_variant(cb, g.rr > 0 ? g.rr : 1, resmode);
         }
-        g.smem = loop_smem(g.rows_max, wpg, cb, n, g.rs).total;
+        // rows left over for L2/HBM: stream them through a TMA ring (whole rows, 16-B aligned:
+        // n even and an aligned A~), taking shared memory from the resident rows
+        if (!clu && !resmode && g.var && g.rr + g.rt + g.rs < g.rb && (n % 2) == 0 && st_aligned &&
+            !(flags & CSK_SOLVE_NO_STREAM_RING)) {
+            const LoopVariant *sv = nullptr;
+            for (const auto &v : kVariantsSt)
+                if (v.cb == cb && v.tm == (tmk == 1)) sv = &v;
+            int R = 4;
+            while (R > 1 && static_cast<int64_t>(R) * n * 8 > 65536) R >>= 1;
+            const size_t sb = st_stage_bytes(n, R);
+            const size_t fixed = loop_smem(g.rows_max, wpg, cb, n, 0, 0, 0).total + static_cast<size_t>(rg) * 8 * 16;
+            const size_t avail = static_cast<size_t>(ctx->max_smem_optin) > fixed ? ctx->max_smem_optin - fixed : 0;
+            const size_t budget = avail < kRingMaxBytes ? avail : kRingMaxBytes;
+            const int S = static_cast<int>(std::min<size_t>(8, budget / (static_cast<size_t>(rg) * sb)));
+            if (sv && tmk != 2 && S >= 2) {
+                g.var = sv;
+                if (g.rr > sv->rrmax) g.rr = sv->rrmax;
+                g.st_rows = R;
+                g.st_stages = S;
+                g.rs = smem_fit(g.rb - g.rr - g.rt);
+            }
+        }
+        g.smem = loop_smem(g.rows_max, wpg, cb, n, g.rs, g.st_stages, g.st_rows).total;
         return g.var != nullptr && g.smem <= static_cast<size_t>(ctx->max_smem_optin);
     };
     Geo geo{};
@@ -1332,6 +1455,8 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.rr = rr;
     prm.rs = rs;
     prm.rt = rt;
+    prm.st_rows = geo.st_rows;
+    prm.st_stages = geo.st_stages;
     prm.key_bits = kb;
     prm.rows_max = rows_max;
     prm.trace_cap = opts ? opts->trace_cap : 0;
@@ -1369,8 +1494,9 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     time_mark(ctx, 1, true, stream);
     static const bool dbg = getenv("CSK_DEBUG") != nullptr;
     if (dbg)
-        fprintf(stderr, "[csk] loop: d=%lld n=%lld G=%d cluster=%d wpg=%d cb=%d rrmax=%d tm=%d rr=%d rt=%d rs=%d rows/CTA=%d smem=%zu\n",
-                (long long)d, (long long)n, G, clu ? kCS : 0, wpg, cb, var->rrmax, (int)var->tm, rr, rt, rs, rows_max, smem);
+        fprintf(stderr, "[csk] loop: d=%lld n=%lld G=%d cluster=%d wpg=%d cb=%d rrmax=%d tm=%d rr=%d rt=%d rs=%d ring=%dx%d rows/CTA=%d smem=%zu\n",
+                (long long)d, (long long)n, G, clu ? kCS : 0, wpg, cb, var->rrmax, (int)var->tm, rr, rt, rs,
+                geo.st_stages, geo.st_rows, rows_max, smem);
     ctx->last_solve_geom[0] = G;
     ctx->last_solve_geom[1] = clu ? kCS : 1;
     ctx->last_solve_geom[2] = rs;

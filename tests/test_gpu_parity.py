@@ -327,6 +327,27 @@ def test_identity_map_solve_is_mwrk(csk):
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
 
 
+@pytest.mark.parametrize("d,n,num_ctas,smem_rows,tmem,ring", [
+    (6000, 150, 8, 0, None, True), (6000, 150, 8, 0, None, False), (5000, 100, 6, -1, None, True),
+    (4000, 50, 3, 0, None, True), (3000, 2, 2, 0, None, True), (3000, 64, 1, 0, None, True),
+    (2500, 500, 4, 0, None, True), (2500, 500, 4, 3, False, True), (1200, 2000, 6, 0, None, True),
+    (900, 2048, 5, 0, None, True), (3001, 130, 5, 0, None, True), (4000, 151, 5, 0, None, True)])
+def test_solve_stream_ring(csk, d, n, num_ctas, smem_rows, tmem, ring):
+    """Rows past the on-chip tiers through the TMA stream ring (ST variants, loop.cu): stages of
+    up to 4 whole rows, several row groups per CTA, ragged last chunks, odd n (plain-load path),
+    and the ring disabled (stream_ring=False) -- the same i_k sequence and x_k as the oracle."""
+    p = make_dense(d, n, "lognormal_rows", d + n, "cuda")
+    At, bt = p.A, p.b
+    nsq = csk.csk_row_norms(At)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, num_ctas=num_ctas, smem_rows=smem_rows, tmem=tmem,
+                      stream_ring=ring, trace=200, trace_x=True, max_iters=200 if n > 1000 else 50000)
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), trace=200,
+                     max_iters=200 if n > 1000 else 50000)
+    if n <= 1000:
+        _free_running(g, o)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 200)
+
+
 @pytest.mark.parametrize("smem_rows,tmem", [(0, None), (-1, False)])
 def test_mwrk_unsketched_parity(csk, smem_rows, tmem):
     """MWRK on the unsketched system (Remark 1) = the same loop
