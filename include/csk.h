@@ -202,6 +202,12 @@ CSK_API csk_status_t csk_last_kernel_ms(csk_ctx_t ctx, int32_t which, float *ms)
 CSK_API csk_status_t csk_last_solve_geometry(csk_ctx_t ctx, int32_t *num_ctas, int32_t *cluster_size,
                                              int32_t *smem_rows);
 
+/* Row tiers of the last csk_solve* on this ctx, per row group of a CTA (loop.cu): out[0] CTAs,
+ * out[1] CTAs per cluster, out[2] register rows, out[3] TMEM rows, out[4] shared-memory rows,
+ * out[5] warps per group, out[6] stream-ring stages, out[7] rows per stage (0: no ring; rows
+ * past out[2] + out[3] + out[4] are re-read from L2/HBM every iteration).  out: 8 int32 (host). */
+CSK_API csk_status_t csk_last_solve_tiers(csk_ctx_t ctx, int32_t *out);
+
 /* ---- Whole Algorithm 1 (INPUT A, b, d, x0 -> OUTPUT x) ---------------- */
 /* Plan + sketch + norms + loop on device buffers (workspace for A~, b~, nsq owned
  * by ctx).  Blocks; fills *report. */

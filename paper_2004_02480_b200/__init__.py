@@ -89,6 +89,7 @@ def _load():
         "csk_solve_wait": ([P, ctypes.POINTER(Report)], i32),
         "csk_ctx_set_timing": ([P, i32], i32),
         "csk_last_kernel_ms": ([P, i32, ctypes.POINTER(ctypes.c_float)], i32),
+        "csk_last_solve_tiers": ([P, P], i32),
         "csk_last_solve_geometry": ([P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_int32)], i32),
         "csk_run": ([P, P, i64, P, i64, i64, i64, u64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
@@ -364,6 +365,16 @@ def csk_last_solve_geometry(ctx: Context | None = None) -> dict:
     g, c, r = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     ctx.check(lib.csk_last_solve_geometry(ctx.handle, ctypes.byref(g), ctypes.byref(c), ctypes.byref(r)))
     return {"num_ctas": g.value, "cluster_size": c.value, "smem_rows": r.value}
+
+
+def csk_last_solve_tiers(ctx: Context | None = None) -> dict:
+    """Row tiers per row group of the last solve on ``ctx`` (csk_last_solve_tiers, loop.cu)."""
+    ctx = ctx or default_context()
+    out = (ctypes.c_int32 * 8)()
+    ctx.check(lib.csk_last_solve_tiers(ctx.handle, ctypes.cast(out, ctypes.c_void_p)))
+    keys = ["num_ctas", "cluster_size", "reg_rows", "tmem_rows", "smem_rows", "group_warps", "ring_stages",
+            "ring_rows"]
+    return dict(zip(keys, list(out)))
 
 
 def csk_solve_wait(ctx: Context | None = None) -> Report:

@@ -311,6 +311,12 @@ csk_status_t csk_last_solve_geometry(csk_ctx_t ctx, int32_t *num_ctas, int32_t *
     return CSK_OK;
 }
 
+csk_status_t csk_last_solve_tiers(csk_ctx_t ctx, int32_t *out) {
+    if (!ctx || !out) return CSK_E_ARG;
+    for (int i = 0; i < 8; ++i) out[i] = ctx->last_solve_tiers[i];
+    return CSK_OK;
+}
+
 csk_status_t csk_run(csk_ctx_t ctx, const double *A, int64_t lda, const double *b, int64_t m,
                      int64_t n, int64_t d, uint64_t seed, double *x, const double *x_star,
                      double tol, int64_t max_iters, csk_report_t *report, void *stream) {

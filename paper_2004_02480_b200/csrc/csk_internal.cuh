@@ -42,6 +42,7 @@ struct csk_ctx_s {
     bool pending = false;
     bool pending_resmode = false;
     int last_solve_geom[5] = {0, 0, 0, 0, 0};  // CTAs, cluster size, smem rows, register rows, warps/group
+    int last_solve_tiers[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // csk_last_solve_tiers
     // host-side memo of driver queries that would otherwise sit between short kernels
     std::set<const void *> smem_raised;                              // kernels set to max dyn smem
     std::map<std::tuple<const void *, int, size_t>, int> occ_cache;  // (fn, cluster, smem) -> n

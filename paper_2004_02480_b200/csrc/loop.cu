@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const int b = p.key_bits;
     const int RM = p.rows_max;
     // ---- ST: the rows past the on-chip tiers stream through a per-group ring of shared-memory
-    //      stages filled by TMA bulk copies (whole rows, contiguous in A~).  Chunk g (of SC per
+    //      stages filled by TMA bulk copies (SR whole rows, contiguous in A~).  Chunk g (of SC per
     //      iteration, g counted over the whole loop) holds rows s0 + (g mod SC) SR ... and lives in
     //      stage g mod SS; the copies of the next iteration's first chunks are issued as soon as
     //      their stages are drained, so they load during the exchange. ----
@@ -744,8 +744,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             }
         }
         if constexpr (ST) {
-            // ---- S6 GEMV: streamed rows from the TMA ring, SR (<= 4) rows per stage, transposed
-            //      tree (row j of a stage ends in lanes [8j, 8j + 8)) ----
+            // ---- S6 GEMV: streamed rows from the TMA ring, SR rows per stage (a multiple of 4) in
+            //      passes of 4, transposed tree (row j of a pass ends in lanes [8j, 8j + 8)) ----
             for (int c = 0; c < SC; ++c) {
                 const uint32_t g = static_cast<uint32_t>(k) * static_cast<uint32_t>(SC) + static_cast<uint32_t>(c);
                 const int st = static_cast<int>(g % static_cast<uint32_t>(SS));
@@ -753,23 +753,33 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 const int nr = min(SR, ng - s0 - c * SR);
                 mbar_wait(rbar + 2 * st, par);
                 const double *rp = ring + st * st_stride;
-                double u[4];
+                auto pass = [&](int p0, double (&u)[4]) {  // 4 rows of the stage against x
 #pragma unroll
-                for (int j = 0; j < 4; ++j) u[j] = 0.0;
+                    for (int jj = 0; jj < 4; ++jj) u[jj] = 0.0;
 #pragma unroll
-                for (int q = 0; q < CB; ++q) {
-                    const int col = tg + TG * q;
+                    for (int q = 0; q < CB; ++q) {
+                        const int col = tg + TG * q;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const double v = (j < nr && col < n) ? rp[j * n + col] : 0.0;
-                        u[j] = __fma_rn(v, x[q], u[j]);
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const double v = (p0 + jj < nr && col < n) ? rp[(p0 + jj) * n + col] : 0.0;
+                            u[jj] = __fma_rn(v, x[q], u[jj]);
+                        }
                     }
+                };
+                const int j = lane >> 3;
+                int p0 = 0;
+                for (; p0 + 4 < nr; p0 += 4) {  // all passes but the last
+                    double u[4];
+                    pass(p0, u);
+                    const double sj = treduce<4>(u, lane);
+                    if ((lane & 7) == 0) dotp[wg * RM + lr0 + s0 + c * SR + p0 + j] = sj;
                 }
+                double u[4];
+                pass(p0, u);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(rbar + 2 * st + 1);  // this warp is done with the stage
                 const double sj = treduce<4>(u, lane);
-                const int j = lane >> 3;
-                if ((lane & 7) == 0 && j < nr) dotp[wg * RM + lr0 + s0 + c * SR + j] = sj;
+                if ((lane & 7) == 0 && p0 + j < nr) dotp[wg * RM + lr0 + s0 + c * SR + p0 + j] = sj;
                 if (producer) {  // refill the stage with chunk g + SS once every warp has read it
                     mbar_wait(rbar + 2 * st + 1, par);
                     st_issue(g + static_cast<uint32_t>(SS));
@@ -1334,13 +1344,17 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
             const LoopVariant *sv = nullptr;
             for (const auto &v : kVariantsSt)
                 if (v.cb == cb && v.tm == (tmk == 1)) sv = &v;
+            // rows per stage: a multiple of 4 (the GEMV passes), >= ~8 KB per stage for short rows
             int R = 4;
-            while (R > 1 && static_cast<int64_t>(R) * n * 8 > 65536) R >>= 1;
-            const size_t sb = st_stage_bytes(n, R);
+            while (R < 64 && static_cast<int64_t>(R + 4) * n * 8 <= 8192) R += 4;
             const size_t fixed = loop_smem(g.rows_max, wpg, cb, n, 0, 0, 0).total + static_cast<size_t>(rg) * 8 * 16;
             const size_t avail = static_cast<size_t>(ctx->max_smem_optin) > fixed ? ctx->max_smem_optin - fixed : 0;
             const size_t budget = avail < kRingMaxBytes ? avail : kRingMaxBytes;
-            const int S = static_cast<int>(std::min<size_t>(8, budget / (static_cast<size_t>(rg) * sb)));
+            auto stages = [&](int r) {
+                return static_cast<int>(std::min<size_t>(8, budget / (static_cast<size_t>(rg) * st_stage_bytes(n, r))));
+            };
+            while (R > 4 && stages(R) < 2) R -= 4;  // the largest stage that is still double-buffered
+            const int S = stages(R);
             if (sv && tmk != 2 && S >= 2) {
                 g.var = sv;
                 if (g.rr > sv->rrmax) g.rr = sv->rrmax;
@@ -1502,6 +1516,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     ctx->last_solve_geom[2] = rs;
     ctx->last_solve_geom[3] = rr;
     ctx->last_solve_geom[4] = wpg;
+    {
+        const int t[8] = {G, clu ? kCS : 1, rr, rt, rs, wpg, geo.st_stages, geo.st_rows};
+        for (int i = 0; i < 8; ++i) ctx->last_solve_tiers[i] = t[i];
+    }
     CSK_CHECK(ensure_host_report(ctx));
     CSK_CUDA(ctx, cudaMemcpyAsync(ctx->report_host, ctx->report.ptr, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
     ctx->pending_stream = stream;

@@ -34,7 +34,7 @@ At, bt, nsq = csk.csk_sketch_csr(p.row_ptr, p.col, p.val, p.b, p.n, cfg.d, seed=
 del p.row_ptr, p.col, p.val
 timed(At, bt, nsq, p.x_star, "C5 CSK loop", 8 * cfg.d * cfg.n)
 del At, bt, nsq
-for (m, n) in [(700000, 100), (700000, 150)]:
+for (m, n) in [(700000, 50), (700000, 100), (700000, 150)]:
     g = torch.Generator(device="cuda").manual_seed(5)
     xs = torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
     A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
