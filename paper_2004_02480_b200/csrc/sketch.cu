@@ -16,6 +16,8 @@
 //     fp64 register accumulators in ring (= row) order; at a bucket boundary they
 //     store the row of A~ (coalesced) and reduce its squared norm (S4, fused);
 //   * a b-warp folds b~ for the same buckets, one bucket per lane, row order.
+// Short rows (n <= 256, the paper's Table-1 shapes): warp per bucket, rows loaded straight
+//   from HBM with R rows in flight per warp (k_sketch_dense_wpb).
 // CSR kernel (config C5): warp per bucket, dense shared-memory accumulator row.
 #include "csk_internal.cuh"
 
@@ -435,6 +437,123 @@ __global__ void k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t 
     }
 }
 
+// Short rows (n <= 256): one warp per bucket.  The row-per-CTA ring above moves each gathered
+// row with its own bulk copy, and for rows of a few hundred bytes the copy issue rate, not HBM,
+// bounds it (one consumer warp per CTA at n <= 64).  Here every warp owns whole buckets: lane l
+// holds column pairs l + 32 v (v < V), the bucket's rows are folded in ascending order (the same
+// adds as the oracle), R rows' loads in flight per warp, b~ folded alongside by every lane.  The
+// fused norm keeps the standalone k_row_norms order (for n <= 256 its team is tc = 32 V' threads,
+// thread t = 32 v + l holding pair t): a partial per v, butterfly, then v ascending.
+template <int V, bool VEC>
+__global__ void __launch_bounds__(256, 2)
+k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m, int64_t n, int64_t d,
+                   const int32_t *__restrict__ perm, const int32_t *__restrict__ offsets, double *__restrict__ At,
+                   double *__restrict__ bt, double *__restrict__ nsq, int tcw) {
+    constexpr int R = V == 1 ? 16 : V == 2 ? 8 : 4;  // rows in flight per warp
+    const int lane = threadIdx.x & 31;
+    const int W = static_cast<int>((static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
+    const int w = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    // warp w: the buckets whose first row lies in [w m / W, (w + 1) m / W) of the sorted order
+    // (contiguous, balanced by rows); their rows are one contiguous range of perm, streamed in
+    // batches of R rows that may span bucket boundaries
+    int64_t j, je;
+    cta_buckets(offsets, m, d, w, W, j, je);
+    if (j >= je) return;
+    const int64_t T1 = offsets[je];
+    int64_t t = offsets[j];
+    // bucket ends in a lane-distributed window: lane l holds offsets[wb + 1 + l]
+    int64_t wb = j;
+    int32_t owin = (wb + 1 + lane <= je) ? __ldg(offsets + wb + 1 + lane) : static_cast<int32_t>(T1);
+    auto end_of = [&](int64_t jj) -> int64_t {  // offsets[jj + 1] (warp-uniform jj >= wb)
+        if (jj - wb >= 32) {
+            wb = jj;
+            owin = (wb + 1 + lane <= je) ? __ldg(offsets + wb + 1 + lane) : static_cast<int32_t>(T1);
+        }
+        return __shfl_sync(0xffffffffu, owin, static_cast<int>(jj - wb));
+    };
+    int64_t e = end_of(j);  // end of bucket j in perm order
+    double2 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = make_double2(0.0, 0.0);
+    double bacc = 0.0;
+    // bucket epilogue: the row of A~, b~_j, and the fused norm in the standalone order
+    auto flush = [&]() {
+        double *dst = At + j * n;
+        double tot = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int64_t col = 2 * static_cast<int64_t>(lane + 32 * v);
+            double part = 0.0;
+            if (col + 1 < n) {
+                if (VEC) *reinterpret_cast<double2 *>(dst + col) = acc[v];
+                else { dst[col] = acc[v].x; dst[col + 1] = acc[v].y; }
+                part = __fma_rn(acc[v].x, acc[v].x, part);
+                part = __fma_rn(acc[v].y, acc[v].y, part);
+            } else if (col < n) {
+                dst[col] = acc[v].x;
+                part = __fma_rn(acc[v].x, acc[v].x, part);
+            }
+            if (v < tcw) {
+                part = warp_sum(part);
+                tot = (v == 0) ? part : tot + part;
+            }
+            acc[v] = make_double2(0.0, 0.0);
+        }
+        if (lane == 0) {
+            bt[j] = bacc;
+            if (nsq) nsq[j] = tot;
+        }
+        bacc = 0.0;
+        ++j;
+        e = (j < je) ? end_of(j) : T1;
+    };
+    while (j < je && e == t) flush();  // leading empty buckets
+    int32_t prn = (t + lane < T1) ? __ldg(perm + t + lane) : 0;  // the next batch's perm window
+    for (; t < T1; t += R) {
+        const int cnt = (T1 - t) < R ? static_cast<int>(T1 - t) : R;
+        // lane r holds the batch's r-th perm entry and its b value; the next window is in flight
+        const int32_t prl = prn;
+        prn = (t + R + lane < T1) ? __ldg(perm + t + R + lane) : 0;
+        const double bl = lane < cnt ? __ldg(b + (prl & 0x7fffffff)) : 0.0;
+        int32_t pr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) pr[r] = __shfl_sync(0xffffffffu, prl, r);
+        double2 val[R][V];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double *src = A + static_cast<int64_t>(pr[r] & 0x7fffffff) * lda;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const int64_t col = 2 * static_cast<int64_t>(lane + 32 * v);
+                double2 x2 = make_double2(0.0, 0.0);
+                if (r < cnt && col < n) {
+                    if (VEC && col + 1 < n) {
+                        x2 = __ldg(reinterpret_cast<const double2 *>(src + col));
+                    } else {
+                        x2.x = __ldg(src + col);
+                        if (col + 1 < n) x2.y = __ldg(src + col + 1);
+                    }
+                }
+                val[r][v] = x2;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r < cnt) {  // ascending row order; the sign flip is exact
+                const bool neg = pr[r] < 0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    acc[v].x = acc[v].x + (neg ? -val[r][v].x : val[r][v].x);
+                    acc[v].y = acc[v].y + (neg ? -val[r][v].y : val[r][v].y);
+                }
+                const double bvr = __shfl_sync(0xffffffffu, bl, r);
+                bacc = bacc + (neg ? -bvr : bvr);
+                while (j < je && e == t + r + 1) flush();  // bucket boundary (and empty buckets)
+            }
+        }
+    }
+}
+
 }  // namespace
 
 int norm_team_threads(int64_t n) { return dense_geom(n, true).tc; }
@@ -445,6 +564,28 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
                                  cudaStream_t stream) {
     const bool tma = aligned16(A) && (lda % 2 == 0);
     const DenseGeom g = dense_geom(n, tma);
+    static const bool no_wpb = getenv("CSK_SKETCH_NO_WPB") != nullptr;
+    if (n <= 256 && !no_wpb) {  // short rows: warp per bucket
+        const int tcw = g.tc / 32;  // the standalone norm team (k_row_norms) in warps
+        const int V = static_cast<int>((n + 63) / 64);
+        const int64_t grid = int64_t(ctx->num_sms) * 2;  // persistent, 16 warps per SM
+        time_mark(ctx, 0, false, stream);
+#define CSK_WPB(VV)                                                                                       \
+        if (tma) k_sketch_dense_wpb<VV, true><<<static_cast<int>(grid), 256, 0, stream>>>(                 \
+            A, lda, b, m, n, d, perm, offsets, At, bt, nsq, tcw);                                         \
+        else k_sketch_dense_wpb<VV, false><<<static_cast<int>(grid), 256, 0, stream>>>(                   \
+            A, lda, b, m, n, d, perm, offsets, At, bt, nsq, tcw);
+        switch (V) {
+            case 1: CSK_WPB(1) break;
+            case 2: CSK_WPB(2) break;
+            case 3: CSK_WPB(3) break;
+            default: CSK_WPB(4) break;
+        }
+#undef CSK_WPB
+        time_mark(ctx, 0, true, stream);
+        CSK_CUDA(ctx, cudaGetLastError());
+        return CSK_OK;
+    }
     int grid = ctx->num_sms;
     if (grid > d) grid = static_cast<int>(d);
     const int threads = g.tc + 64;
