@@ -19,3 +19,11 @@ python tools/sketch_time.py C3 > /dev/null 2>&1 && \
 CSK_NO_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sketch_dense -s 2 -c 1 \
     -o gpurun_out/${R}_sketch_C3 python tools/sketch_time.py C3 > gpurun_out/${R}_ncu_sketch_C3.log 2>&1
 ls -la gpurun_out
+# stream-ring loop (C5, capped) and the warp-per-bucket sketch (Table-1 shape)
+python tools/run_c5_once.py 100 > /dev/null 2>&1 && \
+CSK_PROFILE_NONCOOP=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_loop -c 1 \
+    -o gpurun_out/${R}_loop_C5 python tools/run_c5_once.py 100 > gpurun_out/${R}_ncu_loop_C5.log 2>&1
+python tools/csk_breakdown.py 700000x150 > /dev/null 2>&1 && \
+CSK_NO_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sketch_dense_wpb -s 2 -c 1 \
+    -o gpurun_out/${R}_sketch_wpb python tools/csk_breakdown.py 700000x150 > gpurun_out/${R}_ncu_sketch_wpb.log 2>&1
+ls -la gpurun_out
