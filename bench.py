@@ -300,10 +300,14 @@ def run_ours(args, dist, rank, ws):
                             "traffic": _ncu_traffic(f"r01_ncu_sketch_{cfg.name}.txt"),
                             "with_plan": {"ms": round(sk_ms, 5), "achieved": round(sketch_gbs, 1),
                                           "frac": round(sketch_gbs / hbm_peak, 4),
-                                          "note": "whole csk_sketch call: hash + CUB radix-sort plan + sketch"}},
+                                          "note": "whole csk_sketch call: plan (S1 hash + S2 stable bucketing) + sketch kernel"}},
         "clocks": clocks,
-        "gpu_launches": 4 * args.steps,
-        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB onesweep radix-sort kernels and one memset)",
+        "gpu_launches": (3 if 8192 < cfg.m <= 200000 and cfg.m <= 256 * cfg.d else 4) * args.steps,
+        "gpu_launches_note": ("per step: k_plan_fused (one cooperative launch: hash, bucket counts, scan, scatter, "
+                              "per-bucket sort), k_sketch_dense, k_loop (+ one memset)"
+                              if 8192 < cfg.m <= 200000 and cfg.m <= 256 * cfg.d else
+                              "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB onesweep radix-sort "
+                              "kernels and one memset)"),
     }
 
     # ---- e2e: the public API with HOST buffers, copies inside the timed region
@@ -592,8 +596,9 @@ def run_sharded(args, dist, rank, ws):
         "sketch_hbm_gbs": round(alg_bytes_sketch(cfg) / (sk * 1e-3) / 1e9, 1),
         "clocks": sampler.summary(t0, t1),
         "gpu_launches": args.steps * 4,
-        "gpu_launches_note": "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB radix-sort kernels, "
-                             "the NCCL reduce-scatter of S9 and the NCCL handle/barrier collectives of S10)",
+        "gpu_launches_note": "per step: the plan (k_plan_fused, or k_hash_keys + CUB radix sort + k_offsets), "
+                             "k_sketch_dense, k_loop (+ the NCCL reduce-scatter of S9 and the NCCL handle/barrier "
+                             "collectives of S10)",
     }
     csk.comm_destroy(ctx)
     return out
