@@ -246,6 +246,7 @@ def run_ours(args, dist, rank, ws):
     smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
     loop_tflops = 2.0 * cfg.d * cfg.n * it / (k_loop_ms * 1e-3) / 1e12
     fp64_peak = 148 * DFMA_PER_CLK_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
+    loop_floor_us = (3230.0 + -(-cfg.d // 148) * cfg.n / 64.0) / sm_max_mhz
     sketch_gbs = alg_bytes_sketch(cfg) / (sk_ms * 1e-3) / 1e9
     out = {
         "metric": METRIC,
@@ -291,6 +292,15 @@ def run_ours(args, dist, rank, ws):
                           "alg_flops_per_iteration": 2 * cfg.d * cfg.n,
                           "note": "the loop is latency-bound: one grid-wide exchange (atomic max-key + count, "
                                   "~2.3k cycles floor measured) per iteration"},
+        # what actually bounds the loop: one grid-wide exchange per iteration.  Floor = the
+        # microbenchmarked 148-CTA atomic exchange with a 500-double winner-row fetch (3230 cycles,
+        # profiles/r01_microbench_k7b.txt "+row500") + the GEMV at the FP64 FMA rate
+        "roofline_latency": {"kernel": "k_loop", "bound": "latency",
+                             "floor_us_per_iteration": round(loop_floor_us, 3),
+                             "achieved_us_per_iteration": round(k_loop_ms * 1e3 / max(it, 1), 3),
+                             "frac": round(loop_floor_us / (k_loop_ms * 1e3 / max(it, 1)), 4),
+                             "floor_source": "3230 cycles (microbench_xchg atomic_pair +row500, G=148) + "
+                                             "ceil(d/148) n / 64 DFMA cycles, at sm_max_mhz"},
         "roofline_sketch": {"kernel": "k_sketch_dense", "bound": "hbm",
                             "achieved": round(alg_bytes_sketch(cfg) / (k_sketch_ms * 1e-3) / 1e9, 1),
                             "peak": hbm_peak, "unit": "GB/s",
