@@ -444,6 +444,24 @@ __global__ void k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t 
 // adds as the oracle), R rows' loads in flight per warp, b~ folded alongside by every lane.  The
 // fused norm keeps the standalone k_row_norms order (for n <= 256 its team is tc = 32 V' threads,
 // thread t = 32 v + l holding pair t): a partial per v, butterfly, then v ascending.
+// lower_bound(a[0..len), v) by one warp: 32 probes per step (log32 len dependent loads instead of
+// log2 len); every lane returns the same index
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t *a, int64_t len, int64_t v, int lane) {
+    int64_t lo = 0, hi = len;
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t pk = lo + lane * step;
+        const bool below = pk < hi && static_cast<int64_t>(__ldg(a + pk)) < v;
+        const int c = __popc(__ballot_sync(0xffffffffu, below));
+        if (c == 0) return lo;
+        const int64_t nhi = lo + c * step < hi ? lo + c * step : hi;
+        lo = lo + (c - 1) * step + 1;
+        hi = nhi;
+    }
+    const bool below = lo + lane < hi && static_cast<int64_t>(__ldg(a + lo + lane)) < v;
+    return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
 template <int V, bool VEC>
 __global__ void __launch_bounds__(256, 2)
 k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m, int64_t n, int64_t d,
@@ -456,8 +474,8 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
     // warp w: the buckets whose first row lies in [w m / W, (w + 1) m / W) of the sorted order
     // (contiguous, balanced by rows); their rows are one contiguous range of perm, streamed in
     // batches of R rows that may span bucket boundaries
-    int64_t j, je;
-    cta_buckets(offsets, m, d, w, W, j, je);
+    int64_t j = warp_lower_bound(offsets, d, m * w / W, lane);
+    int64_t je = (w == W - 1) ? d : warp_lower_bound(offsets, d, m * (w + 1) / W, lane);
     if (j >= je) return;
     const int64_t T1 = offsets[je];
     int64_t t = offsets[j];
