@@ -49,7 +49,7 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 20 ms while running."""
+    """nvidia-smi (NVML) clocks/throttle reasons sampled every 2 ms while running."""
 
     def __init__(self, device_index: int):
         self.dev = device_index
@@ -81,7 +81,7 @@ class ClockSampler:
                 self.samples.append(self._sample())
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)
 
     def start(self):
         if self._nvml:
@@ -617,7 +617,7 @@ def run_sharded(args, dist, rank, ws):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
