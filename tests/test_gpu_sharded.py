@@ -48,6 +48,19 @@ def test_virtual_ranks_match_oracle(csk, P):
     assert abs(g.iterations - rep.iterations) <= max(1, 0.05 * o.iterations)
 
 
+@pytest.mark.parametrize("P", [2, 4])
+def test_virtual_ranks_streamed_rows(csk, P):
+    """Rows past the on-chip tiers (92 MB of A > what 148 SMs hold) stream through the TMA ring
+    inside the P-rank decomposition too (MWRK on a tall system, Remark 1)."""
+    p = make_dense(90000, 128, "lognormal_rows", 31, "cuda")
+    nsq = csk.csk_row_norms(p.A)
+    x, copies, rep = csk.csk_solve_virtual_ranks(p.A, p.b, nsq, P, x_star=p.x_star, tol=1e-6, max_iters=5000)
+    assert all(torch.equal(copies[q], copies[0]) for q in range(P))
+    o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), tol=1e-6, max_iters=5000)
+    assert rep.termination == csk.CONVERGED and rep.final_res <= 1e-6
+    assert abs(rep.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
+
+
 def test_virtual_ranks_residual_mode_and_cap(csk):
     p = make_dense(6000, 40, "gauss", 12, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, 400, seed=2)
