@@ -378,12 +378,16 @@ k_row_norms(const double *__restrict__ At, int64_t d, int64_t n, double *__restr
     }
 }
 
-// CSR sketch: one warp per bucket; a dense fp64 accumulator row of n in shared
-// memory per warp; rows of the bucket in ascending order, each row's stored
-// (col, val) pairs spread over lanes (columns are distinct within a row, so
-// per-column adds keep row order).  Row norms fused as in the dense epilogue
-// but with the warp-only team (documented in DESIGN.md; checked to tolerance).
-__global__ void k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+// CSR sketch: one warp per bucket; a dense fp64 accumulator row of n in shared memory per
+// warp; the bucket's rows are folded in ascending order.  Rows come in batches of 32: lane r
+// holds the r-th row's perm entry, row_ptr pair and b value (three parallel loads), then the
+// first 32 stored (col, val) pairs of every row of the batch are loaded into registers (lane l
+// holding pair l of each row) before any add, so a batch costs three dependent memory latencies
+// instead of three per row.  Within a row the columns are distinct, so its pairs are added by
+// the lanes in parallel; rows are separated by __syncwarp (row order per column).  Pairs past the
+// first 32 of a row are read in the add loop.  Row norms fused as in the dense epilogue but with
+// the warp-only team (documented in DESIGN.md; checked to tolerance).
+__global__ void __launch_bounds__(384, 1) k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                              const double *__restrict__ val, const double *__restrict__ b,
                              int64_t n, int64_t d, const int32_t *__restrict__ perm,
                              const int32_t *__restrict__ offsets, double *__restrict__ At,
@@ -399,23 +403,41 @@ __global__ void k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t 
         __syncwarp();
         const int64_t a = offsets[j], e = offsets[j + 1];
         double bacc = 0.0;
-        for (int64_t t = a; t < e; ++t) {
-            const int32_t pr = __ldg(perm + t);
-            const int64_t row = pr & 0x7fffffff;
-            const bool neg = pr < 0;
-            const int64_t s0 = __ldg(row_ptr + row), s1 = __ldg(row_ptr + row + 1);
-            for (int64_t q = s0 + lane; q < s1; q += 32) {
-                const int32_t cc = __ldg(col + q);
-                double v = __ldg(val + q);
-                if (neg) v = -v;
-                acc[cc] = acc[cc] + v;
+        for (int64_t t = a; t < e; t += 32) {
+            const int cnt = (e - t) < 32 ? static_cast<int>(e - t) : 32;
+            const int32_t prl = lane < cnt ? __ldg(perm + t + lane) : 0;
+            const int64_t rowl = prl & 0x7fffffff;
+            const int64_t rsl = lane < cnt ? __ldg(row_ptr + rowl) : 0;
+            const int64_t rel = lane < cnt ? __ldg(row_ptr + rowl + 1) : 0;
+            const double bl = lane < cnt ? __ldg(b + rowl) : 0.0;
+            int32_t cc[32];
+            double vv[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                const int64_t s0 = __shfl_sync(0xffffffffu, rsl, r), s1 = __shfl_sync(0xffffffffu, rel, r);
+                const int64_t q = s0 + lane;
+                const bool ok = r < cnt && q < s1;
+                cc[r] = ok ? __ldg(col + q) : 0;
+                vv[r] = ok ? __ldg(val + q) : 0.0;
             }
-            __syncwarp();
-            if (lane == 0) {
-                const double bv = __ldg(b + row);
-                bacc = bacc + (neg ? -bv : bv);
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                if (r < cnt) {
+                    const int64_t s0 = __shfl_sync(0xffffffffu, rsl, r), s1 = __shfl_sync(0xffffffffu, rel, r);
+                    const bool neg = __shfl_sync(0xffffffffu, prl, r) < 0;
+                    if (s0 + lane < s1) acc[cc[r]] = acc[cc[r]] + (neg ? -vv[r] : vv[r]);
+                    for (int64_t q = s0 + 32 + lane; q < s1; q += 32) {  // rows with > 32 stored pairs
+                        const int32_t c = __ldg(col + q);
+                        const double v = __ldg(val + q);
+                        acc[c] = acc[c] + (neg ? -v : v);
+                    }
+                    __syncwarp();
+                    const double bv = __shfl_sync(0xffffffffu, bl, r);
+                    bacc = bacc + (neg ? -bv : bv);
+                }
             }
         }
+        __syncwarp();
         double part = 0.0;
         double *dst = At + j * n;
         for (int64_t k = 2 * lane; k < n; k += 64) {
@@ -659,7 +681,7 @@ csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int3
     (void)m;
     const int64_t stride = (n + 1) & ~int64_t(1);
     int wpb = static_cast<int>((ctx->max_smem_optin - 1024) / (stride * 8));
-    if (wpb > 16) wpb = 16;
+    if (wpb > 12) wpb = 12;  // __launch_bounds__(384): the batch's (col, val) registers
     if (wpb < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
     const size_t smem = static_cast<size_t>(wpb) * stride * 8;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_csr)));

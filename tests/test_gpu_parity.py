@@ -429,6 +429,26 @@ def test_sketch_csr_bitexact(csk, m, n, d, k):
     assert np.all(np.abs(_np(nsq) - nsq_o) <= 2 * n * U * nsq_o)
 
 
+@pytest.mark.parametrize("m,n,d,maxlen", [(5000, 300, 400, 70), (3000, 1500, 50, 40)])
+def test_sketch_csr_ragged_rows(csk, m, n, d, maxlen):
+    """CSR rows of 0..maxlen stored pairs (empty rows, rows past one 32-pair batch load, unsorted
+    bucket sizes): the batched CSR kernel folds every row in ascending order."""
+    g = np.random.default_rng(m + n)
+    lens = g.integers(0, maxlen + 1, size=m)
+    lens[::97] = 0
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(g.choice(n, size=int(k), replace=False)) for k in lens]).astype(np.int32)
+    val = g.standard_normal(int(rp[-1]))
+    b = g.standard_normal(m)
+    At, bt, nsq = csk.csk_sketch_csr(torch.from_numpy(rp).cuda(), torch.from_numpy(col).cuda(),
+                                     torch.from_numpy(val).cuda(), torch.from_numpy(b).cuda(), n, d, seed=13)
+    At_o, bt_o = oracle.sketch_csr(rp, col, val, b, n, d, seed=13)
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+    nsq_o = oracle.row_norms(At_o)
+    assert np.all(np.abs(_np(nsq) - nsq_o) <= 2 * n * U * nsq_o + 1e-300)
+
+
 def test_C5_full_size_sampled(csk):
     """4e6 x 2000 CSR (4e7 nnz): sampled buckets against the oracle's fold of exactly those
     rows; the first iterations in lockstep against the oracle's residual."""
