@@ -403,13 +403,23 @@ __global__ void __launch_bounds__(384, 1) k_sketch_csr(const int64_t *__restrict
         __syncwarp();
         const int64_t a = offsets[j], e = offsets[j + 1];
         double bacc = 0.0;
+        // the batch's perm entries, row_ptr pairs and b values, one batch ahead
+        int32_t prn = (a + lane < e) ? __ldg(perm + a + lane) : 0;
+        int64_t rsn = (a + lane < e) ? __ldg(row_ptr + (prn & 0x7fffffff)) : 0;
+        int64_t ren = (a + lane < e) ? __ldg(row_ptr + (prn & 0x7fffffff) + 1) : 0;
+        double bn = (a + lane < e) ? __ldg(b + (prn & 0x7fffffff)) : 0.0;
         for (int64_t t = a; t < e; t += 32) {
             const int cnt = (e - t) < 32 ? static_cast<int>(e - t) : 32;
-            const int32_t prl = lane < cnt ? __ldg(perm + t + lane) : 0;
-            const int64_t rowl = prl & 0x7fffffff;
-            const int64_t rsl = lane < cnt ? __ldg(row_ptr + rowl) : 0;
-            const int64_t rel = lane < cnt ? __ldg(row_ptr + rowl + 1) : 0;
-            const double bl = lane < cnt ? __ldg(b + rowl) : 0.0;
+            const int32_t prl = prn;
+            const int64_t rsl = rsn, rel = ren;
+            const double bl = bn;
+            if (t + 32 < e) {
+                const bool ok = t + 32 + lane < e;
+                prn = ok ? __ldg(perm + t + 32 + lane) : 0;
+                rsn = ok ? __ldg(row_ptr + (prn & 0x7fffffff)) : 0;
+                ren = ok ? __ldg(row_ptr + (prn & 0x7fffffff) + 1) : 0;
+                bn = ok ? __ldg(b + (prn & 0x7fffffff)) : 0.0;
+            }
             int32_t cc[32];
             double vv[32];
 #pragma unroll
