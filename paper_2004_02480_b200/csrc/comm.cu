@@ -465,7 +465,8 @@ struct IpcRec {
     cudaIpcMemHandle_t a;  // allocation holding this rank's A~ rows
     long long a_off;       // offset of A~_local inside it
     cudaIpcMemHandle_t x;  // this rank's exchange buffer (ctx->slots)
-    long long pad;
+    long long x_off;       // offset of the exchange buffer inside its allocation
+    long long ok;          // 1: both handles exported (0: e.g. a VMM allocation -- every rank falls back)
 };
 
 static csk_status_t ipc_handle(csk_ctx_t ctx, const void *ptr, cudaIpcMemHandle_t *h, long long *off) {
@@ -555,11 +556,15 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
     CSK_CHECK(ensure(ctx, ctx->slots, ex));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
     const size_t xch_bytes = ex - static_cast<size_t>(2) * rs.Gr * 8 * 8;
-    // swap IPC handles (A~ rows, exchange buffer) through NCCL
+    // swap IPC handles (A~ rows, exchange buffer) through NCCL.  An export failure is not an
+    // error here: every rank sees every rank's `ok` after the all-gather and all of them take the
+    // host-driven NCCL loop together
     IpcRec mine{};
-    CSK_CHECK(ipc_handle(ctx, A_tilde_local, &mine.a, &mine.a_off));
-    long long xoff = 0;
-    CSK_CHECK(ipc_handle(ctx, ctx->slots.ptr, &mine.x, &xoff));
+    mine.ok = (ipc_handle(ctx, A_tilde_local, &mine.a, &mine.a_off) == CSK_OK &&
+               ipc_handle(ctx, ctx->slots.ptr, &mine.x, &mine.x_off) == CSK_OK)
+                  ? 1
+                  : 0;
+    if (!mine.ok) cudaGetLastError();  // clear a sticky-free runtime error of the failed export
     std::vector<IpcRec> all(P);
     void *dbuf = nullptr;
     CSK_CUDA(ctx, cudaMallocAsync(&dbuf, sizeof(IpcRec) * (P + 1), s));
@@ -569,6 +574,12 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
                                 cm->nccl, s));
     CSK_CUDA(ctx, cudaMemcpyAsync(all.data(), dbuf, sizeof(IpcRec) * P, cudaMemcpyDeviceToHost, s));
     CSK_CUDA(ctx, cudaStreamSynchronize(s));
+    for (int r = 0; r < P; ++r)
+        if (!all[r].ok) {
+            CSK_CUDA(ctx, cudaFreeAsync(dbuf, s));
+            return CSK_E_UNSUPPORTED;  // every rank returns here: the host-driven loop
+        }
+    int open_bad = 0;  // a failed peer mapping is agreed on through the probe's all-reduce below
     for (int r = 0; r < P; ++r) {
         unsigned char *xb = nullptr;
         if (r == me) {
@@ -576,10 +587,15 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
             xb = static_cast<unsigned char *>(ctx->slots.ptr);
         } else {
             void *a = nullptr, *xp = nullptr;
-            CSK_CHECK(ipc_open(ctx, all[r].a, &a));
-            CSK_CHECK(ipc_open(ctx, all[r].x, &xp));
-            rs.At_r[r] = reinterpret_cast<const double *>(static_cast<unsigned char *>(a) + all[r].a_off);
-            xb = static_cast<unsigned char *>(xp) + xoff;  // same ctx workspace layout on every rank
+            if (ipc_open(ctx, all[r].a, &a) != CSK_OK || ipc_open(ctx, all[r].x, &xp) != CSK_OK) {
+                cudaGetLastError();
+                open_bad = 1;
+                rs.At_r[r] = A_tilde_local;  // placeholders, never dereferenced
+                xb = static_cast<unsigned char *>(ctx->slots.ptr);
+            } else {
+                rs.At_r[r] = reinterpret_cast<const double *>(static_cast<unsigned char *>(a) + all[r].a_off);
+                xb = static_cast<unsigned char *>(xp) + all[r].x_off;
+            }
         }
         rs.slots_r[r] = reinterpret_cast<unsigned long long *>(xb + xch_bytes);
         if (r == 0) rs.xch = reinterpret_cast<unsigned long long *>(xb);
@@ -603,9 +619,9 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
         CSK_CUDA(ctx, cudaMallocAsync(&pb, sizeof(words) + 16, s));
         CSK_CUDA(ctx, cudaMemcpyAsync(pb, words, sizeof(words), cudaMemcpyHostToDevice, s));
         int *bad = reinterpret_cast<int *>(static_cast<unsigned char *>(pb) + sizeof(words));
-        CSK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), s));
+        CSK_CUDA(ctx, cudaMemcpyAsync(bad, &open_bad, sizeof(int), cudaMemcpyHostToDevice, s));
         CSK_NCCL(ctx, ncclAllReduce(bad, bad, 1, ncclInt32, ncclMax, cm->nccl, s));  // barrier: all words written
-        k_peer_probe<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned long long *const *>(pb), P, bad);
+        if (!open_bad) k_peer_probe<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned long long *const *>(pb), P, bad);
         CSK_NCCL(ctx, ncclAllReduce(bad, bad, 1, ncclInt32, ncclMax, cm->nccl, s));
         int bad_h = 0;
         CSK_CUDA(ctx, cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
