@@ -1092,9 +1092,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         LP(4)
         __syncthreads();  // B2
         LP(5)
+        // every control word at once (independent loads, in flight during the row wait)
         int stop = static_cast<int>(ctl[0]);
+        const int64_t conv = RESMODE ? 0 : ctl[4];
+        const int64_t res_bits = RESMODE ? ctl[3] : ctl[5];
+        const int64_t wrow_b = ctl[1];
+        const double *wrow_ptr = reinterpret_cast<const double *>(slotbuf[4]);
         prow = -1;
-        if (!RESMODE && ctl[4] == CSK_CONVERGED) {  // RES_k <= tol: no update
+        if (!RESMODE && conv == CSK_CONVERGED) {  // RES_k <= tol: no update
             if (stop == -1) mbar_wait(mbar, mphase);  // drain the copies of the exchange
             stop = CSK_CONVERGED;
         }
@@ -1114,17 +1119,16 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             if (sc == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
         }
         LP(6)
-        if (!RESMODE) res = __longlong_as_double(ctl[5]);
-        else res = __longlong_as_double(ctl[3]);
+        res = __longlong_as_double(res_bits);
         if (stop != -1) {
             term = stop;
             break;
         }
-        const int64_t wrow = ctl[1];
+        const int64_t wrow = wrow_b;
         if (lead && tid == 0 && p.idx_trace && k < p.trace_cap) p.idx_trace[k] = wrow;
         last = wrow;
         prow = wrow;
-        prow_ptr = reinterpret_cast<const double *>(slotbuf[4]);
+        prow_ptr = wrow_ptr;
     }
 #undef LP
     if constexpr (ST) {  // drain the copies already issued for the iteration that never ran
