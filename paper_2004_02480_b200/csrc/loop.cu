@@ -610,10 +610,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     // finalize lanes keep their rows' b~ and 1/nsq in registers (groups of <= 32 rows; with the
     // TMEM tier <= 64: rows lane and lane + 32)
     const bool fast_fin = ng <= (TM != 0 ? 64 : 32);
-    const double fin_b = (fast_fin && lane < ng) ? btl[lr0 + lane] : 0.0;
-    const double fin_i = (fast_fin && lane < ng) ? invl[lr0 + lane] : 0.0;
-    const double fin_b2 = (TM != 0 && fast_fin && lane + 32 < ng) ? btl[lr0 + 32 + lane] : 0.0;
-    const double fin_i2 = (TM != 0 && fast_fin && lane + 32 < ng) ? invl[lr0 + 32 + lane] : 0.0;
+    // (the narrow-TMEM variants run at the register limit: there the finalize re-reads them from
+    // shared memory, measured faster at C2; the others keep them in registers)
+    constexpr bool kFinReg = TM != 2;
+    const double fin_b = (kFinReg && fast_fin && lane < ng) ? btl[lr0 + lane] : 0.0;
+    const double fin_i = (kFinReg && fast_fin && lane < ng) ? invl[lr0 + lane] : 0.0;
+    const double fin_b2 = (TM == 1 && fast_fin && lane + 32 < ng) ? btl[lr0 + 32 + lane] : 0.0;
+    const double fin_i2 = (TM == 1 && fast_fin && lane + 32 < ng) ? invl[lr0 + 32 + lane] : 0.0;
     const bool all_reg = rr == ng;  // every row of the group in registers: own partial by shuffle
 
     int64_t k = 0, last = -1;
@@ -822,22 +825,24 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     const int l = lr0 + lane;
                     double dot = all_reg ? own : dotp[l];
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
-                    const double ri = fin_b - dot;
-                    const double sc = fin_i > 0.0 ? (ri * ri) * fin_i : -1.0;
+                    const double fb = kFinReg ? fin_b : btl[l], fi = kFinReg ? fin_i : invl[l];
+                    const double ri = fb - dot;
+                    const double sc = fi > 0.0 ? (ri * ri) * fi : -1.0;
                     if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
                     bk = row_key(sc, r0 + l, b);
-                    bl = ri * fin_i;
+                    bl = ri * fi;
                     bs = sc;
                 }
                 if (TM != 0 && lane + 32 < ng) {  // second row of the lane (groups of 33..64 rows)
                     const int l = lr0 + 32 + lane;
                     double dot = dotp[l];
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
-                    const double ri = fin_b2 - dot;
-                    const double sc = fin_i2 > 0.0 ? (ri * ri) * fin_i2 : -1.0;
+                    const double fb2 = TM == 1 ? fin_b2 : btl[l], fi2 = TM == 1 ? fin_i2 : invl[l];
+                    const double ri = fb2 - dot;
+                    const double sc = fi2 > 0.0 ? (ri * ri) * fi2 : -1.0;
                     if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
                     const unsigned long long kk = row_key(sc, r0 + l, b);
-                    if (kk > bk) { bk = kk; bl = ri * fin_i2; bs = sc; }
+                    if (kk > bk) { bk = kk; bl = ri * fi2; bs = sc; }
                 }
             } else for (int l0 = 0; l0 < ng; l0 += 32) {
                 const int l = lr0 + l0 + lane;
