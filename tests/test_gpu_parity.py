@@ -82,6 +82,26 @@ def test_sketch_bitexact_shapes(csk, m, n, d):
     _check_sketch(csk, p.A, p.b, d, seed=3)
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 128, 129, 255, 256, 257])
+def test_sketch_short_row_boundaries(csk, n):
+    """The warp-per-bucket kernel's column blocks (V = ceil(n/64) pairs per lane, odd tails) and
+    its hand-over to the TMA ring kernel at n = 257; m = 20000 takes the one-launch plan."""
+    p = make_dense(20000, n, "lognormal_rows", 500 + n, "cuda")
+    _check_sketch(csk, p.A, p.b, 1000, seed=6)
+
+
+@pytest.mark.parametrize("n,lda", [(50, 51), (64, 67), (200, 203)])
+def test_sketch_short_rows_unaligned(csk, n, lda):
+    """Odd lda (8-byte aligned rows): the warp-per-bucket kernel's scalar-load path."""
+    p = make_dense(7000, n, "gauss", n + lda, "cuda")
+    buf = torch.zeros(7000 * lda, dtype=torch.float64, device="cuda")
+    Ab = buf.view(7000, lda)
+    Ab[:, :n] = p.A
+    At, bt, _ = csk.csk_sketch(Ab[:, :n], p.b, 600, seed=12)
+    At_o, bt_o = oracle.sketch_dense(_np(p.A), _np(p.b), 600, seed=12)
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+
+
 @pytest.mark.parametrize("lda,shift", [(136, 0), (131, 0), (130, 1)])
 def test_sketch_padded_and_unaligned_lda(csk, lda, shift):
     """lda > n (even: TMA path), odd lda and an 8-byte-aligned A (plain-load path)."""
