@@ -41,6 +41,7 @@ namespace csk {
 namespace {
 
 constexpr int kLW = 8;             // warps per CTA
+constexpr int kTmRowsDev = 16;     // rows per thread in the TMEM tier (kTmRows)
 constexpr int kLT = kLW * 32;      // threads per CTA
 constexpr int kXchWords = 16;      // one 128-byte line per {count, max} pair
 constexpr int kSlotWords = 8;      // LL slot: lambda, score, rr as tagged 32-bit halves + pad
@@ -695,8 +696,19 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
         if constexpr (TM != 0) {
             // blocks of 8 / 4 / 2 rows (a block may run one row past rt, reading an unused row
-            // of this thread's TMEM area that is never written back)
-            for (int j0 = 0; j0 < rt;) {
+            // of this thread's TMEM area that is never written back); a full wide tier (16 rows)
+            // folds both blocks into one 16-row tree (one tree depth instead of two)
+            int j0 = 0;
+            if (TM == 1 && rt == kTmRowsDev) {
+                double acc16[16];
+                tmem_block_wide<8, CB>(tbase, x, *reinterpret_cast<double(*)[8]>(&acc16[0]));
+                tmem_block_wide<8, CB>(tbase + 16u * 8, x, *reinterpret_cast<double(*)[8]>(&acc16[8]));
+                const double s = treduce<16>(acc16, lane);
+                const int i = lane >> 1;
+                if ((lane & 1) == 0) dotp[wg * RM + lr0 + rr + i] = s;
+                j0 = rt;
+            }
+            for (; j0 < rt;) {
                 if (rt - j0 > 4) {
                     double acc8[8];
                     if constexpr (TM == 1) tmem_block_wide<8, CB>(tbase + 16u * j0, x, acc8);
@@ -727,8 +739,21 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S6 GEMV: shared-memory rows, blocks of 8, transposed tree ----
         {
             // blocks of 8 (a tail of <= 4 rows: a block of 4), columns outer so the block's rows
-            // form independent fma chains; rows past rs re-read row rs-1 (never written back)
-            for (int i0 = 0; i0 < rs;) {
+            // form independent fma chains; rows past rs re-read row rs-1 (never written back).
+            // 9..12 rows with the TMEM tier: one 16-row tree over a block of 8 and a block of 4
+            int i0 = 0;
+            if (TM == 1 && rs > 8 && rs <= 12) {
+                double acc16[16];
+                smem_block<8, CB>(arows, tg, 0, rs, TG, x, *reinterpret_cast<double(*)[8]>(&acc16[0]));
+                smem_block<4, CB>(arows, tg, 8, rs, TG, x, *reinterpret_cast<double(*)[4]>(&acc16[8]));
+#pragma unroll
+                for (int j = 12; j < 16; ++j) acc16[j] = 0.0;
+                const double s = treduce<16>(acc16, lane);
+                const int i = lane >> 1;
+                if ((lane & 1) == 0 && i < rs) dotp[wg * RM + lr0 + rr + rt + i] = s;
+                i0 = rs;
+            }
+            for (; i0 < rs;) {
                 if (rs - i0 > 4) {
                     double acc8[8];
                     smem_block<8, CB>(arows, tg, i0, rs, TG, x, acc8);
