@@ -59,3 +59,30 @@ def test_table1_iteration_means_on_gpu(csk, m, n, trials):
     # the printed means are over 50 trials; the trial-to-trial spread of IT is a few iterations
     assert abs(np.mean(its) - csk_it) <= 0.03 * csk_it, (np.mean(its), csk_it, its)
     assert abs(np.mean(mws) - mwrk_it) <= 2.5, (np.mean(mws), mwrk_it, mws)
+
+
+@pytest.mark.parametrize("spec", ["C1", "300000x50"])
+def test_theorem2_rate_on_gpu(csk, spec):
+    """Theorem 2 with Lemma 1's distortion measured on the GPU sketch (SURVEY §8(f)
+    NEXT #4, tools/distortion.py): every observed one-step contraction of ||x_k - x*||^2 is at
+    most 1 - (1 - eps)^3 / n * s_r(A)^2 / ||A||_2^2."""
+    import importlib.util, os
+    spec_mod = importlib.util.spec_from_file_location(
+        "distortion", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "distortion.py"))
+    dist = importlib.util.module_from_spec(spec_mod)
+    spec_mod.loader.exec_module(dist)
+    A, b, xs, d, seed = dist.problem(spec)
+    m, n = A.shape
+    Q, R = torch.linalg.qr(A, mode="reduced")
+    SQ, _, _ = csk.csk_sketch(Q.contiguous(), torch.zeros(m, dtype=torch.float64, device="cuda"), d, seed=seed)
+    s = torch.linalg.svdvals(SQ)
+    eps11 = max(float(s[0] ** 2 - 1.0), float(1.0 - s[-1] ** 2))
+    At, bt, nsq = csk.csk_sketch(A, b, d, seed=seed)
+    sA, sSA = torch.linalg.svdvals(R), torch.linalg.svdvals(At)
+    eps = max(eps11, float((sA / sSA - 1.0).abs().max()))
+    assert 0.0 < eps < 1.0
+    rho = 1.0 - (1.0 - eps) ** 3 / n * float(sA[-1] ** 2) / float(sA[0] ** 2)
+    r = csk.csk_solve(At, bt, nsq, x_star=xs, trace=300, trace_x=True)
+    k = min(r.iterations, 299)
+    e2 = ((r.x_trace[: k + 1] - xs[None, :]) ** 2).sum(dim=1)
+    assert float((e2[1:] / e2[:-1]).max()) <= rho
