@@ -117,9 +117,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
-def _dist():
+def _dist(force: bool = False):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws > 1:
+    if ws > 1 or force:
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", str(ws))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
         import torch.distributed as dist
         rank = int(os.environ["RANK"])
         local = int(os.environ.get("LOCAL_RANK", rank))
@@ -622,6 +626,8 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (S9/S10) path even at N = 1 (a 1-rank NCCL communicator; tests the N > 1 code path)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -633,8 +639,8 @@ def main():
             return
         print(json.dumps(run_reference(args)))
         return
-    dist, rank, ws, _ = _dist()
-    out = run_ours(args, dist, rank, ws) if ws == 1 else run_sharded(args, dist, rank, ws)
+    dist, rank, ws, _ = _dist(force=args.sharded)
+    out = run_ours(args, dist, rank, ws) if ws == 1 and not args.sharded else run_sharded(args, dist, rank, ws)
     if rank == 0:
         print(json.dumps(out))
     if dist is not None:
