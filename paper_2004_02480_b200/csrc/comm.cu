@@ -539,9 +539,9 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
     RankSetup rs;
     rs.P = P;
     rs.rank = me;
-    // about one SM's worth of CTAs in the whole exchange, as on one GPU: the loop is bound by
-    // the exchange latency, and every participant adds traffic on rank 0's {count, max} line
-    rs.Gr = ctx->num_sms / P > 0 ? ctx->num_sms / P : 1;
+    // every SM of every GPU: the CTAs of a rank meet in that rank's memory, and only one key per
+    // rank crosses NVLink (loop.cu, SYS), so the participant count does not grow with P
+    rs.Gr = ctx->num_sms;
     rs.sys = 1;
     for (int r = 0; r < P; ++r) {
         int64_t lo, hi;

@@ -44,6 +44,9 @@ constexpr int kLW = 8;             // warps per CTA
 constexpr int kTmRowsDev = 16;     // rows per thread in the TMEM tier (kTmRows)
 constexpr int kLT = kLW * 32;      // threads per CTA
 constexpr int kXchWords = 16;      // one 128-byte line per {count, max} pair
+// after the 3 pairs: [2 parities][kMaxRanks] LL key slots (16 B each) of the cross-GPU exchange
+constexpr int kKeySlotWords = 2 * kMaxRanks * 2;
+constexpr size_t kXchBytes = static_cast<size_t>(3) * kXchWords * 8 + kKeySlotWords * 8;
 constexpr int kSlotWords = 8;      // LL slot: lambda, score, rr as tagged 32-bit halves + pad
 
 struct LoopParams {
@@ -84,6 +87,8 @@ struct LoopParams {
     const double *bt_r[kMaxRanks];
     const double *nsq_r[kMaxRanks];
     unsigned long long *slots_r[kMaxRanks];  // rank r's LL slots [2][Gr][kSlotWords]
+    unsigned long long *lxch;                // sys: this rank's own pairs (the intra-GPU exchange)
+    unsigned long long *kslot_r[kMaxRanks];  // sys: rank r's LL key slots [2][kMaxRanks][2]
     double *x_r[kMaxRanks];                 // rank r's output x (virtual: per-rank copies)
 };
 
@@ -427,7 +432,7 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CB, int RRMAX, bool RESMODE, int TM, bool CLU, bool ST = false>
+template <int CB, int RRMAX, bool RESMODE, int TM, bool CLU, bool ST = false, bool SYS = false>
 __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     // CLU: the whole grid is one kCS-CTA thread-block cluster and the exchange is an
     // all-to-all of the CTA candidates over DSMEM (no global atomics)
@@ -647,7 +652,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S8 of iteration k-1, fused at the top of iteration k: x_q += lambda a_{i_{k-1}}[c_q]
         //      (the row is in the fixed-offset row buffer, zero past n; odd n: from L2) ----
         if (prow >= 0) {
-            if (even && !p.sys) {
+            if (even && !SYS) {
                 const double *rb = reinterpret_cast<const double *>(smem + kRowbufOff) + tg;
 #pragma unroll
                 for (int q = 0; q < CB; ++q) x[q] = __fma_rn(lam, rb[TG * q], x[q]);
@@ -982,14 +987,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
                     const size_t par_off = static_cast<size_t>(k & 1) * p.Gr * kSlotWords;
                     if (lane == 0) {
-                        // (sys: the pair lives in rank 0's memory and the slots are read by the
-                        //  other GPUs -- system-scope atomics, polls and stores over NVLink)
+                        // (SYS: the slots are read by the other GPUs -- system-scope stores)
                         unsigned long long *my = p.slots_r[rk] + par_off + static_cast<size_t>(lc) * kSlotWords;
                         unsigned long long h0, l0, h1, l1, h2 = 0, l2 = 0;
                         ll_pack(cl_l, tag, h0, l0);
                         ll_pack(cl_s, tag, h1, l1);
                         if (RESMODE) ll_pack(crr, tag, h2, l2);
-                        if (!p.sys) {
+                        if constexpr (!SYS) {
                             if (lead) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
                             red_max_u64(pair + 1, kc);
                             red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
@@ -998,9 +1002,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             st_relaxed_v2_u64(my + 2, h1, l1);
                             if (RESMODE) st_relaxed_v2_u64(my + 4, h2, l2);
                         } else {
-                            if (lead) st_relaxed_v2_u64_sys(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
-                            red_max_u64_sys(pair + 1, kc);
-                            red_add_release_u64_sys(pair, 1ull);
+                            // across GPUs, in two levels: this rank's CTAs meet on a pair in this
+                            // rank's memory (GPU scope: a system-scope release costs microseconds);
+                            // the rank's leader then pushes one LL-tagged key to every rank (below)
+                            unsigned long long *lp = p.lxch + static_cast<int>(k % 3) * kXchWords;
+                            if (lc == 0) st_relaxed_v2_u64(p.lxch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                            red_max_u64(lp + 1, kc);
+                            red_add_release_u64(lp, 1ull);
                             st_relaxed_v2_u64_sys(my, h0, l0);
                             st_relaxed_v2_u64_sys(my + 2, h1, l1);
                             if (RESMODE) st_relaxed_v2_u64_sys(my + 4, h2, l2);
@@ -1014,24 +1022,51 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         p.skew[(k - 8) * 2 * G + cta] = static_cast<long long>(gt);
                     }
 #endif
-                    unsigned long long c, mx;
+                    unsigned long long c = 0ull, mx = 0ull;
                     unsigned long long t_spin = 0ull;
                     uint32_t spins = 0u;
                     bool timed_out = false;
-                    do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
-                        if (p.sys) ld_relaxed_v2_sys(pair, c, mx);
-                        else ld_relaxed_v2(pair, c, mx);
-                        // watchdog: a rank that never arrives (a peer that failed to launch) turns
-                        // into an error instead of a hang; the clock is read only every 4096 polls
-                        // (a normal exchange ends after a few), so it is off the fast path
-                        if (((++spins) & 4095u) == 0u && c < static_cast<unsigned long long>(G)) {
+                    // watchdog: a rank that never arrives (a peer that failed to launch) turns into
+                    // an error instead of a hang; the clock is read only every 4096 polls
+                    auto watchdog = [&]() {
+                        if (((++spins) & 4095u) == 0u) {
                             const unsigned long long now = globaltimer_ns();
                             if (t_spin == 0ull) t_spin = now;
-                            else if (now - t_spin > p.timeout_ns) {
-                                timed_out = true;
-                                break;
-                            }
+                            else if (now - t_spin > p.timeout_ns) timed_out = true;
                         }
+                        return timed_out;
+                    };
+                    if constexpr (SYS) {
+                        // the rank's leader (its CTA 0): once every local CTA has counted, push the
+                        // rank's max key into every rank's key slot (LL: key halves + tag, no fence)
+                        const uint32_t tag = static_cast<uint32_t>(k + 1);
+                        if (lc == 0 && lane == 0) {
+                            const unsigned long long *lp = p.lxch + static_cast<int>(k % 3) * kXchWords;
+                            unsigned long long lc2 = 0ull, lmx = 0ull;
+                            do {
+                                ld_relaxed_v2(lp, lc2, lmx);
+                            } while (lc2 < static_cast<unsigned long long>(p.Gr) && !watchdog());
+                            unsigned long long h, l;
+                            ll_pack(__longlong_as_double(static_cast<long long>(lmx)), tag, h, l);
+                            for (int q = 0; q < p.P; ++q)
+                                st_relaxed_v2_u64_sys(p.kslot_r[q] + ((k & 1) * kMaxRanks + rk) * 2, h, l);
+                        }
+                        // every CTA: the P rank keys from its own rank's key slots
+                        for (int q = 0; q < p.P && !timed_out; ++q) {
+                            const unsigned long long *ks = p.kslot_r[rk] + ((k & 1) * kMaxRanks + q) * 2;
+                            unsigned long long a0, a1;
+                            do {
+                                ld_relaxed_v2_sys(ks, a0, a1);
+                            } while (!ll_ok(a0, a1, tag) && !watchdog());
+                            const unsigned long long kq =
+                                static_cast<unsigned long long>(__double_as_longlong(ll_val(a0, a1)));
+                            if (kq > mx) mx = kq;
+                        }
+                        timed_out = __any_sync(0xffffffffu, timed_out);
+                        c = static_cast<unsigned long long>(G);
+                    } else do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
+                        ld_relaxed_v2(pair, c, mx);
+                        if (c < static_cast<unsigned long long>(G) && watchdog()) break;
                     } while (c < static_cast<unsigned long long>(G));
                     if (timed_out) {
                         stop = -3;
@@ -1072,7 +1107,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             unsigned long long *sb = const_cast<unsigned long long *>(slotbuf);
                             sb[4] = reinterpret_cast<unsigned long long>(orow);
                             sb[7] = reinterpret_cast<unsigned long long>(oslot);
-                            if (!p.sys) {
+                            if constexpr (!SYS) {
                                 // winner's (lambda, score) slot and A~^(ik) -> shared memory, one
                                 // mbarrier (odd n: the row is read with plain loads in the update)
                                 const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
@@ -1098,7 +1133,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         double t = 0.0;
                         for (int cc = lane; cc < G; cc += 32) {
                             const int cr = cc / p.Gr, cl2 = cc - cr * p.Gr;
-                            t = t + ll_load(p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4, tag, p.sys != 0);
+                            t = t + ll_load(p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4, tag, SYS);
                         }
                         t = lwarp_sum(t);
                         res = bb > 0.0 ? t / bb : t;
@@ -1143,8 +1178,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 sc = ll_val(slotbuf[2], slotbuf[3]);
             } else if (!CLU) {  // the copy raced the owner's slot store: re-read until the tags match
                 const unsigned long long *gs = reinterpret_cast<const unsigned long long *>(slotbuf[7]);
-                lam = ll_load(gs, tag, p.sys != 0);
-                sc = ll_load(gs + 2, tag, p.sys != 0);
+                lam = ll_load(gs, tag, SYS);
+                sc = ll_load(gs + 2, tag, SYS);
             }
             if (sc == 0.0) stop = CSK_STAGNATED;  // every unmasked residual is 0
         }
@@ -1218,6 +1253,35 @@ struct LoopVariant {
     bool tm = false;
     bool clu = false;
 };
+// Real multi-GPU launches (SYS: peer memory, the two-level exchange) get their own, smaller set
+// of instantiations; the single-GPU kernels carry none of that code.  {cb, rrmax, fn, tm kind
+// (0 none, 1 wide, 2 narrow), stream ring, residual mode}
+struct SysVariant {
+    int cb, rrmax, tmk;
+    bool st, res;
+    LoopFn fn;
+};
+const SysVariant kVariantsSys[] = {
+    {1, 32, 0, false, false, k_loop<1, 32, false, 0, false, false, true>},
+    {2, 32, 0, false, false, k_loop<2, 32, false, 0, false, false, true>},
+    {4, 20, 0, false, false, k_loop<4, 20, false, 0, false, false, true>},
+    {8, 10, 0, false, false, k_loop<8, 10, false, 0, false, false, true>},
+    {16, 5, 0, false, false, k_loop<16, 5, false, 0, false, false, true>},
+    {1, 32, 0, false, true, k_loop<1, 32, true, 0, false, false, true>},
+    {2, 32, 0, false, true, k_loop<2, 32, true, 0, false, false, true>},
+    {4, 20, 0, false, true, k_loop<4, 20, true, 0, false, false, true>},
+    {8, 10, 0, false, true, k_loop<8, 10, true, 0, false, false, true>},
+    {16, 5, 0, false, true, k_loop<16, 5, true, 0, false, false, true>},
+    {8, 6, 1, false, false, k_loop<8, 6, false, 1, false, false, true>},
+    {8, 6, 1, false, true, k_loop<8, 6, true, 1, false, false, true>},
+    {8, 8, 2, false, false, k_loop<8, 8, false, 2, false, false, true>},
+    {8, 8, 2, false, true, k_loop<8, 8, true, 2, false, false, true>},
+    {1, 8, 0, true, false, k_loop<1, 8, false, 0, false, true, true>},
+    {2, 8, 0, true, false, k_loop<2, 8, false, 0, false, true, true>},
+    {4, 8, 0, true, false, k_loop<4, 8, false, 0, false, true, true>},
+    {8, 8, 0, true, false, k_loop<8, 8, false, 0, false, true, true>},
+    {8, 6, 1, true, false, k_loop<8, 6, false, 1, false, true, true>},
+};
 const LoopVariant kVariants[] = {
     {1, 2, k_loop<1, 2, false, 0, false>},   {1, 8, k_loop<1, 8, false, 0, false>},   {1, 32, k_loop<1, 32, false, 0, false>},
     {2, 2, k_loop<2, 2, false, 0, false>},   {2, 8, k_loop<2, 8, false, 0, false>},   {2, 32, k_loop<2, 32, false, 0, false>},
@@ -1282,7 +1346,7 @@ __global__ void k_sumsq_loop(const double *v, int64_t len, double *out) {
 }  // namespace
 
 size_t loop_exchange_bytes(int total_ctas) {
-    return static_cast<size_t>(3) * kXchWords * 8 + static_cast<size_t>(2) * total_ctas * kSlotWords * 8;
+    return kXchBytes + static_cast<size_t>(2) * total_ctas * kSlotWords * 8;
 }
 
 csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq, int64_t d,
@@ -1441,7 +1505,17 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     const int G = geo.G, rows_max = geo.rows_max, rr = geo.rr, rt = geo.rt, rs = geo.rs;
     const size_t smem = geo.smem;
     const LoopVariant *var = geo.var;
-    const LoopFn fn = var->fn;
+    LoopFn fn = var->fn;
+    if (multi && ranks->sys) {  // the SYS twin of the chosen layout
+        const int tmk = !var->tm ? 0 : (var->rrmax == kTmRegRowsWide ? 1 : 2);
+        const SysVariant *sv = nullptr;
+        for (const auto &v : kVariantsSys)
+            if (v.cb == var->cb && v.tmk == tmk && v.st == (geo.st_rows > 0) && v.res == resmode &&
+                (tmk != 0 ? v.rrmax == var->rrmax : v.rrmax >= rr) && (!sv || v.rrmax < sv->rrmax))
+                sv = &v;
+        if (!sv) return CSK_E_UNSUPPORTED;  // the caller takes the host-driven NCCL loop
+        fn = sv->fn;
+    }
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(fn)));
     int per = 0;
     // CTAs of this launch (virtual ranks: all of them) and of the whole exchange
@@ -1454,7 +1528,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     int kb = 1;
     while ((1ll << kb) < d + 1) ++kb;
 
-    const size_t xch_bytes = 3 * kXchWords * 8;
+    const size_t xch_bytes = kXchBytes;
     const size_t ex_bytes = loop_exchange_bytes(gtotal);
     CSK_CHECK(ensure(ctx, ctx->slots, ex_bytes));
     CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
@@ -1496,6 +1570,14 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         for (int r = 0; r < ranks->P; ++r)  // virtual ranks: slices of this ctx's slots
             prm.slots_r[r] = ranks->slots_r[r] ? ranks->slots_r[r]
                                                : prm.slots + static_cast<size_t>(r) * 2 * ranks->Gr * kSlotWords;
+    }
+    if (multi && ranks->sys) {  // the two-level cross-GPU exchange (this rank's pairs, every rank's key slots)
+        prm.lxch = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(prm.slots_r[ranks->rank]) -
+                                                          xch_bytes);
+        for (int r = 0; r < ranks->P; ++r)
+            prm.kslot_r[r] = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(prm.slots_r[r]) -
+                                                                     xch_bytes) +
+                             3 * kXchWords;
     }
     prm.report = static_cast<int64_t *>(ctx->report.ptr);
     prm.bb = bb;
