@@ -87,8 +87,7 @@ struct LoopParams {
     const double *bt_r[kMaxRanks];
     const double *nsq_r[kMaxRanks];
     unsigned long long *slots_r[kMaxRanks];  // rank r's LL slots [2][Gr][kSlotWords]
-    unsigned long long *lxch;                // sys: this rank's own pairs (the intra-GPU exchange)
-    unsigned long long *kslot_r[kMaxRanks];  // sys: rank r's LL key slots [2][kMaxRanks][2]
+    unsigned long long *xch_r[kMaxRanks];    // SYS: rank r's exchange region (its pairs, then its key slots)
     double *x_r[kMaxRanks];                 // rank r's output x (virtual: per-rank copies)
 };
 
@@ -450,6 +449,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const int grp = warp / WPG, wg = warp - grp * WPG, tg = tid - grp * TG;
     // rank rk owns the rows [dlo[rk], dlo[rk+1]); its CTA lc the rows [dlo + lc RMr, ...),
     // RMr = ceil(rank rows / Gr): the owner of global row i is (rank of i, (i - dlo) / RMr)
+    // (non-SYS kernels serve one rank -- every multi-rank launch, virtual or real, uses SYS --
+    //  but keep the general form: the single-rank values come from the parameters)
     const int rk = p.rank >= 0 ? p.rank : cta / p.Gr;
     const int lc = p.rank >= 0 ? cta : cta - rk * p.Gr;
     const int G = p.P * p.Gr;  // CTAs in the exchange (all ranks)
@@ -1005,8 +1006,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             // across GPUs, in two levels: this rank's CTAs meet on a pair in this
                             // rank's memory (GPU scope: a system-scope release costs microseconds);
                             // the rank's leader then pushes one LL-tagged key to every rank (below)
-                            unsigned long long *lp = p.lxch + static_cast<int>(k % 3) * kXchWords;
-                            if (lc == 0) st_relaxed_v2_u64(p.lxch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                            unsigned long long *lp = p.xch_r[rk] + static_cast<int>(k % 3) * kXchWords;
+                            if (lc == 0) st_relaxed_v2_u64(p.xch_r[rk] + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
                             red_max_u64(lp + 1, kc);
                             red_add_release_u64(lp, 1ull);
                             st_relaxed_v2_u64_sys(my, h0, l0);
@@ -1041,7 +1042,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         // rank's max key into every rank's key slot (LL: key halves + tag, no fence)
                         const uint32_t tag = static_cast<uint32_t>(k + 1);
                         if (lc == 0 && lane == 0) {
-                            const unsigned long long *lp = p.lxch + static_cast<int>(k % 3) * kXchWords;
+                            const unsigned long long *lp = p.xch_r[rk] + static_cast<int>(k % 3) * kXchWords;
                             unsigned long long lc2 = 0ull, lmx = 0ull;
                             do {
                                 ld_relaxed_v2(lp, lc2, lmx);
@@ -1049,11 +1050,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             unsigned long long h, l;
                             ll_pack(__longlong_as_double(static_cast<long long>(lmx)), tag, h, l);
                             for (int q = 0; q < p.P; ++q)
-                                st_relaxed_v2_u64_sys(p.kslot_r[q] + ((k & 1) * kMaxRanks + rk) * 2, h, l);
+                                st_relaxed_v2_u64_sys(p.xch_r[q] + 3 * kXchWords + ((k & 1) * kMaxRanks + rk) * 2, h, l);
                         }
                         // every CTA: the P rank keys from its own rank's key slots
                         for (int q = 0; q < p.P && !timed_out; ++q) {
-                            const unsigned long long *ks = p.kslot_r[rk] + ((k & 1) * kMaxRanks + q) * 2;
+                            const unsigned long long *ks = p.xch_r[rk] + 3 * kXchWords + ((k & 1) * kMaxRanks + q) * 2;
                             unsigned long long a0, a1;
                             do {
                                 ld_relaxed_v2_sys(ks, a0, a1);
@@ -1506,7 +1507,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     const size_t smem = geo.smem;
     const LoopVariant *var = geo.var;
     LoopFn fn = var->fn;
-    if (multi && ranks->sys) {  // the SYS twin of the chosen layout
+    if (multi) {  // the SYS twin of the chosen layout (virtual ranks included)
         const int tmk = !var->tm ? 0 : (var->rrmax == kTmRegRowsWide ? 1 : 2);
         const SysVariant *sv = nullptr;
         for (const auto &v : kVariantsSys)
@@ -1529,7 +1530,9 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     while ((1ll << kb) < d + 1) ++kb;
 
     const size_t xch_bytes = kXchBytes;
-    const size_t ex_bytes = loop_exchange_bytes(gtotal);
+    // multi-rank launches on this GPU (virtual ranks) need one exchange region per rank
+    const int nreg = (multi && ranks->rank < 0) ? ranks->P : 1;
+    const size_t ex_bytes = loop_exchange_bytes(gtotal) + static_cast<size_t>(nreg - 1) * xch_bytes;
     CSK_CHECK(ensure(ctx, ctx->slots, ex_bytes));
     CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
@@ -1563,21 +1566,21 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     }
     prm.x_star = x_star; prm.tol = tol; prm.max_iters = max_iters;
     prm.xch = static_cast<unsigned long long *>(ctx->slots.ptr);
-    prm.slots = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(ctx->slots.ptr) + xch_bytes);
+    prm.slots = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(ctx->slots.ptr) +
+                                                       static_cast<size_t>(nreg) * xch_bytes);
     prm.slots_r[0] = prm.slots;
     if (multi) {
-        if (ranks->xch) prm.xch = ranks->xch;
-        for (int r = 0; r < ranks->P; ++r)  // virtual ranks: slices of this ctx's slots
-            prm.slots_r[r] = ranks->slots_r[r] ? ranks->slots_r[r]
-                                               : prm.slots + static_cast<size_t>(r) * 2 * ranks->Gr * kSlotWords;
-    }
-    if (multi && ranks->sys) {  // the two-level cross-GPU exchange (this rank's pairs, every rank's key slots)
-        prm.lxch = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(prm.slots_r[ranks->rank]) -
-                                                          xch_bytes);
-        for (int r = 0; r < ranks->P; ++r)
-            prm.kslot_r[r] = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(prm.slots_r[r]) -
-                                                                     xch_bytes) +
-                             3 * kXchWords;
+        for (int r = 0; r < ranks->P; ++r) {
+            if (ranks->slots_r[r]) {  // real ranks: each rank's buffer is [its region][its slots]
+                prm.slots_r[r] = ranks->slots_r[r];
+                prm.xch_r[r] = reinterpret_cast<unsigned long long *>(
+                    reinterpret_cast<unsigned char *>(ranks->slots_r[r]) - xch_bytes);
+            } else {  // virtual ranks: regions and slot slices of this ctx's buffer
+                prm.slots_r[r] = prm.slots + static_cast<size_t>(r) * 2 * ranks->Gr * kSlotWords;
+                prm.xch_r[r] = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(ctx->slots.ptr) +
+                                                                      static_cast<size_t>(r) * xch_bytes);
+            }
+        }
     }
     prm.report = static_cast<int64_t *>(ctx->report.ptr);
     prm.bb = bb;
