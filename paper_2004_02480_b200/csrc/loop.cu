@@ -46,7 +46,11 @@ constexpr int kLT = kLW * 32;      // threads per CTA
 constexpr int kXchWords = 16;      // one 128-byte line per {count, max} pair
 // after the 3 pairs: [2 parities][kMaxRanks] LL key slots (16 B each) of the cross-GPU exchange
 constexpr int kKeySlotWords = 2 * kMaxRanks * 2;
-constexpr size_t kXchBytes = static_cast<size_t>(3) * kXchWords * 8 + kKeySlotWords * 8;
+// then (SYS, P > 1) two row-staging buffers: one 128-B flag line, then [2][CSK_MAX_N] doubles --
+// the winner's row is fetched over NVLink once per GPU, not once per CTA
+constexpr size_t kStageFlagOff = static_cast<size_t>(3) * kXchWords * 8 + kKeySlotWords * 8;  // bytes
+constexpr size_t kStageRowOff = kStageFlagOff + 128;
+constexpr size_t kXchBytes = kStageRowOff + static_cast<size_t>(2) * CSK_MAX_N * 8;
 constexpr int kSlotWords = 8;      // LL slot: lambda, score, rr as tagged 32-bit halves + pad
 
 struct LoopParams {
@@ -657,6 +661,24 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 const double *rb = reinterpret_cast<const double *>(smem + kRowbufOff) + tg;
 #pragma unroll
                 for (int q = 0; q < CB; ++q) x[q] = __fma_rn(lam, rb[TG * q], x[q]);
+            } else if (SYS && p.P > 1) {
+                // the row staged in this rank's memory by its CTA 0: wait for the iteration's flag,
+                // then coherent (L2) loads of this thread's columns
+                const unsigned char *reg = reinterpret_cast<const unsigned char *>(p.xch_r[rk]);
+                const unsigned long long *flag =
+                    reinterpret_cast<const unsigned long long *>(reg + kStageFlagOff) + ((k - 1) & 1);
+                const uint32_t want = static_cast<uint32_t>(k);  // the row of iteration k - 1: tag k
+                unsigned long long f;
+                do {  // relaxed polls, then one acquire load orders the row loads after the flag
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(flag) : "memory");
+                } while (static_cast<uint32_t>(f) != want);
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(flag) : "memory");
+                const double *src = reinterpret_cast<const double *>(reg + kStageRowOff) + ((k - 1) & 1) * CSK_MAX_N;
+#pragma unroll
+                for (int q = 0; q < CB; ++q) {
+                    const int c = tg + TG * q;
+                    if (c < n) x[q] = __fma_rn(lam, __ldcg(src + c), x[q]);
+                }
             } else {
                 const double *src = prow_ptr;
 #pragma unroll
@@ -1195,6 +1217,22 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         last = wrow;
         prow = wrow;
         prow_ptr = wrow_ptr;
+        if constexpr (SYS) {
+            if (p.P > 1 && lc == 0) {
+                // this rank's CTA 0 stages the winner's row (read over NVLink once for the GPU)
+                // for the update at the top of iteration k + 1, then raises the flag (tag k + 1)
+                unsigned char *reg = reinterpret_cast<unsigned char *>(p.xch_r[rk]);
+                double *dst = reinterpret_cast<double *>(reg + kStageRowOff) + (k & 1) * CSK_MAX_N;
+                for (int c = tid; c < n; c += kLT) dst[c] = ldg_stream1(wrow_ptr + c);
+                __syncthreads();
+                if (tid == 0) {
+                    unsigned long long *flag = reinterpret_cast<unsigned long long *>(reg + kStageFlagOff) + (k & 1);
+                    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag),
+                                 "l"(static_cast<unsigned long long>(k + 1))
+                                 : "memory");
+                }
+            }
+        }
     }
 #undef LP
     if constexpr (ST) {  // drain the copies already issued for the iteration that never ran
