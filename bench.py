@@ -614,6 +614,35 @@ def run_sharded(args, dist, rank, ws):
                              "k_sketch_dense, k_loop (+ the NCCL reduce-scatter of S9 and the NCCL handle/barrier "
                              "collectives of S10)",
     }
+    # ---- e2e at N GPUs: every rank's pinned host shard -> device, S9 + S10 through the public
+    #      API, x back to the host (max over ranks of the per-step wall time)
+    if not args.no_e2e:
+        A_h = A_loc.cpu().pin_memory()
+        b_h = b_loc.cpu().pin_memory()
+        xs_h = xs.cpu().pin_memory()
+        times = []
+        for k in range(4):
+            _barrier(dist)
+            torch.cuda.synchronize()
+            ta = time.perf_counter()
+            A_d = A_h.to(dev, non_blocking=True)
+            b_d = b_h.to(dev, non_blocking=True)
+            xs_d = xs_h.to(dev, non_blocking=True)
+            At, bt, nsq, dlo, dhi = csk.csk_sketch_sharded(A_d, b_d, lo, cfg.m, cfg.d, ws, rank,
+                                                           seed=cfg.sketch_seed, ctx=ctx)
+            x, rep = csk.csk_solve_sharded(At, bt, nsq, dlo, dhi, cfg.d, cfg.n, x_star=xs_d, tol=cfg.tol,
+                                           max_iters=cfg.max_iters, ctx=ctx)
+            x_h = x.cpu()
+            torch.cuda.synchronize()
+            if k:
+                times.append((time.perf_counter() - ta) * 1e3)
+            del A_d, b_d, xs_d, At, bt, nsq, x, x_h
+        e2e_ms = _max_over_ranks(dist, sum(times) / len(times))
+        out["e2e"] = {"value": round(e2e_ms, 4), "unit": "ms",
+                      "h2d_bytes_per_step": 8 * (hi - lo) * cfg.n + 8 * (hi - lo) + 8 * cfg.n,
+                      "d2h_bytes_per_step": 8 * cfg.n,
+                      "api": "csk_sketch_sharded + csk_solve_sharded (binding over the C ABI), pinned host shards "
+                             "per rank; max over ranks"}
     csk.comm_destroy(ctx)
     return out
 
