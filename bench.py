@@ -540,6 +540,30 @@ def run_reference(args):
             "iterations": r.iterations, "vs_baseline": None}
 
 
+def _sharded_roofline(dist, cfg, ws, it, kloop, ksk):
+    """Roofline of the dominant kernel (the SYS k_loop) at N ranks: this rank's rows of A~ per
+    iteration over one GPU's on-chip yardstick (max of the kernel time over ranks), beside the
+    sketch kernel against HBM."""
+    hbm_peak, sm_max_mhz, peak_src = _peaks()
+    k_loop_ms = _max_over_ranks(dist, sum(kloop) / len(kloop))
+    k_sk_ms = _max_over_ranks(dist, sum(ksk) / len(ksk))
+    rows = -(-cfg.d // ws)
+    loop_bytes = (8 * rows * cfg.n + 16 * rows) * it
+    smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
+    gbs = loop_bytes / (k_loop_ms * 1e-3) / 1e9
+    sk_bytes = alg_bytes_sketch(cfg) / ws
+    return {"kernel": "k_loop (SYS: two-level cross-GPU exchange), per rank", "bound": "smem",
+            "achieved": round(gbs, 1), "peak": round(smem_peak, 1), "unit": "GB/s", "frac": round(gbs / smem_peak, 4),
+            "traffic": None, "alg_bytes_per_iteration_per_rank": 8 * rows * cfg.n + 16 * rows,
+            "kernel_ms": round(k_loop_ms, 5), "us_per_iteration": round(k_loop_ms * 1e3 / max(it, 1), 3),
+            "peak_source": f"derived: 148 SM x {SMEM_BYTES_PER_CLK_PER_SM} B/clk x {sm_max_mhz:.0f} MHz",
+            "sketch": {"kernel": "k_sketch_dense (this rank's rows)", "bound": "hbm",
+                       "achieved": round(sk_bytes / (k_sk_ms * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
+                       "frac": round(sk_bytes / (k_sk_ms * 1e-3) / 1e9 / hbm_peak, 4), "kernel_ms": round(k_sk_ms, 5),
+                       "peak_source": peak_src},
+            "timing": "CUDA events recorded by libcsk around the kernels (csk_ctx_set_timing), max over ranks"}
+
+
 def run_sharded(args, dist, rank, ws):
     """N > 1: the same workload, sharded (S9/S10); CUDA events, max over ranks."""
     import paper_2004_02480_b200 as csk
@@ -556,6 +580,7 @@ def run_sharded(args, dist, rank, ws):
     torch.cuda.empty_cache()
     ctx = csk.Context()
     init_comm(ctx)
+    csk.csk_ctx_set_timing(True, ctx=ctx)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
 
@@ -583,9 +608,13 @@ def run_sharded(args, dist, rank, ws):
     _barrier(dist)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    kloop, ksk = [], []
     for k in range(args.steps):
         flush.fill_(1.0)
         reps.append(step(evs[k]))
+        torch.cuda.synchronize()  # (outside the events of step k)
+        kloop.append(csk.csk_last_kernel_ms("loop", ctx=ctx))
+        ksk.append(csk.csk_last_kernel_ms("sketch", ctx=ctx))
     torch.cuda.synchronize()
     _barrier(dist)
     t1 = time.perf_counter()
@@ -609,6 +638,7 @@ def run_sharded(args, dist, rank, ws):
         "iterations_per_s": round(it / (sv * 1e-3), 1), "sketch_ms": round(sk, 5), "solve_ms": round(sv, 4),
         "sketch_hbm_gbs": round(alg_bytes_sketch(cfg) / (sk * 1e-3) / 1e9, 1),
         "clocks": sampler.summary(t0, t1),
+        "roofline": _sharded_roofline(dist, cfg, ws, it, kloop, ksk),
         "gpu_launches": args.steps * 4,
         "gpu_launches_note": "per step: the plan (k_plan_fused, or k_hash_keys + CUB radix sort + k_offsets), "
                              "k_sketch_dense, k_loop (+ the NCCL reduce-scatter of S9 and the NCCL handle/barrier "
