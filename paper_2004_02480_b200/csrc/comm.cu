@@ -39,6 +39,16 @@ struct Comm {
     int nranks = 1, rank = 0;
     // peer mappings (cudaIpcOpenMemHandle) of the other ranks' allocations, by handle bytes
     std::map<std::string, void *> peer_open;
+    // the fused S10 setup of the last solve (peer pointers, probed): reused when every rank calls
+    // again with the same A~ shard and exchange buffer
+    struct FusedSetup {
+        bool valid = false;
+        const void *a = nullptr;
+        void *slots = nullptr;
+        int gr = 0;
+        int64_t d_lo = 0, d_hi = 0;
+        RankSetup rs;
+    } fused;
 };
 
 namespace {
@@ -558,6 +568,40 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
     CSK_CHECK(ensure(ctx, ctx->slots, ex));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
     const size_t xch_bytes = ex - static_cast<size_t>(2) * rs.Gr * 8 * 8;
+    // the peer setup of the previous solve, if every rank calls again with the same buffers
+    // (agreed by one all-reduce; any miss redoes the exchange of handles and the probe everywhere)
+    {
+        Comm::FusedSetup &fc = cm->fused;
+        int hit = (fc.valid && fc.a == A_tilde_local && fc.slots == ctx->slots.ptr && fc.gr == rs.Gr &&
+                   fc.d_lo == d_lo && fc.d_hi == d_hi)
+                      ? 1
+                      : 0;
+        int *dflag = reinterpret_cast<int *>(static_cast<double *>(ctx->scalars.ptr) + 1);
+        CSK_CUDA(ctx, cudaMemcpyAsync(dflag, &hit, sizeof(int), cudaMemcpyHostToDevice, s));
+        CSK_NCCL(ctx, ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, cm->nccl, s));
+        int all_hit = 0;
+        CSK_CUDA(ctx, cudaMemcpyAsync(&all_hit, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CSK_CUDA(ctx, cudaStreamSynchronize(s));
+        if (all_hit) {
+            RankSetup rc = fc.rs;
+            rc.bt_r[me] = b_tilde_local;
+            rc.nsq_r[me] = nsq_local;
+            rc.x_r[me] = x;
+            CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, ex, s));
+            double *bb = static_cast<double *>(ctx->scalars.ptr);
+            CSK_CUDA(ctx, cudaMemsetAsync(bb, 0, 8, s));
+            rc.bb = nullptr;
+            if (x_star == nullptr) {
+                k_sumsq_shard<<<1, 1024, 0, s>>>(b_tilde_local, d_hi - d_lo, bb);
+                rc.bb = bb;
+            }
+            CSK_NCCL(ctx, ncclAllReduce(bb, bb, 1, ncclFloat64, ncclSum, cm->nccl, s));  // + the barrier
+            rc.exchange_zeroed = true;
+            return run_loop(ctx, A_tilde_local, b_tilde_local, nsq_local, d_hi - d_lo, n, x, x_star, tol, max_iters,
+                            nullptr, report, s, &rc);
+        }
+        fc.valid = false;
+    }
     // swap IPC handles (A~ rows, exchange buffer) through NCCL.  An export failure is not an
     // error here: every rank sees every rank's `ok` after the all-gather and all of them take the
     // host-driven NCCL loop together
@@ -643,6 +687,13 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
     CSK_NCCL(ctx, ncclAllReduce(bb, bb, 1, ncclFloat64, ncclSum, cm->nccl, s));
     CSK_CUDA(ctx, cudaFreeAsync(dbuf, s));
     rs.exchange_zeroed = true;
+    cm->fused.valid = true;  // peers mapped and probed: reusable while the buffers stay the same
+    cm->fused.a = A_tilde_local;
+    cm->fused.slots = ctx->slots.ptr;
+    cm->fused.gr = rs.Gr;
+    cm->fused.d_lo = d_lo;
+    cm->fused.d_hi = d_hi;
+    cm->fused.rs = rs;
     return run_loop(ctx, A_tilde_local, b_tilde_local, nsq_local, d_hi - d_lo, n, x, x_star, tol, max_iters, nullptr,
                     report, s, &rs);
 }
