@@ -27,3 +27,10 @@ python tools/csk_breakdown.py 700000x150 > /dev/null 2>&1 && \
 CSK_NO_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sketch_dense_wpb -s 2 -c 1 \
     -o gpurun_out/${R}_sketch_wpb python tools/csk_breakdown.py 700000x150 > gpurun_out/${R}_ncu_sketch_wpb.log 2>&1
 ls -la gpurun_out
+# summarise on the box and drop the reports (gpurun merges at most 64 MiB of gpurun_out/)
+for rep in gpurun_out/${R}_*.ncu-rep; do
+    [ -f "$rep" ] || continue
+    b=$(basename "$rep" .ncu-rep)
+    python tools/ncu_summary.py "$rep" > "gpurun_out/${b/${R}_/${R}_ncu_}.txt" 2>&1 && rm -f "$rep"
+done
+ls -la gpurun_out
