@@ -644,7 +644,6 @@ static csk_status_t solve_sharded_fused(csk_ctx_t ctx, const double *A_tilde_loc
             }
         }
         rs.slots_r[r] = reinterpret_cast<unsigned long long *>(xb + xch_bytes);
-        if (r == 0) rs.xch = reinterpret_cast<unsigned long long *>(xb);
     }
     rs.bt_r[me] = b_tilde_local;
     rs.nsq_r[me] = nsq_local;

@@ -133,8 +133,8 @@ struct RankSetup {
     const double *At_r[kMaxRanks] = {};
     const double *bt_r[kMaxRanks] = {};
     const double *nsq_r[kMaxRanks] = {};
-    unsigned long long *slots_r[kMaxRanks] = {};  // null: carved from ctx->slots (virtual ranks)
-    unsigned long long *xch = nullptr;            // null: ctx->slots
+    unsigned long long *slots_r[kMaxRanks] = {};  // null: carved from ctx->slots (virtual ranks); real
+                                                  // ranks: each buffer is [exchange region][slots]
     double *x_r[kMaxRanks] = {};
     const double *bb = nullptr;                   // residual mode: global ||b~||^2 (device), null: computed
     bool exchange_zeroed = false;                 // the caller zeroed xch/slots (and synchronised the ranks)
