@@ -624,6 +624,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     // (the narrow-TMEM variants run at the register limit: there the finalize re-reads them from
     // shared memory, measured faster at C2; the others keep them in registers)
     constexpr bool kFinReg = TM != 2;
+    // wide TMEM tier with groups of up to 64 rows: two finalize warps per group (CTA-uniform)
+    const bool split2 = TM == 1 && WPG >= 2 && (RM + RG - 1) / RG > 32 && (RM + RG - 1) / RG <= 64;
     const double fin_b = (kFinReg && fast_fin && lane < ng) ? btl[lr0 + lane] : 0.0;
     const double fin_i = (kFinReg && fast_fin && lane < ng) ? invl[lr0 + lane] : 0.0;
     const double fin_b2 = (TM == 1 && fast_fin && lane + 32 < ng) ? btl[lr0 + 32 + lane] : 0.0;
@@ -867,10 +869,27 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // ---- S7 (group): r_i = b~_i - dot, score, lambda, key; group argmax -> cand[grp] ----
         if (WPG > 1) group_bar(1 + grp, TG);
         else __syncwarp();
-        if (wg == 0) {
+        if (wg == 0 || (split2 && wg == 1)) {
             unsigned long long bk = 0ull;
             double bl = 0.0, bs = -1.0, rr2 = 0.0;
-            if (fast_fin) {
+            if (split2) {
+                // groups of 33..64 rows with the wide TMEM tier: the group's first two warps take
+                // rows lane and lane + 32 side by side (one candidate each); warp 0's own partial
+                // comes by shuffle when every row of the group is a register row (all_reg)
+                const double own = __shfl_sync(0xffffffffu, sreg, (lane * LPR) & 31);
+                const int l = lr0 + 32 * wg + lane;
+                if (32 * wg + lane < ng) {
+                    double dot = (all_reg && wg == 0) ? own : dotp[l];
+                    for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
+                    const double fb = wg == 0 ? fin_b : fin_b2, fi = wg == 0 ? fin_i : fin_i2;
+                    const double ri = fb - dot;
+                    const double sc = fi > 0.0 ? (ri * ri) * fi : -1.0;
+                    if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
+                    bk = row_key(sc, r0 + l, b);
+                    bl = ri * fi;
+                    bs = sc;
+                }
+            } else if (fast_fin) {
                 // one row per lane; the warp's own partial of row `lane` comes by shuffle when all
                 // rows are register rows, the other warps' partials from shared memory
                 const double own = __shfl_sync(0xffffffffu, sreg, (lane * LPR) & 31);
@@ -914,12 +933,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             if (RESMODE) rr2 = lwarp_sum(rr2);
             unsigned long long km;
             const int wl = warp_max_key_lane(bk, km);
+            const int ci = split2 ? 2 * grp + wg : grp;  // candidate slot
             if (lane == wl) {
-                cand[grp * 4 + 0] = __longlong_as_double(static_cast<long long>(km));
-                cand[grp * 4 + 1] = bl;
-                cand[grp * 4 + 2] = bs;
+                cand[ci * 4 + 0] = __longlong_as_double(static_cast<long long>(km));
+                cand[ci * 4 + 1] = bl;
+                cand[ci * 4 + 2] = bs;
             }
-            if (RESMODE && lane == 0) cand[grp * 4 + 3] = rr2;
+            if (RESMODE && lane == 0) cand[ci * 4 + 3] = rr2;
             LP(0)
             // ---- arrival: the LAST group to finish combines the CTA candidate and runs the
             //      exchange (no CTA barrier before the publish) ----
@@ -950,14 +970,15 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 int64_t wrow = -1;
                 if (stop < 0) {
                     // CTA candidate: max key over the RG group candidates
+                    const int ncand = split2 ? 2 * RG : RG;
                     const unsigned long long ck =
-                        lane < RG ? static_cast<unsigned long long>(__double_as_longlong(cand[lane * 4])) : 0ull;
+                        lane < ncand ? static_cast<unsigned long long>(__double_as_longlong(cand[lane * 4])) : 0ull;
                     unsigned long long kc;
                     const int cl = warp_max_key_lane(ck, kc);
                     const double cl_l = cand[cl * 4 + 1], cl_s = cand[cl * 4 + 2];
                     double crr = 0.0;
                     if (RESMODE)
-                        for (int g = 0; g < RG; ++g) crr = crr + cand[g * 4 + 3];
+                        for (int g = 0; g < ncand; ++g) crr = crr + cand[g * 4 + 3];
                     const uint32_t tag = static_cast<uint32_t>(k + 1);
                     if constexpr (CLU) {
                         // ---- all-to-all over DSMEM: this CTA arms its barrier of this parity for
