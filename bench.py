@@ -83,6 +83,15 @@ class ClockSampler:
                 pass
             time.sleep(0.002)
 
+    def sample_now(self):
+        """One sample from the caller's thread (between timed steps, outside their CUDA events),
+        so a short timed region still has samples taken while the GPU was busy."""
+        if self._nvml:
+            try:
+                self.samples.append(self._sample())
+            except Exception:
+                pass
+
     def start(self):
         if self._nvml:
             self._t = threading.Thread(target=self._run, daemon=True)
@@ -225,6 +234,7 @@ def run_ours(args, dist, rank, ws):
         reps.append(step(evs[k]))
         for w in kern_ms:  # the step already synchronised (csk_solve_wait)
             kern_ms[w].append(csk.csk_last_kernel_ms(w, ctx=ctx))
+        sampler.sample_now()
     torch.cuda.synchronize()
     _barrier(dist)
     t1 = time.perf_counter()
@@ -615,6 +625,7 @@ def run_sharded(args, dist, rank, ws):
         torch.cuda.synchronize()  # (outside the events of step k)
         kloop.append(csk.csk_last_kernel_ms("loop", ctx=ctx))
         ksk.append(csk.csk_last_kernel_ms("sketch", ctx=ctx))
+        sampler.sample_now()
     torch.cuda.synchronize()
     _barrier(dist)
     t1 = time.perf_counter()
