@@ -104,3 +104,23 @@ def test_one_rank_nccl_row_offset_shard(csk):
     At_o, bt_o = oracle.sketch_dense(_np(p.A)[lo:hi], _np(p.b)[lo:hi], d, h=h[lo:hi], s=s[lo:hi])
     assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
     csk.comm_destroy(ctx)
+
+
+def test_bench_sharded_path_one_rank(csk):
+    """bench.py's N > 1 path (S9 + S10 through NCCL, the fused peer-memory loop, its roofline
+    and e2e keys) run through a 1-rank communicator on this GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_PORT="29631")
+    out = subprocess.run([sys.executable, "bench.py", "--sharded", "--steps", "2", "--warmup", "3", "--no-extras",
+                          "--no-cpu"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["termination"] == "converged" and d["final_res"] <= 1e-6
+    for key in ("metric", "value", "unit", "n_gpus", "ms_per_step", "scaling", "config", "clocks", "e2e", "roofline",
+                "gpu_launches"):
+        assert key in d, key
+    assert d["roofline"]["kernel_ms"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
