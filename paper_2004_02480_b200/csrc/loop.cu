@@ -693,14 +693,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         LP(7)
         // ---- S5 partial (last group): ||x_k - x*||^2, combined by the group's finalize warp ----
         double e2 = 0.0;
-        if (!RESMODE && resgrp) {
-            if (lead && p.x_trace && k < p.trace_cap) {
+        if (resgrp && lead && p.x_trace && k < p.trace_cap) {  // both stop modes record the iterates
 #pragma unroll
-                for (int q = 0; q < CB; ++q) {
-                    const int c = tg + TG * q;
-                    if (c < n) p.x_trace[k * n + c] = x[q];
-                }
+            for (int q = 0; q < CB; ++q) {
+                const int c = tg + TG * q;
+                if (c < n) p.x_trace[k * n + c] = x[q];
             }
+        }
+        if (!RESMODE && resgrp) {
 #pragma unroll
             for (int q = 0; q < CB; ++q) {
                 const double e = x[q] - xs[tg + TG * q];
@@ -1174,10 +1174,25 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     LP(9)
                     if (RESMODE) {
                         // ||r_k||^2: the G CTA partials in fixed order (rank-major)
+                        // (a lane's slots are loaded together, 4 in flight, and re-polled only
+                        //  if a tag is stale: one L2 round trip instead of G / 32 in a chain)
                         double t = 0.0;
-                        for (int cc = lane; cc < G; cc += 32) {
+                        auto slot_rr = [&](int cc) {
                             const int cr = cc / p.Gr, cl2 = cc - cr * p.Gr;
-                            t = t + ll_load(p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4, tag, SYS);
+                            return p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4;
+                        };
+                        for (int c0 = lane; c0 < G; c0 += 32 * 4) {
+                            unsigned long long h[4], l[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (c0 + 32 * u < G) {
+                                    if (SYS) ld_relaxed_v2_sys(slot_rr(c0 + 32 * u), h[u], l[u]);
+                                    else ld_relaxed_v2_u64(slot_rr(c0 + 32 * u), h[u], l[u]);
+                                }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (c0 + 32 * u < G)
+                                    t = t + (ll_ok(h[u], l[u], tag) ? ll_val(h[u], l[u]) : ll_load(slot_rr(c0 + 32 * u), tag, SYS));
                         }
                         t = lwarp_sum(t);
                         res = bb > 0.0 ? t / bb : t;
@@ -1341,6 +1356,11 @@ const SysVariant kVariantsSys[] = {
     {4, 8, 0, true, false, k_loop<4, 8, false, 0, false, true, true>},
     {8, 8, 0, true, false, k_loop<8, 8, false, 0, false, true, true>},
     {8, 6, 1, true, false, k_loop<8, 6, false, 1, false, true, true>},
+    {1, 8, 0, true, true, k_loop<1, 8, true, 0, false, true, true>},
+    {2, 8, 0, true, true, k_loop<2, 8, true, 0, false, true, true>},
+    {4, 8, 0, true, true, k_loop<4, 8, true, 0, false, true, true>},
+    {8, 8, 0, true, true, k_loop<8, 8, true, 0, false, true, true>},
+    {8, 6, 1, true, true, k_loop<8, 6, true, 1, false, true, true>},
 };
 const LoopVariant kVariants[] = {
     {1, 2, k_loop<1, 2, false, 0, false>},   {1, 8, k_loop<1, 8, false, 0, false>},   {1, 32, k_loop<1, 32, false, 0, false>},
@@ -1364,12 +1384,23 @@ const LoopVariant kVariantsClu[] = {
     {16, 5, k_loop<16, 5, false, 0, true>, false, true}, {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, false, 1, true>, true, true},
     {8, kTmRegRowsNarrow, k_loop<8, kTmRegRowsNarrow, false, 2, true>, true, true},
 };
-// Stream-ring variants (rows past the on-chip tiers through TMA stages; x* stop rule only):
+const LoopVariant kVariantsCluRes[] = {  // the same with the residual stop (x* unknown)
+    {1, 8, k_loop<1, 8, true, 0, true>, false, true},   {2, 8, k_loop<2, 8, true, 0, true>, false, true},
+    {4, 8, k_loop<4, 8, true, 0, true>, false, true},   {8, 10, k_loop<8, 10, true, 0, true>, false, true},
+    {16, 5, k_loop<16, 5, true, 0, true>, false, true}, {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, true, 1, true>, true, true},
+    {8, kTmRegRowsNarrow, k_loop<8, kTmRegRowsNarrow, true, 2, true>, true, true},
+};
+// Stream-ring variants (rows past the on-chip tiers through TMA stages):
 // few register rows, so the registers go to the streamed chunk's loads
 const LoopVariant kVariantsSt[] = {
     {1, 8, k_loop<1, 8, false, 0, false, true>},  {2, 8, k_loop<2, 8, false, 0, false, true>},
     {4, 8, k_loop<4, 8, false, 0, false, true>},  {8, 8, k_loop<8, 8, false, 0, false, true>},
     {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, false, 1, false, true>, true},
+};
+const LoopVariant kVariantsStRes[] = {  // residual stop (no x*): the same ring, RES from the residuals
+    {1, 8, k_loop<1, 8, true, 0, false, true>},  {2, 8, k_loop<2, 8, true, 0, false, true>},
+    {4, 8, k_loop<4, 8, true, 0, false, true>},  {8, 8, k_loop<8, 8, true, 0, false, true>},
+    {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, true, 1, false, true>, true},
 };
 constexpr size_t kRingMaxBytes = 128 * 1024;  // per CTA, all groups' stages
 const LoopVariant kVariantsRes[] = {
@@ -1484,7 +1515,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         g.var = nullptr;
         if (clu) {
             const int want_rr = tmk == 2 ? kTmRegRowsNarrow : tmk == 1 ? kTmRegRowsWide : (g.rr > 0 ? g.rr : 1);
-            for (const auto &v : kVariantsClu)
+            for (const auto &v : (resmode ? kVariantsCluRes : kVariantsClu))
                 if (v.cb == cb && v.tm == (tmk != 0) && v.rrmax >= want_rr && (tmk == 0 || v.rrmax == want_rr) &&
                     (!g.var || v.rrmax < g.var->rrmax))
                     g.var = &v;
@@ -1497,10 +1528,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         }
         // rows left over for L2/HBM: stream them through a TMA ring (whole rows, 16-B aligned:
         // n even and an aligned A~), taking shared memory from the resident rows
-        if (!clu && !resmode && g.var && g.rr + g.rt + g.rs < g.rb && (n % 2) == 0 && st_aligned &&
+        if (!clu && g.var && g.rr + g.rt + g.rs < g.rb && (n % 2) == 0 && st_aligned &&
             !(flags & CSK_SOLVE_NO_STREAM_RING)) {
             const LoopVariant *sv = nullptr;
-            for (const auto &v : kVariantsSt)
+            for (const auto &v : (resmode ? kVariantsStRes : kVariantsSt))
                 if (v.cb == cb && v.tm == (tmk == 1)) sv = &v;
             // rows per stage: a multiple of 4 (the GEMV passes), >= ~8 KB per stage for short rows
             int R = 4;
@@ -1530,7 +1561,7 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     // no streamed rows and is small enough that 16 SMs' GEMV beats the grid-wide exchange
     // (cluster_size: 0 = auto, 16 = prefer the cluster, 1 = never).
     const int want_cs = opts ? opts->cluster_size : 0;
-    if (!multi && !resmode && want_cs != 1 && (want_cs == kCS || (d * n <= kCluMaxElems && !(opts && opts->num_ctas > 0))) &&
+    if (!multi && want_cs != 1 && (want_cs == kCS || (d * n <= kCluMaxElems && !(opts && opts->num_ctas > 0))) &&
         d >= kCS) {
         Geo g{};
         if (geometry(kCS, true, g) && g.rr + g.rt + g.rs >= g.rb) {

@@ -304,6 +304,11 @@ def test_solve_residual_mode(csk, num_ctas, cluster):
     assert abs(g.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
     r = _np(bt) - _np(At) @ _np(g.x)
     assert float(r @ r) / float(_np(bt) @ _np(bt)) <= 1e-10 * (1 + 1e-6)
+    # the residual-mode kernel records its iterates too: step for step with the oracle
+    g2 = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-30, max_iters=200, num_ctas=num_ctas,
+                       cluster_size=cluster, trace=201, trace_x=True)
+    assert not np.isnan(_np(g2.x_trace)).any()
+    _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 200)
 
 
 def test_solve_edge_cases(csk):
@@ -378,6 +383,26 @@ def test_solve_stream_ring(csk, d, n, num_ctas, smem_rows, tmem, ring):
     if n <= 1000:
         _free_running(g, o)
     _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 200)
+
+
+@pytest.mark.parametrize("d,n,num_ctas,tmem", [(6000, 150, 8, None), (4000, 50, 3, None), (1200, 2000, 6, None),
+                                                (2500, 500, 4, False), (3001, 130, 5, None)])
+def test_solve_stream_ring_residual_mode(csk, d, n, num_ctas, tmem):
+    """The residual stop (no x*, RES_k = ||b~ - A~ x_k||^2 / ||b~||^2) with streamed rows: the
+    RESMODE ring variants give the oracle's i_k and x_k step for step and its stop."""
+    p = make_dense(d, n, "lognormal_rows", d + n + 1, "cuda")
+    At, bt = p.A, p.b
+    nsq = csk.csk_row_norms(At)
+    its = 150 if n > 1000 else 50000
+    g = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-12, num_ctas=num_ctas, tmem=tmem, trace=150,
+                      trace_x=True, max_iters=its)
+    assert csk.csk_last_solve_tiers()["ring_stages"] >= 2
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=None, tol=1e-12, trace=150, max_iters=its)
+    assert g.stop_mode == csk.STOP_RESIDUAL
+    if n <= 1000:
+        assert g.termination == o.termination == csk.CONVERGED
+        assert abs(g.iterations - o.iterations) <= max(1, 0.02 * o.iterations)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 150)
 
 
 @pytest.mark.parametrize("smem_rows,tmem", [(0, None), (-1, False)])
@@ -501,4 +526,8 @@ def test_C5_full_size_sampled(csk):
         a1, b1 = oracle.sketch_csr(sub_rp, cols, vals, bs, cfg.n, 1, h=np.zeros(len(rows), np.int32), s=s[rows])
         assert np.array_equal(_np(At[j]), a1[0]) and _np(bt[j]) == b1[0]
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=6, tol=1e-30, trace=7, trace_x=True)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6)
+    # the residual stop at full size (x* unknown): streamed rows through the RESMODE ring
+    g = csk.csk_solve(At, bt, nsq, x_star=None, max_iters=6, tol=1e-30, trace=7, trace_x=True)
+    assert g.stop_mode == csk.STOP_RESIDUAL and csk.csk_last_solve_tiers()["ring_stages"] >= 2
     _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6)

@@ -58,9 +58,29 @@ def main():
         if not ok_sk:
             print(f"FAIL sketch case {k}: m={m} n={n} d={d} kind={kind}", flush=True)
             sys.exit(1)
+        # a random CSR input of the same shape (0..maxlen stored pairs per row), bit-exact too
+        if rng.random() < 0.3 and n >= 2:
+            maxlen = int(min(n, rng.integers(1, 80)))
+            mm = int(min(m, 30000))
+            lens = rng.integers(0, maxlen + 1, size=mm)
+            rp = np.zeros(mm + 1, np.int64)
+            rp[1:] = np.cumsum(lens)
+            col = np.concatenate([np.sort(rng.choice(n, size=int(c), replace=False)) for c in lens]).astype(np.int32) \
+                if rp[-1] else np.zeros(0, np.int32)
+            val = rng.standard_normal(int(rp[-1]))
+            bb = rng.standard_normal(mm)
+            dd = int(max(1, min(d, mm - 1)))
+            Atc, btc, _ = csk.csk_sketch_csr(torch.from_numpy(rp).cuda(), torch.from_numpy(col).cuda(),
+                                             torch.from_numpy(val).cuda(), torch.from_numpy(bb).cuda(), n, dd, seed=k)
+            Ao, bo = oracle.sketch_csr(rp, col, val, bb, n, dd, seed=k)
+            if not (np.array_equal(_np(Atc), Ao) and np.array_equal(_np(btc), bo)):
+                print(f"FAIL csr case {k}: m={mm} n={n} d={dd} maxlen={maxlen}", flush=True)
+                sys.exit(1)
+            del Atc, btc
         iters = 40
+        xs = p.x_star if rng.random() < 0.85 else None  # residual mode sometimes
         try:
-            g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=1e-30, max_iters=iters, trace=iters + 1,
+            g = csk.csk_solve(At, bt, nsq, x_star=xs, tol=1e-30, max_iters=iters, trace=iters + 1,
                               trace_x=True, **opts)
         except csk.CskError as e:
             if e.status == csk.CSK_E_UNSUPPORTED:
