@@ -102,6 +102,16 @@ __device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long
 __device__ __forceinline__ void red_add_release_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+// {count, max, sum} of one pair in one 32-byte load (one L2 sector: read as one snapshot)
+__device__ __forceinline__ void ld_relaxed_v4(const unsigned long long *p, unsigned long long &a,
+                                              unsigned long long &b, unsigned long long &c) {
+    unsigned long long d;
+    asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p) : "memory");
+}
 // system-scope variants for the cross-GPU exchange (peer memory over NVLink)
 __device__ __forceinline__ void red_max_u64_sys(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -1038,13 +1048,18 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         ll_pack(cl_s, tag, h1, l1);
                         if (RESMODE) ll_pack(crr, tag, h2, l2);
                         if constexpr (!SYS) {
-                            if (lead) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                            if (lead) {
+                                st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                                if (RESMODE) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords + 2, 0ull, 0ull);
+                            }
                             red_max_u64(pair + 1, kc);
-                            red_add_release_u64(pair, 1ull);  // orders the max (and the reset) before the count
+                            // residual stop: ||r_k||^2 accumulates beside the count (one sum,
+                            // read by every CTA in the same load as the count)
+                            if (RESMODE) red_add_f64(reinterpret_cast<double *>(pair + 2), crr);
+                            red_add_release_u64(pair, 1ull);  // orders the max, sum (and reset) before the count
                             // the slot needs no ordering: readers validate its LL tags
                             st_relaxed_v2_u64(my, h0, l0);
                             st_relaxed_v2_u64(my + 2, h1, l1);
-                            if (RESMODE) st_relaxed_v2_u64(my + 4, h2, l2);
                         } else {
                             // across GPUs, in two levels: this rank's CTAs meet on a pair in this
                             // rank's memory (GPU scope: a system-scope release costs microseconds);
@@ -1066,7 +1081,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         p.skew[(k - 8) * 2 * G + cta] = static_cast<long long>(gt);
                     }
 #endif
-                    unsigned long long c = 0ull, mx = 0ull;
+                    unsigned long long c = 0ull, mx = 0ull, rsum = 0ull;
                     unsigned long long t_spin = 0ull;
                     uint32_t spins = 0u;
                     bool timed_out = false;
@@ -1109,7 +1124,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         timed_out = __any_sync(0xffffffffu, timed_out);
                         c = static_cast<unsigned long long>(G);
                     } else do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
-                        ld_relaxed_v2(pair, c, mx);
+                        if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
+                        else ld_relaxed_v2(pair, c, mx);
                         if (c < static_cast<unsigned long long>(G) && watchdog()) break;
                     } while (c < static_cast<unsigned long long>(G));
                     if (timed_out) {
@@ -1173,10 +1189,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
                     LP(9)
                     if (RESMODE) {
-                        // ||r_k||^2: the G CTA partials in fixed order (rank-major)
-                        // (a lane's slots are loaded together, 4 in flight, and re-polled only
-                        //  if a tag is stale: one L2 round trip instead of G / 32 in a chain)
+                        // ||r_k||^2: on one GPU the sum beside the count; across ranks the G CTA
+                        // partials in fixed order (rank-major)
                         double t = 0.0;
+                        if constexpr (!SYS) {
+                            t = __longlong_as_double(static_cast<long long>(rsum));
+                        } else {
+                        // (across ranks, from the LL slots; a lane's slots are loaded together, 4
+                        //  in flight, and re-polled only if a tag is stale)
                         auto slot_rr = [&](int cc) {
                             const int cr = cc / p.Gr, cl2 = cc - cr * p.Gr;
                             return p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4;
@@ -1195,6 +1215,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                                     t = t + (ll_ok(h[u], l[u], tag) ? ll_val(h[u], l[u]) : ll_load(slot_rr(c0 + 32 * u), tag, SYS));
                         }
                         t = lwarp_sum(t);
+                        }
                         res = bb > 0.0 ? t / bb : t;
                         if (lead && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
                         if (res <= p.tol) stop = CSK_CONVERGED;
