@@ -59,6 +59,12 @@ def test_virtual_ranks_streamed_rows(csk, P):
     o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), tol=1e-6, max_iters=5000)
     assert rep.termination == csk.CONVERGED and rep.final_res <= 1e-6
     assert abs(rep.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
+    # the residual stop (x* unknown) through the ring's SYS twins: the partials cross ranks
+    x, copies, rep = csk.csk_solve_virtual_ranks(p.A, p.b, nsq, P, x_star=None, tol=1e-12, max_iters=5000)
+    assert all(torch.equal(copies[q], copies[0]) for q in range(P))
+    o = oracle.mwrk(_np(p.A), _np(p.b), x_star=None, tol=1e-12, max_iters=5000)
+    assert rep.stop_mode == csk.STOP_RESIDUAL and rep.termination == o.termination == csk.CONVERGED
+    assert abs(rep.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
 
 
 def test_virtual_ranks_residual_mode_and_cap(csk):
