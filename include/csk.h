@@ -171,8 +171,12 @@ CSK_API csk_status_t csk_row_norms(csk_ctx_t ctx, const double *A_tilde, int64_t
  *   persistent cooperative kernel runs every iteration: GEMV r = b~ - A~ x_k,
  *   score r_i^2/nsq_i (rows with nsq_i = 0 masked), argmax with lowest-index
  *   ties, x_{k+1} = x_k + (r_ik/nsq_ik) A~^(ik)T, stop test; A~ rows stay
- *   resident in shared memory (the remainder is re-read from L2/HBM).
- *   x_star != NULL: stop when RES <= tol; NULL: residual mode.
+ *   on chip (registers, TMEM, shared memory; the remainder streams from
+ *   L2/HBM through a TMA ring each iteration).
+ *   x_star != NULL: stop when RES <= tol; NULL: residual mode,
+ *   available on every tier.  In residual mode on one GPU the CTA partials of
+ *   ||r_k||^2 are summed in arrival order, so the last bits of RES (and, at a
+ *   RES within rounding of tol, the stop iteration) may differ run to run.
  *   Stops at max_iters (>= 0).  Blocks; fills *report (host pointer).
  *   Returns CSK_E_ZERO_SKETCH if every nsq is 0. */
 CSK_API csk_status_t csk_solve(csk_ctx_t ctx, const double *A_tilde, const double *b_tilde,
