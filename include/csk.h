@@ -51,7 +51,8 @@ typedef enum {
     CSK_OK = 0,
     CSK_E_ARG = 1,          /* bad size, null/misaligned pointer, d >= m, tol <= 0, ... */
     CSK_E_ZERO_SKETCH = 2,  /* every row of A~ is zero: nothing to select */
-    CSK_E_UNSUPPORTED = 3,  /* valid input outside what this build implements */
+    CSK_E_UNSUPPORTED = 3,  /* valid input outside what this build implements (solve: n > 2048,
+                               a grid that cannot be co-resident, or > ~9000 rows per CTA) */
     CSK_E_CUDA = 4,         /* a CUDA runtime error; csk_last_error has the text */
     CSK_E_NCCL = 5,         /* an NCCL error in a sharded call */
     CSK_E_NOMEM = 6         /* workspace allocation failed */
