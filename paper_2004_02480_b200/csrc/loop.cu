@@ -1423,6 +1423,9 @@ const LoopVariant kVariantsStRes[] = {  // residual stop (no x*): the same ring,
     {4, 8, k_loop<4, 8, true, 0, false, true>},  {8, 8, k_loop<8, 8, true, 0, false, true>},
     {8, kTmRegRowsWide, k_loop<8, kTmRegRowsWide, true, 1, false, true>, true},
 };
+// (the host picks between a table and its residual-stop twin with ?:, which needs equal types)
+static_assert(sizeof(kVariantsStRes) == sizeof(kVariantsSt), "stream-ring twins differ in size");
+static_assert(sizeof(kVariantsCluRes) == sizeof(kVariantsClu), "cluster twins differ in size");
 constexpr size_t kRingMaxBytes = 128 * 1024;  // per CTA, all groups' stages
 const LoopVariant kVariantsRes[] = {
     {1, 32, k_loop<1, 32, true, 0, false>}, {2, 32, k_loop<2, 32, true, 0, false>}, {4, 20, k_loop<4, 20, true, 0, false>},
