@@ -1,4 +1,4 @@
-"""Re-run one fuzz case with option variants: python tools/fuzz_case.py m n d kind seed"""
+"""Re-run one fuzz case with option variants: python tests/fuzz_case.py m n d kind seed"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))

@@ -1,6 +1,6 @@
 """Randomised parity sweep against the oracle (seeded; not part of the default test run).
 
-python tools/fuzz_parity.py [count] [seed]
+python tests/fuzz_parity.py [count] [seed]
 
 For each random case: m, n, d, the input kind, and the solve's launch options (grid, cluster,
 resident rows, TMEM tier, stream ring) are drawn; the sketch must be bit-exact against the oracle

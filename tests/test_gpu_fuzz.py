@@ -1,4 +1,4 @@
-"""A short run of the randomised parity sweep (tools/fuzz_parity.py): random m, n, d, input kinds
+"""A short run of the randomised parity sweep (tests/fuzz_parity.py): random m, n, d, input kinds
 and launch options; the dense and CSR sketches bit-exact against the oracle and the solve in
 lockstep with it, in both stop modes.  The full sweeps are in profiles/r01_fuzz_parity.txt."""
 import importlib.util
@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def test_random_cases(seed, monkeypatch, capsys):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "fuzz_parity.py")
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "fuzz_parity.py")
     spec = importlib.util.spec_from_file_location("fuzz_parity", path)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
