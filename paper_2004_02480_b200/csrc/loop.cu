@@ -45,7 +45,7 @@ constexpr int kTmRowsDev = 16;     // rows per thread in the TMEM tier (kTmRows)
 constexpr int kLT = kLW * 32;      // threads per CTA
 constexpr int kXchWords = 16;      // one 128-byte line per {count, max} pair
 // after the 3 pairs: [2 parities][kMaxRanks] LL key slots (16 B each) of the cross-GPU exchange
-constexpr int kKeySlotWords = 2 * kMaxRanks * 2;
+constexpr int kKeySlotWords = 2 * kMaxRanks * 2 * 2;  // per parity and rank: the LL key, then the LL ||r||^2 sum
 // then (SYS, P > 1) two row-staging buffers: one 128-B flag line, then [2][CSK_MAX_N] doubles --
 // the winner's row is fetched over NVLink once per GPU, not once per CTA
 constexpr size_t kStageFlagOff = static_cast<size_t>(3) * kXchWords * 8 + kKeySlotWords * 8;  // bytes
@@ -1043,10 +1043,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     if (lane == 0) {
                         // (SYS: the slots are read by the other GPUs -- system-scope stores)
                         unsigned long long *my = p.slots_r[rk] + par_off + static_cast<size_t>(lc) * kSlotWords;
-                        unsigned long long h0, l0, h1, l1, h2 = 0, l2 = 0;
+                        unsigned long long h0, l0, h1, l1;
                         ll_pack(cl_l, tag, h0, l0);
                         ll_pack(cl_s, tag, h1, l1);
-                        if (RESMODE) ll_pack(crr, tag, h2, l2);
                         if constexpr (!SYS) {
                             if (lead) {
                                 st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
@@ -1065,12 +1064,15 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             // rank's memory (GPU scope: a system-scope release costs microseconds);
                             // the rank's leader then pushes one LL-tagged key to every rank (below)
                             unsigned long long *lp = p.xch_r[rk] + static_cast<int>(k % 3) * kXchWords;
-                            if (lc == 0) st_relaxed_v2_u64(p.xch_r[rk] + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                            if (lc == 0) {
+                                st_relaxed_v2_u64(p.xch_r[rk] + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                                if (RESMODE) st_relaxed_v2_u64(p.xch_r[rk] + ((k + 1) % 3) * kXchWords + 2, 0ull, 0ull);
+                            }
                             red_max_u64(lp + 1, kc);
+                            if (RESMODE) red_add_f64(reinterpret_cast<double *>(lp + 2), crr);  // the rank's ||r||^2
                             red_add_release_u64(lp, 1ull);
                             st_relaxed_v2_u64_sys(my, h0, l0);
                             st_relaxed_v2_u64_sys(my + 2, h1, l1);
-                            if (RESMODE) st_relaxed_v2_u64_sys(my + 4, h2, l2);
                         }
                     }
                     LP(2)
@@ -1101,14 +1103,19 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         const uint32_t tag = static_cast<uint32_t>(k + 1);
                         if (lc == 0 && lane == 0) {
                             const unsigned long long *lp = p.xch_r[rk] + static_cast<int>(k % 3) * kXchWords;
-                            unsigned long long lc2 = 0ull, lmx = 0ull;
+                            unsigned long long lc2 = 0ull, lmx = 0ull, lsum = 0ull;
                             do {
-                                ld_relaxed_v2(lp, lc2, lmx);
+                                if (RESMODE) ld_relaxed_v4(lp, lc2, lmx, lsum);
+                                else ld_relaxed_v2(lp, lc2, lmx);
                             } while (lc2 < static_cast<unsigned long long>(p.Gr) && !watchdog());
-                            unsigned long long h, l;
+                            unsigned long long h, l, hs = 0ull, ls = 0ull;
                             ll_pack(__longlong_as_double(static_cast<long long>(lmx)), tag, h, l);
-                            for (int q = 0; q < p.P; ++q)
-                                st_relaxed_v2_u64_sys(p.xch_r[q] + 3 * kXchWords + ((k & 1) * kMaxRanks + rk) * 2, h, l);
+                            if (RESMODE) ll_pack(__longlong_as_double(static_cast<long long>(lsum)), tag, hs, ls);
+                            for (int q = 0; q < p.P; ++q) {
+                                unsigned long long *ks = p.xch_r[q] + 3 * kXchWords + ((k & 1) * kMaxRanks + rk) * 2;
+                                st_relaxed_v2_u64_sys(ks, h, l);
+                                if (RESMODE) st_relaxed_v2_u64_sys(ks + 2 * kMaxRanks * 2, hs, ls);
+                            }
                         }
                         // every CTA: the P rank keys from its own rank's key slots
                         for (int q = 0; q < p.P && !timed_out; ++q) {
@@ -1120,6 +1127,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             const unsigned long long kq =
                                 static_cast<unsigned long long>(__double_as_longlong(ll_val(a0, a1)));
                             if (kq > mx) mx = kq;
+                            if (RESMODE) {  // the ranks' sums in rank order: every rank adds the same way
+                                const double sq = ll_load(ks + 2 * kMaxRanks * 2, tag, true);
+                                rsum = static_cast<unsigned long long>(__double_as_longlong(
+                                    __longlong_as_double(static_cast<long long>(rsum)) + sq));
+                            }
                         }
                         timed_out = __any_sync(0xffffffffu, timed_out);
                         c = static_cast<unsigned long long>(G);
@@ -1189,33 +1201,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
                     LP(9)
                     if (RESMODE) {
-                        // ||r_k||^2: on one GPU the sum beside the count; across ranks the G CTA
-                        // partials in fixed order (rank-major)
-                        double t = 0.0;
-                        if constexpr (!SYS) {
-                            t = __longlong_as_double(static_cast<long long>(rsum));
-                        } else {
-                        // (across ranks, from the LL slots; a lane's slots are loaded together, 4
-                        //  in flight, and re-polled only if a tag is stale)
-                        auto slot_rr = [&](int cc) {
-                            const int cr = cc / p.Gr, cl2 = cc - cr * p.Gr;
-                            return p.slots_r[cr] + par_off + static_cast<size_t>(cl2) * kSlotWords + 4;
-                        };
-                        for (int c0 = lane; c0 < G; c0 += 32 * 4) {
-                            unsigned long long h[4], l[4];
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (c0 + 32 * u < G) {
-                                    if (SYS) ld_relaxed_v2_sys(slot_rr(c0 + 32 * u), h[u], l[u]);
-                                    else ld_relaxed_v2_u64(slot_rr(c0 + 32 * u), h[u], l[u]);
-                                }
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (c0 + 32 * u < G)
-                                    t = t + (ll_ok(h[u], l[u], tag) ? ll_val(h[u], l[u]) : ll_load(slot_rr(c0 + 32 * u), tag, SYS));
-                        }
-                        t = lwarp_sum(t);
-                        }
+                        // ||r_k||^2: each rank's CTA partials summed beside its count (arrival
+                        // order); across ranks the ranks' sums in rank order
+                        const double t = __longlong_as_double(static_cast<long long>(rsum));
                         res = bb > 0.0 ? t / bb : t;
                         if (lead && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
                         if (res <= p.tol) stop = CSK_CONVERGED;
