@@ -51,7 +51,7 @@ constexpr int kKeySlotWords = 2 * kMaxRanks * 2 * 2;  // per parity and rank: th
 constexpr size_t kStageFlagOff = static_cast<size_t>(3) * kXchWords * 8 + kKeySlotWords * 8;  // bytes
 constexpr size_t kStageRowOff = kStageFlagOff + 128;
 constexpr size_t kXchBytes = kStageRowOff + static_cast<size_t>(2) * CSK_MAX_N * 8;
-constexpr int kSlotWords = 8;      // LL slot: lambda, score, rr as tagged 32-bit halves + pad
+constexpr int kSlotWords = 8;      // LL slot: lambda, score as tagged 32-bit halves + pad (64 B)
 
 struct LoopParams {
     const double *At;
