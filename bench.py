@@ -367,6 +367,31 @@ def run_ours(args, dist, rank, ws):
             out["per_config"]["C5"] = c5_extra(csk, ctx)
         # the paper's comparison (Table 1 columns): MWRK on the unsketched system
         out["vs_mwrk"] = mwrk_compare(csk, ctx, cfg, p, ms_step, it)
+        out["stop_modes"] = stop_modes(csk, ctx, cfg, p)
+    return out
+
+
+def stop_modes(csk, ctx, cfg, p, cap=300):
+    """The loop's cost per iteration in both stop rules on this config's sketch: RES on the
+    iterate error (x* known; the timed step) and the residual stop (x* unknown, S:279:
+    ||b~ - A~ x_k||^2 / ||b~||^2 formed in the same pass), each capped at `cap` iterations."""
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed, ctx=ctx)
+    x = torch.zeros(cfg.n, dtype=torch.float64, device="cuda")
+    out = {"capped_at": cap}
+    for name, xs in (("x_star", p.x_star), ("residual", None)):
+        best = None
+        for _ in range(3):
+            x.zero_()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            csk.csk_solve_async(At, bt, nsq, x, x_star=xs, tol=1e-30, max_iters=cap, ctx=ctx)
+            ev[1].record()
+            rep = csk.csk_solve_wait(ctx)
+            torch.cuda.synchronize()
+            us = ev[0].elapsed_time(ev[1]) * 1e3 / max(rep.iterations, 1)
+            best = us if best is None else min(best, us)
+        out[name + "_us_per_iteration"] = round(best, 3)
+    del At, bt, nsq
     return out
 
 
