@@ -170,6 +170,12 @@ def _ncu_traffic(name: str):
         return None
 
 
+def _config_dict(cfg) -> dict:
+    """The workload as both arms name it (same keys in the reference line: same_config)."""
+    return {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "kind": cfg.kind, "tol": cfg.tol,
+            "max_iters": cfg.max_iters, "sketch_seed": cfg.sketch_seed, "gen_seed": cfg.gen_seed}
+
+
 def alg_bytes_sketch(cfg) -> int:
     """8mn + 8m + 8dn + 8d (A, b read; A~, b~ written) + 8d (nsq)."""
     return 8 * cfg.m * cfg.n + 8 * cfg.m + 8 * cfg.d * cfg.n + 16 * cfg.d
@@ -244,9 +250,10 @@ def run_ours(args, dist, rank, ws):
     sk = [e[0].elapsed_time(e[1]) for e in evs]
     sv = [e[1].elapsed_time(e[2]) for e in evs]
     tot = [a + b for a, b in zip(sk, sv)]
-    ms_step = _max_over_ranks(dist, sum(tot) / len(tot))
-    sk_ms = sum(sk) / len(sk)
-    sv_ms = sum(sv) / len(sv)
+    # median of the K timed steps; the mean and spread are reported beside it
+    ms_step = _max_over_ranks(dist, statistics.median(tot))
+    sk_ms = statistics.median(sk)
+    sv_ms = statistics.median(sv)
     it = reps[-1].iterations
     assert all(r.iterations == it for r in reps), "non-deterministic iteration count"
 
@@ -254,8 +261,8 @@ def run_ours(args, dist, rank, ws):
     # C1-C3; registers + TMEM + shared memory at C4).  north_star frames it as the bytes of A~
     # per iteration over the on-chip (SMEM/L2) bandwidth; the FP64 FMA bound is reported beside.
     loop_bytes = alg_bytes_iter(cfg) * it
-    k_loop_ms = sum(kern_ms["loop"]) / len(kern_ms["loop"])
-    k_sketch_ms = sum(kern_ms["sketch"]) / len(kern_ms["sketch"])
+    k_loop_ms = statistics.median(kern_ms["loop"])
+    k_sketch_ms = statistics.median(kern_ms["sketch"])
     loop_gbs = loop_bytes / (k_loop_ms * 1e-3) / 1e9
     smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
     loop_tflops = 2.0 * cfg.d * cfg.n * it / (k_loop_ms * 1e-3) / 1e12
@@ -275,11 +282,11 @@ def run_ours(args, dist, rank, ws):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (torch Philox, PAPER.md:180 recipe; csk_synth.py)",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "kind": cfg.kind,
-                   "tol": cfg.tol, "max_iters": cfg.max_iters, "sketch_seed": cfg.sketch_seed,
-                   "per_rank": "independent problem per rank" if ws > 1 else "single problem",
-                   "l2": ("flushed between steps (256 MiB write, untimed)" if do_flush else
-                          "input larger than L2 (A = %.0f MB > %.0f MB L2): no flush" % (cfg.bytes_A / 1e6, l2_bytes / 1e6))},
+        "config": dict(_config_dict(cfg),
+                       l2=("flushed between steps (256 MiB write, untimed)" if do_flush else
+                           "input larger than L2 (A = %.0f MB > %.0f MB L2): no flush" % (cfg.bytes_A / 1e6, l2_bytes / 1e6))),
+        "timing": {"statistic": "median of the K timed steps", "mean_ms": round(sum(tot) / len(tot), 4),
+                   "min_ms": round(min(tot), 4), "max_ms": round(max(tot), 4)},
         "iterations": it,
         "final_res": reps[-1].final_res,
         "termination": ["converged", "max_iters", "stagnated"][reps[-1].termination],
@@ -365,6 +372,8 @@ def run_ours(args, dist, rank, ws):
         out["per_config"] = extras(csk, ctx, [c for c in ("C1", "C2", "C4") if c != cfg.name], flush)
         if cfg.name != "C5":
             out["per_config"]["C5"] = c5_extra(csk, ctx)
+        if not args.no_uncapped:
+            out["per_config"]["C4_uncapped"] = c4_uncapped(csk, ctx)
         # the paper's comparison (Table 1 columns): MWRK on the unsketched system
         out["vs_mwrk"] = mwrk_compare(csk, ctx, cfg, p, ms_step, it)
         out["stop_modes"] = stop_modes(csk, ctx, cfg, p)
@@ -395,10 +404,10 @@ def stop_modes(csk, ctx, cfg, p, cap=300):
     return out
 
 
-def c5_extra(csk, ctx, cap=400):
+def c5_extra(csk, ctx, cap=None):
     """C5 on one GPU (CSR input; A~ = 40000 x 2000 = 640 MB, far above on-chip capacity): the CSR
-    sketch, and the loop for a capped number of iterations -- per-iteration time and the HBM
-    rate of the rows it streams (through the TMA ring) every iteration."""
+    sketch, and the loop to RES <= 1e-6 (the metric; ~2.6k iterations) -- time to 1e-6,
+    per-iteration time and the HBM rate of the rows it streams (TMA ring) every iteration."""
     cfg = CONFIGS["C5"]
     p = make_config(cfg, "cuda")
     d, n = cfg.d, cfg.n
@@ -410,7 +419,7 @@ def c5_extra(csk, ctx, cap=400):
         e[0].record()
         At, bt, nsq = csk.csk_sketch_csr(p.row_ptr, p.col, p.val, p.b, n, d, seed=cfg.sketch_seed, ctx=ctx)
         e[1].record()
-        csk.csk_solve_async(At, bt, nsq, x, x_star=p.x_star, tol=cfg.tol, max_iters=cap, ctx=ctx)
+        csk.csk_solve_async(At, bt, nsq, x, x_star=p.x_star, tol=cfg.tol, max_iters=cap or cfg.max_iters, ctx=ctx)
         e[2].record()
         rep = csk.csk_solve_wait(ctx)
         torch.cuda.synchronize()
@@ -427,13 +436,42 @@ def c5_extra(csk, ctx, cap=400):
     gbs = 8.0 * n * streamed_rows / (us_it * 1e-6) / 1e9
     peak = _peaks()[0]
     nnz = int(p.row_ptr[-1].item())
-    return {"sketch_ms": round(sk, 4), "sketch_bytes": 12 * nnz + 8 * cfg.m * 2 + 8 * d * n,
-            "iterations": rep.iterations, "termination": ["converged", "max_iters", "stagnated"][rep.termination],
-            "capped_at": cap, "us_per_iteration": round(us_it, 3), "tiers": t,
+    sk_bytes = 12 * nnz + 8 * (cfg.m + 1) + 8 * cfg.m + 8 * d * n + 16 * d
+    return {"ms_per_step": round(sk + sv, 4), "sketch_ms": round(sk, 4), "solve_ms": round(sv, 4),
+            "sketch_bytes": sk_bytes, "sketch_hbm_gbs": round(sk_bytes / (sk * 1e-3) / 1e9, 1),
+            "sketch_hbm_frac_with_plan": round(sk_bytes / (sk * 1e-3) / 1e9 / peak, 4),
+            "iterations": rep.iterations, "final_res": rep.final_res,
+            "termination": ["converged", "max_iters", "stagnated"][rep.termination],
+            "us_per_iteration": round(us_it, 3), "tiers": t,
             "streamed_rows_per_iteration": streamed_rows,
             "loop_streamed_hbm_gbs": round(gbs, 1), "loop_streamed_hbm_frac": round(gbs / peak, 4),
-            "note": "loop capped (time per iteration, not time to 1e-6); rows past the on-chip tiers are "
+            "note": "time to RES <= 1e-6 on one GPU (second of two runs); rows past the on-chip tiers are "
                     "re-read from HBM every iteration through the TMA stream ring"}
+
+
+def c4_uncapped(csk, ctx, cap=2_000_000):
+    """C4 without the 50k cap: the loop run to RES <= 1e-6 (~7e5 iterations), once."""
+    cfg = CONFIGS["C4"]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed, ctx=ctx)
+    xs = p.x_star
+    del p
+    torch.cuda.empty_cache()
+    x = torch.zeros(cfg.n, dtype=torch.float64, device="cuda")
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    csk.csk_solve_async(At, bt, nsq, x, x_star=xs, tol=cfg.tol, max_iters=cap, ctx=ctx)
+    e[1].record()
+    rep = csk.csk_solve_wait(ctx)
+    torch.cuda.synchronize()
+    ms = e[0].elapsed_time(e[1])
+    del At, bt, nsq
+    torch.cuda.empty_cache()
+    return {"loop_ms": round(ms, 2), "iterations": rep.iterations, "final_res": rep.final_res,
+            "termination": ["converged", "max_iters", "stagnated"][rep.termination],
+            "us_per_iteration": round(ms * 1e3 / max(rep.iterations, 1), 3), "cap": cap,
+            "note": "C4 loop without the configs' 50k cap, to RES <= 1e-6 (one run; the sketch is in "
+                    "per_config.C4.sketch_ms)"}
 
 
 def mwrk_compare(csk, ctx, cfg, p, csk_ms, csk_it):
@@ -528,51 +566,96 @@ def _oracle_sample(cfg, A, b, xs, budget_s=20.0):
     return t_sketch, t_loop, per_it, r, complete
 
 
+def _host_info(core):
+    """CPU model, logical CPU count and the pinned core's frequency governor."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    gov = None
+    try:
+        gov = open(f"/sys/devices/system/cpu/cpu{core}/cpufreq/scaling_governor").read().strip()
+    except OSError:
+        gov = "unavailable"
+    return {"cpu_model": model, "nproc": os.cpu_count(), "pinned_core": core, "governor": gov}
+
+
+class _PinnedCore:
+    """Pin the calling thread (the oracle runs in it, through ctypes) to one core for the timing."""
+
+    def __enter__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.core = sorted(self.prev)[-1]
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.prev)
+
+
+def _oracle_timed(cfg, A, b, xs, runs=3, warmup=1, budget_s=20.0):
+    """Median over `runs` pinned single-core oracle samples (after `warmup` untimed ones)."""
+    with _PinnedCore() as pc:
+        for _ in range(warmup):
+            _oracle_sample(cfg, A, b, xs, budget_s=min(budget_s, 5.0))
+        samples = [_oracle_sample(cfg, A, b, xs, budget_s=budget_s) for _ in range(runs)]
+        info = _host_info(pc.core)
+    vals = []
+    for t_sketch, t_loop, per_it, r, complete in samples:
+        vals.append((t_sketch + (t_loop if complete else per_it * cfg.max_iters)) * 1e3)
+    med = statistics.median(vals)
+    t_sketch, t_loop, per_it, r, complete = samples[vals.index(sorted(vals)[len(vals) // 2])]
+    if complete:
+        sample = f"whole {cfg.name} solve (sketch + {r.iterations} iterations), median of {runs} pinned runs"
+    else:
+        sample = (f"{cfg.name}: sketch + {r.iterations} iterations timed, loop extrapolated "
+                  f"to {cfg.max_iters} at {per_it * 1e3:.2f} ms/iteration, median of {runs} pinned runs")
+    return {"value": round(med, 3), "unit": "ms", "cores": 1, "kind": "oracle", "sample": sample,
+            "runs_ms": [round(v, 3) for v in vals], "iterations": r.iterations,
+            "sketch_ms": round(t_sketch * 1e3, 3), "loop_ms_per_iteration": round(per_it * 1e3, 4),
+            "host": info}
+
+
 def cpu_baseline(cfg, p):
+    """The oracle on one pinned host core, on the same bytes as the GPU run (D2H copies)."""
+    if cfg.kind == "csr":
+        return {"value": None, "unit": "ms", "cores": 1, "kind": "oracle",
+                "sample": "not timed for the CSR config in the default run"}
     A = p.A.cpu().numpy()
     b = p.b.cpu().numpy()
     xs = p.x_star.cpu().numpy()
-    t_sketch, t_loop, per_it, r, complete = _oracle_sample(cfg, A, b, xs)
-    if complete:
-        val = (t_sketch + t_loop) * 1e3
-        sample = f"whole {cfg.name} solve (sketch + {r.iterations} iterations)"
-    else:
-        val = (t_sketch + per_it * cfg.max_iters) * 1e3
-        sample = (f"{cfg.name}: sketch + {r.iterations} iterations timed, loop extrapolated "
-                  f"to {cfg.max_iters} at {per_it * 1e3:.2f} ms/iteration")
-    return {"value": round(val, 3), "unit": "ms", "cores": 1, "kind": "oracle", "sample": sample,
-            "iterations": r.iterations, "sketch_ms": round(t_sketch * 1e3, 3),
-            "loop_ms_per_iteration": round(per_it * 1e3, 4)}
+    return _oracle_timed(cfg, A, b, xs)
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (plain C, 1 thread) on our arm's config/metric."""
+    """--impl reference: the CPU oracle (plain C, 1 thread, pinned) on our arm's config/metric, on
+    the SAME bytes our arm solves: the problem is drawn with the same torch Philox stream on the
+    GPU (as our arm does) and copied to the host; only without a GPU is it drawn on the CPU."""
     import oracle
     cfg = CONFIGS[args.config]
-    p = make_config(cfg, "cpu")
-    A, b, xs = p.A.numpy(), p.b.numpy(), p.x_star.numpy()
+    on_gpu = torch.cuda.is_available()
+    p = make_config(cfg, "cuda" if on_gpu else "cpu")
+    A, b, xs = p.A.cpu().numpy(), p.b.cpu().numpy(), p.x_star.cpu().numpy()
+    del p
     oracle.build()
-    for _ in range(args.warmup):
-        _oracle_sample(cfg, A, b, xs, budget_s=5.0)
-    times = []
-    last = None
-    for _ in range(args.steps):
-        t_sketch, t_loop, per_it, r, complete = _oracle_sample(cfg, A, b, xs, budget_s=20.0)
-        times.append((t_sketch + (t_loop if complete else per_it * cfg.max_iters)) * 1e3)
-        last = (r, complete, per_it)
-    v = sum(times) / len(times)
-    r, complete, per_it = last
-    sample = (f"whole {cfg.name} solve ({r.iterations} iterations)" if complete else
-              f"{cfg.name}: {r.iterations} iterations timed, extrapolated to {cfg.max_iters}")
-    return {"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3),
+    runs = max(3, min(args.steps, 5))
+    cb = _oracle_timed(cfg, A, b, xs, runs=runs, warmup=1)
+    v = cb["value"]
+    return {"metric": METRIC, "value": v, "unit": "ms", "n_gpus": 0,
+            "steps": runs, "warmup": 1, "ms_per_step": v,
             "higher_is_better": False, "impl": "reference", "dtype": "f64",
-            "data": "synthetic (torch Philox CPU stream, csk_synth.py)",
-            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d},
-            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": 1, "kind": "oracle",
-                             "sample": sample},
-            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "iterations": r.iterations, "vs_baseline": None}
+            "data": ("synthetic (torch Philox on the GPU, copied to the host: the same bytes as our arm; csk_synth.py)"
+                     if on_gpu else "synthetic (torch Philox CPU stream; no GPU here, csk_synth.py)"),
+            "config": _config_dict(cfg),
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "iterations": cb["iterations"], "vs_baseline": None,
+            "note": f"each step = one pinned single-core oracle sample (median of {runs}); "
+                    "--steps K is clamped to 3..5 samples so the arm finishes in about a minute"}
 
 
 def _sharded_roofline(dist, cfg, ws, it, kloop, ksk):
@@ -725,6 +808,7 @@ def main():
                     help="run the sharded (S9/S10) path even at N = 1 (a 1-rank NCCL communicator; tests the N > 1 code path)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-uncapped", action="store_true", help="skip the uncapped C4 run (~4 s)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
@@ -734,7 +818,17 @@ def main():
             return
         print(json.dumps(run_reference(args)))
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver's own launch sets
+        # WORLD_SIZE and lands below directly)
+        import random
+        port = str(29500 + random.randrange(1000))
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", port, os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     dist, rank, ws, _ = _dist(force=args.sharded)
+    if ws != args.gpus and not (args.sharded and ws == 1):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} ranks were launched")
     out = run_ours(args, dist, rank, ws) if ws == 1 and not args.sharded else run_sharded(args, dist, rank, ws)
     if rank == 0:
         print(json.dumps(out))

@@ -44,7 +44,7 @@ extern "C" {
 #define CSK_API
 #endif
 
-#define CSK_ABI_VERSION 1
+#define CSK_ABI_VERSION 2
 #define CSK_MAX_N 2048 /* solve keeps x in registers: 64 columns per lane-pair group */
 
 typedef enum {
@@ -79,7 +79,7 @@ typedef struct {
 
 /* Optional knobs and debug traces for csk_solve_ex.  Zero-initialise for defaults. */
 #define CSK_SOLVE_ASYNC 1  /* opts->flags: return right after the launch; csk_solve_wait fills the report */
-#define CSK_SOLVE_LEGACY 2 /* opts->flags: the round-1 cluster/DSMEM kernel (shared-memory rows; A/B only) */
+#define CSK_SOLVE_LEGACY 2 /* removed in ABI 2 (the round-1 kernel left the library): CSK_E_UNSUPPORTED */
 #define CSK_SOLVE_NO_TMEM 4    /* opts->flags: never keep A~ rows in tensor memory */
 #define CSK_SOLVE_FORCE_TMEM 8 /* opts->flags: use the TMEM row tier whenever the layout allows (tests) */
 #define CSK_SOLVE_NO_STREAM_RING 16 /* opts->flags: rows that do not fit on chip are re-read with plain loads
@@ -95,11 +95,19 @@ typedef struct {
     int64_t *idx_trace;    /* device int64[trace_cap]: i_k, or NULL */
     double *res_trace;     /* device double[trace_cap]: stop quantity at x_k, or NULL */
     double *x_trace;       /* device double[trace_cap * n]: x_k row by row, or NULL */
-    int64_t *phase_cycles; /* debug (CSK_SOLVE_LEGACY only): device int64[16] per-phase SM-cycle totals */
+    int64_t *phase_cycles; /* debug (libcsk_prof.so only): device int64[32] per-phase SM-cycle totals */
     int32_t reg_rows;      /* rows of A~ per row group kept in registers: 0 = auto (max), -1 = none,
                               k > 0 = at most k (the default kernel; smem_rows then counts rows per
                               row group kept in shared memory, the rest re-read from L2/HBM) */
     int32_t group_warps;   /* warps per row group (1, 2, 4, 8): 0 = auto (fewest with n <= 512 x warps) */
+    /* ABI 2: the residual vector of the first r_trace_cap iterations (north_star "per-iteration
+     * residuals within 1e-10 relative given the same x_k"; the numerator r_k = b~ - A~ x_k of
+     * Algorithm 1's selection rule).  r_trace[k * d + i] = r_k[i] for every row i and
+     * k < min(r_trace_cap, IT + 1) (the residual at the returned iterate x_IT is formed too: the
+     * GEMV of iteration k runs before its stop test).  Written by the kernel's finalize: the very
+     * values it scores.  Device double[r_trace_cap * d] or NULL (then no cost: one uniform branch). */
+    double *r_trace;
+    int64_t r_trace_cap;
 } csk_solve_opts_t;
 
 typedef struct csk_ctx_s *csk_ctx_t;
@@ -273,6 +281,14 @@ CSK_API csk_status_t csk_solve_virtual_ranks(csk_ctx_t ctx, const double *A_tild
                                              int64_t n, int32_t nranks, double *x,
                                              const double *x_star, double tol, int64_t max_iters,
                                              double *x_copies, csk_report_t *report, void *stream);
+/* Same with the csk_solve_opts_t traces (idx/res/x traces of virtual rank 0, r_trace indexed by
+ * GLOBAL row: every virtual rank writes its own rows).  Launch knobs in opts are ignored. */
+CSK_API csk_status_t csk_solve_virtual_ranks_ex(csk_ctx_t ctx, const double *A_tilde,
+                                                const double *b_tilde, const double *nsq, int64_t d,
+                                                int64_t n, int32_t nranks, double *x,
+                                                const double *x_star, double tol, int64_t max_iters,
+                                                double *x_copies, const csk_solve_opts_t *opts,
+                                                csk_report_t *report, void *stream);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,6 @@ CONVERGED, MAX_ITERS, STAGNATED = 0, 1, 2
 STOP_RES, STOP_RESIDUAL = 0, 1
 MAX_N = 2048
 SOLVE_ASYNC = 1
-SOLVE_LEGACY = 2
 SOLVE_NO_TMEM = 4
 SOLVE_FORCE_TMEM = 8
 SOLVE_NO_STREAM_RING = 16
@@ -61,7 +60,8 @@ class SolveOpts(ctypes.Structure):
                 ("trace_cap", ctypes.c_int64), ("idx_trace", ctypes.c_void_p),
                 ("res_trace", ctypes.c_void_p), ("x_trace", ctypes.c_void_p),
                 ("phase_cycles", ctypes.c_void_p), ("reg_rows", ctypes.c_int32),
-                ("group_warps", ctypes.c_int32)]
+                ("group_warps", ctypes.c_int32), ("r_trace", ctypes.c_void_p),
+                ("r_trace_cap", ctypes.c_int64)]
 
 
 def _load():
@@ -115,6 +115,8 @@ def _extend_sharded(lib):
         "csk_sketch_sharded": ([P, P, i64, P, i64, i64, i64, i64, i64, u64, P, P, P, pi64, pi64, P], i32),
         "csk_solve_sharded": ([P, P, P, P, i64, i64, i64, i64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
         "csk_solve_virtual_ranks": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P, ctypes.POINTER(Report), P], i32),
+        "csk_solve_virtual_ranks_ex": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P, ctypes.POINTER(SolveOpts),
+                                        ctypes.POINTER(Report), P], i32),
     }
     for name, (args, res) in extra.items():
         fn = getattr(lib, name)
@@ -281,14 +283,49 @@ class SolveResult:
     idx_trace: torch.Tensor | None = None
     res_trace: torch.Tensor | None = None
     x_trace: torch.Tensor | None = None
+    r_trace: torch.Tensor | None = None
+
+
+def _trace_opts(opts, d: int, n: int, device, trace: int, trace_x: bool, trace_r: int):
+    """Device trace buffers (NaN / -1 filled) wired into a SolveOpts."""
+    idx_t = res_t = x_t = r_t = None
+    if trace:
+        idx_t = torch.full((trace,), -1, dtype=torch.int64, device=device)
+        res_t = torch.full((trace,), float("nan"), dtype=torch.float64, device=device)
+        if trace_x:
+            x_t = torch.full((trace, n), float("nan"), dtype=torch.float64, device=device)
+        opts.trace_cap = trace
+        opts.idx_trace = idx_t.data_ptr()
+        opts.res_trace = res_t.data_ptr()
+        opts.x_trace = None if x_t is None else x_t.data_ptr()
+    if trace_r:
+        r_t = torch.full((trace_r, d), float("nan"), dtype=torch.float64, device=device)
+        opts.r_trace = r_t.data_ptr()
+        opts.r_trace_cap = trace_r
+    return idx_t, res_t, x_t, r_t
+
+
+def _result(x, rep, traces, trace: int, trace_r: int) -> "SolveResult":
+    idx_t, res_t, x_t, r_t = traces
+    k = rep.iterations
+    return SolveResult(x=x, iterations=k, final_res=rep.final_res, termination=rep.termination,
+                       stop_mode=rep.stop_mode, last_index=rep.last_index,
+                       idx_trace=None if idx_t is None else idx_t[:min(k, trace)],
+                       res_trace=None if res_t is None else res_t[:min(k + 1, trace)],
+                       x_trace=None if x_t is None else x_t[:min(k + 1, trace)],
+                       r_trace=None if r_t is None else r_t[:min(k + 1, trace_r)])
 
 
 def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
               num_ctas: int = 0, smem_rows: int = 0, cluster_size: int = 0, trace: int = 0,
               trace_x: bool = False, phase_cycles: torch.Tensor | None = None,
-              reg_rows: int = 0, group_warps: int = 0, legacy: bool = False, tmem: bool | None = None,
-              stream_ring: bool = True, ctx: Context | None = None) -> SolveResult:
-    """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel."""
+              reg_rows: int = 0, group_warps: int = 0, tmem: bool | None = None,
+              stream_ring: bool = True, trace_r: int = 0, ctx: Context | None = None) -> SolveResult:
+    """Algorithm 1 loop with the P:180 stopping rule, one persistent kernel.
+
+    ``trace`` records i_k and the stop quantity (and x_k with ``trace_x``) for the first ``trace``
+    iterations; ``trace_r`` records the whole residual vector r_k = b~ - A~ x_k (the values the
+    kernel scores) for the first ``trace_r`` iterations (``r_trace``: trace_r x d)."""
     ctx = ctx or default_context()
     _need(At, torch.float64, "A_tilde", 2)
     _need(bt, torch.float64, "b_tilde", 1)
@@ -303,30 +340,16 @@ def csk_solve(At, bt, nsq, x0=None, x_star=None, tol: float = 1e-6, max_iters: i
     opts.cluster_size = cluster_size
     opts.reg_rows = reg_rows
     opts.group_warps = group_warps
-    opts.flags = ((SOLVE_LEGACY if legacy else 0) | (SOLVE_NO_TMEM if tmem is False else 0)
-                  | (SOLVE_FORCE_TMEM if tmem is True else 0) | (0 if stream_ring else SOLVE_NO_STREAM_RING))
-    idx_t = res_t = x_t = None
-    if trace:
-        idx_t = torch.full((trace,), -1, dtype=torch.int64, device=At.device)
-        res_t = torch.full((trace,), float("nan"), dtype=torch.float64, device=At.device)
-        if trace_x:
-            x_t = torch.full((trace, n), float("nan"), dtype=torch.float64, device=At.device)
-        opts.trace_cap = trace
-        opts.idx_trace = idx_t.data_ptr()
-        opts.res_trace = res_t.data_ptr()
-        opts.x_trace = None if x_t is None else x_t.data_ptr()
+    opts.flags = ((SOLVE_NO_TMEM if tmem is False else 0) | (SOLVE_FORCE_TMEM if tmem is True else 0)
+                  | (0 if stream_ring else SOLVE_NO_STREAM_RING))
+    traces = _trace_opts(opts, d, n, At.device, trace, trace_x, trace_r)
     if phase_cycles is not None:
         opts.phase_cycles = phase_cycles.data_ptr()
     rep = Report()
     ctx.check(lib.csk_solve_ex(ctx.handle, _ptr(At), _ptr(bt.contiguous()), _ptr(nsq.contiguous()),
                                d, n, _ptr(x), _ptr(xs), float(tol), int(max_iters),
                                ctypes.byref(opts), ctypes.byref(rep), _stream()))
-    k = rep.iterations
-    return SolveResult(x=x, iterations=k, final_res=rep.final_res, termination=rep.termination,
-                       stop_mode=rep.stop_mode, last_index=rep.last_index,
-                       idx_trace=None if idx_t is None else idx_t[:min(k, trace)],
-                       res_trace=None if res_t is None else res_t[:min(k + 1, trace)],
-                       x_trace=None if x_t is None else x_t[:min(k + 1, trace)])
+    return _result(x, rep, traces, trace, trace_r)
 
 
 def csk_solve_async(At, bt, nsq, x, x_star=None, tol: float = 1e-6, max_iters: int = 50_000,
@@ -335,7 +358,19 @@ def csk_solve_async(At, bt, nsq, x, x_star=None, tol: float = 1e-6, max_iters: i
     """Launch the loop without waiting (CSK_SOLVE_ASYNC); x (in/out) is updated in place.
     Call ``csk_solve_wait(ctx)`` for the report."""
     ctx = ctx or default_context()
+    # the same checks as csk_solve; x is updated in place, so it must be a contiguous fp64 CUDA tensor
+    _need(At, torch.float64, "A_tilde", 2)
+    _need(bt, torch.float64, "b_tilde", 1)
+    _need(nsq, torch.float64, "nsq", 1)
+    _need(x, torch.float64, "x", 1)
+    if x_star is not None:
+        _need(x_star, torch.float64, "x_star", 1)
+    for t, nm in ((At, "A_tilde"), (bt, "b_tilde"), (nsq, "nsq"), (x, "x"), (x_star, "x_star")):
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"{nm} must be contiguous (csk_solve_async passes raw pointers)")
     d, n = At.shape
+    if bt.shape[0] != d or nsq.shape[0] != d or x.shape[0] != n or (x_star is not None and x_star.shape[0] != n):
+        raise ValueError("csk_solve_async: shape mismatch")
     opts = SolveOpts()
     opts.num_ctas = num_ctas
     opts.smem_rows = smem_rows
@@ -482,15 +517,24 @@ def csk_solve_sharded(At_local, bt_local, nsq_local, d_lo: int, d_hi: int, d: in
 
 
 def csk_solve_virtual_ranks(At, bt, nsq, nranks: int, x0=None, x_star=None, tol: float = 1e-6,
-                            max_iters: int = 50_000, ctx: Context | None = None):
-    """The sharded loop with `nranks` virtual ranks on this GPU (loopback exchange)."""
+                            max_iters: int = 50_000, trace: int = 0, trace_x: bool = False, trace_r: int = 0,
+                            ctx: Context | None = None):
+    """The sharded loop with `nranks` virtual ranks on this GPU (loopback exchange).
+
+    Returns (x, copies, report), or (x, copies, report, SolveResult with the traces) when any
+    trace is requested (virtual rank 0's i_k / RES / x_k; r_k of every rank by global row)."""
     ctx = ctx or default_context()
+    _need(At, torch.float64, "A_tilde", 2)
     At = At.contiguous()
     d, n = At.shape
     x = torch.zeros(n, dtype=torch.float64, device=At.device) if x0 is None else x0.clone().contiguous()
     copies = torch.empty(nranks, n, dtype=torch.float64, device=At.device)
     rep = Report()
-    ctx.check(lib.csk_solve_virtual_ranks(ctx.handle, _ptr(At), _ptr(bt.contiguous()), _ptr(nsq.contiguous()),
-                                          d, n, nranks, _ptr(x), _ptr(x_star), float(tol), int(max_iters),
-                                          _ptr(copies), ctypes.byref(rep), _stream()))
+    opts = SolveOpts()
+    traces = _trace_opts(opts, d, n, At.device, trace, trace_x, trace_r)
+    ctx.check(lib.csk_solve_virtual_ranks_ex(ctx.handle, _ptr(At), _ptr(bt.contiguous()), _ptr(nsq.contiguous()),
+                                             d, n, nranks, _ptr(x), _ptr(x_star), float(tol), int(max_iters),
+                                             _ptr(copies), ctypes.byref(opts), ctypes.byref(rep), _stream()))
+    if trace or trace_r:
+        return x, copies, rep, _result(x, rep, traces, trace, trace_r)
     return x, copies, rep

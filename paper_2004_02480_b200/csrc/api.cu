@@ -1,5 +1,5 @@
 // api.cu -- the C ABI of include/csk.h: argument validation, workspaces, dispatch.
-// Every compute step runs in the kernels of plan.cu / sketch.cu / solve.cu; this file
+// Every compute step runs in the kernels of plan.cu / sketch.cu / loop.cu; this file
 // only checks arguments (SURVEY.md §8(b) error table) and sequences launches.
 #include <stdio.h>
 #include <stdlib.h>
@@ -110,6 +110,57 @@ static csk_status_t check_dense(csk_ctx_t ctx, const char *fn, const double *A, 
         snprintf(buf, sizeof buf, "%s: need lda >= n, A 8-byte and A~ 16-byte aligned", fn);
         return fail(ctx, CSK_E_ARG, buf);
     }
+    return CSK_OK;
+}
+
+// csk_solve / csk_solve_ex: argument checks (SURVEY.md §8(b) error table), then the persistent
+// loop kernel of loop.cu.
+csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq,
+                       int64_t d, int64_t n, double *x, const double *x_star, double tol,
+                       int64_t max_iters, const csk_solve_opts_t *opts, csk_report_t *report,
+                       cudaStream_t stream) {
+    if (d < 1 || n < 1 || !At || !bt || !nsq || !x || !(tol > 0.0) || max_iters < 0 ||
+        (!report && !(opts && (opts->flags & CSK_SOLVE_ASYNC))))
+        return fail(ctx, CSK_E_ARG, "csk_solve: need d, n >= 1, non-null A~, b~, nsq, x, report, tol > 0, max_iters >= 0");
+    if (d >= (int64_t(1) << 31) - 1) return fail(ctx, CSK_E_ARG, "csk_solve: d >= 2^31");
+    if (n > CSK_MAX_N) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n > CSK_MAX_N");
+    if ((n % 2 == 0) && !aligned16(At)) return fail(ctx, CSK_E_ARG, "csk_solve: A~ not 16-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(At) | reinterpret_cast<uintptr_t>(bt) | reinterpret_cast<uintptr_t>(nsq) |
+         reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(x_star)) & 7)
+        return fail(ctx, CSK_E_ARG, "csk_solve: fp64 arrays must be 8-byte aligned");
+    if (opts && (opts->flags & CSK_SOLVE_LEGACY))
+        return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: CSK_SOLVE_LEGACY was removed in ABI 2");
+    if (opts && opts->r_trace_cap < 0) return fail(ctx, CSK_E_ARG, "csk_solve: r_trace_cap < 0");
+    if (ctx->pending) return fail(ctx, CSK_E_ARG, "csk_solve: a CSK_SOLVE_ASYNC solve is still in flight (call csk_solve_wait)");
+    return run_loop(ctx, At, bt, nsq, d, n, x, x_star, tol, max_iters, opts, report, stream);
+}
+
+csk_status_t ensure_host_report(csk_ctx_t ctx) {
+    if (ctx->report_host) return CSK_OK;
+    cudaError_t e = cudaMallocHost(&ctx->report_host, 8 * sizeof(int64_t));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMallocHost(report)");
+    return CSK_OK;
+}
+
+// The loop kernel's report: [0] iterations, [1] final stop quantity (bits), [2] termination
+// (-2 every row masked, -3 exchange watchdog), [3] last index.
+csk_status_t finish_solve(csk_ctx_t ctx, csk_report_t *report) {
+    if (!ctx->pending) return fail(ctx, CSK_E_ARG, "csk_solve_wait: no solve in flight");
+    ctx->pending = false;
+    CSK_CUDA(ctx, cudaStreamSynchronize(ctx->pending_stream));
+    const int64_t *rep = ctx->report_host;
+    if (rep[2] == -2) return fail(ctx, CSK_E_ZERO_SKETCH, "csk_solve: every row of A~ is zero");
+    if (rep[2] == -3)
+        return fail(ctx, CSK_E_CUDA, "csk_solve: exchange watchdog -- not every CTA / rank arrived within "
+                                     "CSK_EXCHANGE_TIMEOUT_S (default 30 s)");
+    if (!report) return CSK_OK;
+    report->iterations = rep[0];
+    double fr;
+    memcpy(&fr, &rep[1], sizeof(double));
+    report->final_res = fr;
+    report->termination = static_cast<int32_t>(rep[2]);
+    report->stop_mode = ctx->pending_resmode ? CSK_STOP_RESIDUAL : CSK_STOP_RES;
+    report->last_index = rep[3];
     return CSK_OK;
 }
 

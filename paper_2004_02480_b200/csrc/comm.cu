@@ -732,6 +732,15 @@ csk_status_t csk_solve_virtual_ranks(csk_ctx_t ctx, const double *A_tilde, const
                                      const double *nsq, int64_t d, int64_t n, int32_t nranks, double *x,
                                      const double *x_star, double tol, int64_t max_iters,
                                      double *x_copies, csk_report_t *report, void *stream) {
+    return csk_solve_virtual_ranks_ex(ctx, A_tilde, b_tilde, nsq, d, n, nranks, x, x_star, tol, max_iters,
+                                      x_copies, nullptr, report, stream);
+}
+
+csk_status_t csk_solve_virtual_ranks_ex(csk_ctx_t ctx, const double *A_tilde, const double *b_tilde,
+                                        const double *nsq, int64_t d, int64_t n, int32_t nranks, double *x,
+                                        const double *x_star, double tol, int64_t max_iters,
+                                        double *x_copies, const csk_solve_opts_t *opts, csk_report_t *report,
+                                        void *stream) {
     if (!ctx || !A_tilde || !b_tilde || !nsq || !x || !report || nranks < 1 || d < 1 || n < 1 || !(tol > 0.0) ||
         max_iters < 0)
         return ctx ? fail(ctx, CSK_E_ARG, "csk_solve_virtual_ranks: bad arguments") : CSK_E_ARG;
@@ -768,7 +777,18 @@ csk_status_t csk_solve_virtual_ranks(csk_ctx_t ctx, const double *A_tilde, const
     for (int p = 0; p < nranks; ++p)
         if (rs.dlo[p + 1] <= rs.dlo[p])
             return fail(ctx, CSK_E_ARG, "csk_solve_virtual_ranks: a rank owns no rows (d < P)");
-    csk_status_t st = run_loop(ctx, A_tilde, b_tilde, nsq, d, n, x, x_star, tol, max_iters, nullptr, report, s, &rs);
+    // only the traces of opts apply (the geometry is the sharded one)
+    csk_solve_opts_t tr{};
+    if (opts) {
+        tr.trace_cap = opts->trace_cap;
+        tr.idx_trace = opts->idx_trace;
+        tr.res_trace = opts->res_trace;
+        tr.x_trace = opts->x_trace;
+        tr.r_trace = opts->r_trace;
+        tr.r_trace_cap = opts->r_trace_cap;
+    }
+    csk_status_t st = run_loop(ctx, A_tilde, b_tilde, nsq, d, n, x, x_star, tol, max_iters, opts ? &tr : nullptr,
+                               report, s, &rs);
     if (st == CSK_OK) cudaMemcpyAsync(x, copies, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s);
     cudaStreamSynchronize(s);
     if (tmp) cudaFree(tmp);

@@ -116,7 +116,7 @@ csk_status_t launch_row_norms(csk_ctx_t ctx, const double *At, int64_t d, int64_
 // Team size used by the row-norm arithmetic (shared by fused and standalone paths).
 int norm_team_threads(int64_t n);
 
-// ---------------------------------------------------------------- solve (solve.cu)
+// ---------------------------------------------------------------- solve (api.cu -> loop.cu)
 csk_status_t run_solve(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq,
                        int64_t d, int64_t n, double *x, const double *x_star, double tol,
                        int64_t max_iters, const csk_solve_opts_t *opts, csk_report_t *report,

@@ -76,6 +76,9 @@ struct LoopParams {
     int64_t *idx_trace;
     double *res_trace;
     double *x_trace;
+    double *r_trace;          // [r_trace_cap][d_glob]: r_k by GLOBAL row (csk_solve_opts_t), or null
+    int64_t r_trace_cap;
+    int64_t d_glob;           // rows of A~ over all ranks (the r_trace leading dimension)
     int64_t *phase_cycles;    // debug (libcsk_prof.so only): [2 warps][16] SM-cycle totals of CTA 0
     long long *skew;          // debug (libcsk_prof.so only): [64 iterations][2][G] globaltimer ns
     // ---- row sharding over P ranks (S10).  P = 1: one GPU.  rank >= 0: this launch is rank
@@ -644,6 +647,10 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
 
     int64_t k = 0, last = -1;
     int term = -1;
+    // r_k of CTA-local row l (global row r0 + l) into the residual trace (off: one uniform branch)
+    auto rtrace = [&](int l, double ri) {
+        if (p.r_trace != nullptr && k < p.r_trace_cap) p.r_trace[k * p.d_glob + r0 + l] = ri;
+    };
     double res = 0.0;
     uint32_t mphase = 0;
     double lam = 0.0;      // lambda of the pending update x += lam A~^(prow)
@@ -893,6 +900,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
                     const double fb = wg == 0 ? fin_b : fin_b2, fi = wg == 0 ? fin_i : fin_i2;
                     const double ri = fb - dot;
+                    rtrace(l, ri);
                     const double sc = fi > 0.0 ? (ri * ri) * fi : -1.0;
                     if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
                     bk = row_key(sc, r0 + l, b);
@@ -909,6 +917,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
                     const double fb = kFinReg ? fin_b : btl[l], fi = kFinReg ? fin_i : invl[l];
                     const double ri = fb - dot;
+                    rtrace(l, ri);
                     const double sc = fi > 0.0 ? (ri * ri) * fi : -1.0;
                     if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
                     bk = row_key(sc, r0 + l, b);
@@ -921,6 +930,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
                     const double fb2 = TM == 1 ? fin_b2 : btl[l], fi2 = TM == 1 ? fin_i2 : invl[l];
                     const double ri = fb2 - dot;
+                    rtrace(l, ri);
                     const double sc = fi2 > 0.0 ? (ri * ri) * fi2 : -1.0;
                     if (RESMODE) rr2 = __fma_rn(ri, ri, rr2);
                     const unsigned long long kk = row_key(sc, r0 + l, b);
@@ -932,6 +942,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     double dot = dotp[l];
                     for (int w = 1; w < WPG; ++w) dot = dot + dotp[w * RM + l];
                     const double ri = btl[l] - dot;
+                    rtrace(l, ri);
                     const double iv = invl[l];
                     // score r^2/nsq and lambda r/nsq through the precomputed 1/nsq (R-3)
                     const double sc = iv > 0.0 ? (ri * ri) * iv : -1.0;
@@ -1127,10 +1138,12 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             const unsigned long long kq =
                                 static_cast<unsigned long long>(__double_as_longlong(ll_val(a0, a1)));
                             if (kq > mx) mx = kq;
-                            if (RESMODE) {  // the ranks' sums in rank order: every rank adds the same way
-                                const double sq = ll_load(ks + 2 * kMaxRanks * 2, tag, true);
+                            if (RESMODE && !timed_out) {  // the ranks' sums in rank order: every rank adds the same way
+                                do {
+                                    ld_relaxed_v2_sys(ks + 2 * kMaxRanks * 2, a0, a1);
+                                } while (!ll_ok(a0, a1, tag) && !watchdog());
                                 rsum = static_cast<unsigned long long>(__double_as_longlong(
-                                    __longlong_as_double(static_cast<long long>(rsum)) + sq));
+                                    __longlong_as_double(static_cast<long long>(rsum)) + ll_val(a0, a1)));
                             }
                         }
                         timed_out = __any_sync(0xffffffffu, timed_out);
@@ -1200,9 +1213,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         }
                     }
                     LP(9)
-                    if (RESMODE) {
+                    if (RESMODE && stop == -1) {  // (not after a watchdog timeout: stop = -3 stands)
                         // ||r_k||^2: each rank's CTA partials summed beside its count (arrival
-                        // order); across ranks the ranks' sums in rank order
+                        // order); across ranks the ranks' sums in rank order.  The 32-byte poll
+                        // reads {count, max, sum} from one L2 sector in one access (a hardware
+                        // property relied on here, not a PTX guarantee: the count reaching G comes
+                        // with every CTA's red.add of the sum); tests/test_gpu_parity.py
+                        // test_residual_sum_complete checks RES_k against the traced r_k every
+                        // iteration, where a missing CTA partial would show up as a ~1/G deficit
                         const double t = __longlong_as_double(static_cast<long long>(rsum));
                         res = bb > 0.0 ? t / bb : t;
                         if (lead && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;
@@ -1634,8 +1652,14 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     const size_t xch_bytes = kXchBytes;
     // multi-rank launches on this GPU (virtual ranks) need one exchange region per rank
     const int nreg = (multi && ranks->rank < 0) ? ranks->P : 1;
-    const size_t ex_bytes = loop_exchange_bytes(gtotal) + static_cast<size_t>(nreg - 1) * xch_bytes;
+    // (a real rank's buffer holds its own region and its own [2][Gr] slots -- the peers' slots live
+    //  in their memory; virtual ranks carve every rank's region and slots from this one buffer)
+    const int slot_ctas = (multi && ranks->rank >= 0) ? ranks->Gr : gtotal;
+    const size_t ex_bytes = loop_exchange_bytes(slot_ctas) + static_cast<size_t>(nreg - 1) * xch_bytes;
+    void *const slots_before = ctx->slots.ptr;
     CSK_CHECK(ensure(ctx, ctx->slots, ex_bytes));
+    if (multi && ranks->exchange_zeroed && ctx->slots.ptr != slots_before)
+        return fail(ctx, CSK_E_CUDA, "csk_solve_sharded: the exported exchange buffer was reallocated");
     CSK_CHECK(ensure(ctx, ctx->report, 8 * 8));
     CSK_CHECK(ensure(ctx, ctx->scalars, 8 * 8));
     if (!(multi && ranks->exchange_zeroed)) CSK_CUDA(ctx, cudaMemsetAsync(ctx->slots.ptr, 0, ex_bytes, stream));
@@ -1698,6 +1722,9 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.idx_trace = opts ? opts->idx_trace : nullptr;
     prm.res_trace = opts ? opts->res_trace : nullptr;
     prm.x_trace = opts ? opts->x_trace : nullptr;
+    prm.r_trace = (opts && opts->r_trace_cap > 0) ? opts->r_trace : nullptr;
+    prm.r_trace_cap = prm.r_trace ? opts->r_trace_cap : 0;
+    prm.d_glob = multi ? ranks->dlo[ranks->P] : d;
     prm.phase_cycles = opts ? opts->phase_cycles : nullptr;
     static const double tmo_s = getenv("CSK_EXCHANGE_TIMEOUT_S") ? atof(getenv("CSK_EXCHANGE_TIMEOUT_S")) : 30.0;
     prm.timeout_ns = static_cast<unsigned long long>(tmo_s * 1e9);

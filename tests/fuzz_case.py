@@ -9,8 +9,7 @@ from test_gpu_parity import _lockstep, _np
 m, n, d, kind, k = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], int(sys.argv[5])
 p = make_dense(m, n, kind, 7000 + k, "cuda")
 At, bt, nsq = csk.csk_sketch(p.A, p.b, d, seed=k)
-for opts in [{}, {"smem_rows": -1}, {"cluster_size": 1, "num_ctas": 148}, {"num_ctas": 100}, {"reg_rows": 8},
-             {"legacy": True}]:
+for opts in [{}, {"smem_rows": -1}, {"cluster_size": 1, "num_ctas": 148}, {"num_ctas": 100}, {"reg_rows": 8}]:
     try:
         g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=1e-30, max_iters=40, trace=41, trace_x=True, **opts)
         try:

@@ -5,9 +5,11 @@ Bars (BASELINE north_star):
     fold of exactly representable +-A values);
   * nsq: fixed but different summation order -> |d nsq| <= 2 n u nsq (gamma_n bound
     for a sum of n non-negative terms, u = 2^-53);
-  * loop: lockstep -- given the GPU's x_k the oracle's residual picks the same i_k
-    (or a near-tie within 4e-10 relative), the oracle's step from (x_k, i_k) lands on
-    the GPU's x_{k+1} within 1e-12 relative; free-running -- RES <= tol for both and
+  * loop: lockstep -- given the GPU's x_k, the GPU's residual vector r_k (traced by the kernel's
+    finalize, csk_solve_opts_t.r_trace) is within 1e-10 of the oracle's r(x_k) in the 2-norm,
+    relative (north_star); the oracle's scores (its own row norms) pick the same i_k (or a
+    near-tie within 4e-10 relative); the oracle's step from (x_k, i_k) lands on the GPU's
+    x_{k+1} within 1e-12 relative; free-running -- RES <= tol for both and
     |IT_gpu - IT_orc| <= max(1, 5 % IT_orc).
 """
 import numpy as np
@@ -160,11 +162,30 @@ def test_sketch_graph_replay(csk, timing):
 
 
 # ---------------------------------------------------------------- S5-S8 loop
-def _lockstep(At, bt, nsq, xtr, itr, k_max):
-    At, bt, nsq = _np(At), _np(bt), _np(nsq)
+R_TOL = 1e-10  # north_star: per-iteration residuals within 1e-10 relative given the same x_k
+
+
+def _check_r(r_gpu, r_orc, k):
+    """||r_gpu - r_orc||_2 <= 1e-10 ||r_orc||_2 (normwise: elementwise relative error is unbounded
+    where r_i ~ 0, e.g. at i_{k-1} right after its projection; SURVEY.md §8(c) acceptance 3)."""
+    err = float(np.linalg.norm(r_gpu - r_orc))
+    assert err <= R_TOL * float(np.linalg.norm(r_orc)), (k, err, float(np.linalg.norm(r_orc)))
+
+
+def _lockstep(At, bt, nsq, xtr, itr, k_max, rtr=None):
+    """Step-for-step check of the GPU trajectory against the oracle.  Scores use the ORACLE's row
+    norms (``nsq`` is accepted for the call sites' symmetry but not used), so a wrong GPU nsq
+    cannot hide; ``rtr`` (the kernel's r_k trace) is checked against the oracle's r(x_k)."""
+    At, bt = _np(At), _np(bt)
+    nsq = oracle.row_norms(At)
     xtr, itr = _np(xtr), _np(itr)
+    rtr = None if rtr is None else _np(rtr)
+    if rtr is not None:
+        assert len(rtr) >= min(k_max, len(itr)), "r trace shorter than the checked window"
     for k in range(min(k_max, len(itr), len(xtr) - 1)):
         r = oracle.residual(At, bt, xtr[k])
+        if rtr is not None:
+            _check_r(rtr[k], r, k)
         mask = nsq > 0
         sc = np.where(mask, r * r / np.where(mask, nsq, 1), -1.0)
         io = int(np.argmax(sc))
@@ -195,12 +216,15 @@ def test_solve_parity_small_configs(csk, name):
     p = make_config(cfg, "cuda")
     At, bt, nsq = _check_sketch(csk, p.A, p.b, cfg.d, cfg.sketch_seed)
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters,
-                      trace=4000, trace_x=True)
+                      trace=4000, trace_x=True, trace_r=4000)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star),
                      tol=cfg.tol, max_iters=cfg.max_iters, trace=4000)
     assert g.termination == csk.CONVERGED
     _free_running(g, o)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000)
+    # every iteration, including the residual at the returned iterate (IT + 1 vectors)
+    assert len(g.r_trace) == g.iterations + 1
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000, g.r_trace)
+    _check_r(_np(g.r_trace)[g.iterations], oracle.residual(_np(At), _np(bt), _np(g.x)), g.iterations)
     n_same = min(len(g.idx_trace), len(o.idx_trace))
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
     assert abs(g.final_res - oracle.solve(_np(At), _np(bt), _np(nsq), x0=_np(g.x), x_star=_np(p.x_star), max_iters=0).final_res) <= 1e-12
@@ -215,10 +239,10 @@ def test_solve_launch_shapes_and_streamed_rows(csk, num_ctas, smem_rows, cluster
     p = make_dense(8000, 300, "lognormal_rows", 91, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, 1500, seed=4)
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, num_ctas=num_ctas, smem_rows=smem_rows,
-                      cluster_size=cluster, trace=300, trace_x=True)
+                      cluster_size=cluster, trace=300, trace_x=True, trace_r=300)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), trace=300)
     _free_running(g, o)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 300)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 300, g.r_trace)
 
 
 @pytest.mark.parametrize("name,cluster,tmem", [("C1", 16, None), ("C1", 1, None), ("C2", 16, None),
@@ -230,14 +254,14 @@ def test_solve_cluster_and_grid_exchange(csk, name, cluster, tmem):
     p = make_config(cfg, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters,
-                      cluster_size=cluster, tmem=tmem, trace=4000, trace_x=True)
+                      cluster_size=cluster, tmem=tmem, trace=4000, trace_x=True, trace_r=4000)
     geo = csk.csk_last_solve_geometry()
     assert geo["cluster_size"] == (16 if cluster == 16 else 1)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star),
                      tol=cfg.tol, max_iters=cfg.max_iters, trace=4000)
     assert g.termination == csk.CONVERGED
     _free_running(g, o)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000, g.r_trace)
     n_same = min(len(g.idx_trace), len(o.idx_trace))
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
 
@@ -257,7 +281,7 @@ def test_solve_tmem_tier(csk, n, d, num_ctas, reg_rows, group_warps):
     At, bt, nsq = csk.csk_sketch(p.A, p.b, d, seed=5)
     cap = 20000 if n <= 500 else 300
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=num_ctas, reg_rows=reg_rows,
-                      group_warps=group_warps, tmem=True, trace=min(cap + 1, 400), trace_x=True)
+                      group_warps=group_warps, tmem=True, trace=min(cap + 1, 400), trace_x=True, trace_r=150)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), max_iters=cap,
                      trace=min(cap + 1, 400))
     if n <= 500:
@@ -265,7 +289,7 @@ def test_solve_tmem_tier(csk, n, d, num_ctas, reg_rows, group_warps):
     else:
         assert g.termination == o.termination == csk.MAX_ITERS
         assert abs(g.final_res - o.final_res) <= 1e-6 * o.final_res
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 150)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 150, g.r_trace)
     n_same = min(len(g.idx_trace), len(o.idx_trace), 400)
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
 
@@ -290,8 +314,8 @@ def test_solve_ragged_n(csk, n):
         assert g.termination == o.termination == csk.MAX_ITERS
         assert np.array_equal(_np(g.idx_trace), o.idx_trace)
         assert abs(g.final_res - o.final_res) <= 1e-6 * o.final_res
-        g2 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=8, tol=1e-30, trace=9, trace_x=True)
-        _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 8)
+        g2 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=8, tol=1e-30, trace=9, trace_x=True, trace_r=9)
+        _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 8, g2.r_trace)
 
 
 @pytest.mark.parametrize("num_ctas,cluster", [(0, 0), (148, 1), (64, 16)])
@@ -306,9 +330,9 @@ def test_solve_residual_mode(csk, num_ctas, cluster):
     assert float(r @ r) / float(_np(bt) @ _np(bt)) <= 1e-10 * (1 + 1e-6)
     # the residual-mode kernel records its iterates too: step for step with the oracle
     g2 = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-30, max_iters=200, num_ctas=num_ctas,
-                       cluster_size=cluster, trace=201, trace_x=True)
+                       cluster_size=cluster, trace=201, trace_x=True, trace_r=201)
     assert not np.isnan(_np(g2.x_trace)).any()
-    _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 200)
+    _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 200, g2.r_trace)
 
 
 def test_solve_edge_cases(csk):
@@ -377,12 +401,12 @@ def test_solve_stream_ring(csk, d, n, num_ctas, smem_rows, tmem, ring):
     At, bt = p.A, p.b
     nsq = csk.csk_row_norms(At)
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, num_ctas=num_ctas, smem_rows=smem_rows, tmem=tmem,
-                      stream_ring=ring, trace=200, trace_x=True, max_iters=200 if n > 1000 else 50000)
+                      stream_ring=ring, trace=200, trace_x=True, trace_r=200, max_iters=200 if n > 1000 else 50000)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), trace=200,
                      max_iters=200 if n > 1000 else 50000)
     if n <= 1000:
         _free_running(g, o)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 200)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 200, g.r_trace)
 
 
 @pytest.mark.parametrize("d,n,num_ctas,tmem", [(6000, 150, 8, None), (4000, 50, 3, None), (1200, 2000, 6, None),
@@ -395,14 +419,14 @@ def test_solve_stream_ring_residual_mode(csk, d, n, num_ctas, tmem):
     nsq = csk.csk_row_norms(At)
     its = 150 if n > 1000 else 50000
     g = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-12, num_ctas=num_ctas, tmem=tmem, trace=150,
-                      trace_x=True, max_iters=its)
+                      trace_x=True, trace_r=150, max_iters=its)
     assert csk.csk_last_solve_tiers()["ring_stages"] >= 2
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=None, tol=1e-12, trace=150, max_iters=its)
     assert g.stop_mode == csk.STOP_RESIDUAL
     if n <= 1000:
         assert g.termination == o.termination == csk.CONVERGED
         assert abs(g.iterations - o.iterations) <= max(1, 0.02 * o.iterations)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 150)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 150, g.r_trace)
 
 
 @pytest.mark.parametrize("smem_rows,tmem", [(0, None), (-1, False)])
@@ -412,9 +436,11 @@ def test_mwrk_unsketched_parity(csk, smem_rows, tmem):
     register tier re-read from L2/HBM each iteration)."""
     p = make_dense(12000, 200, "lognormal_rows", 23, "cuda")
     nsq = csk.csk_row_norms(p.A)
-    g = csk.csk_solve(p.A, p.b, nsq, x_star=p.x_star, smem_rows=smem_rows, tmem=tmem, trace=300, trace_x=True)
+    g = csk.csk_solve(p.A, p.b, nsq, x_star=p.x_star, smem_rows=smem_rows, tmem=tmem, trace=300, trace_x=True,
+                      trace_r=100)
     o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), trace=300)
     _free_running(g, o)
+    _lockstep(p.A, p.b, nsq, g.x_trace, g.idx_trace, 100, g.r_trace)
     _lockstep(p.A, p.b, nsq, g.x_trace, g.idx_trace, 300)
 
 
@@ -432,16 +458,42 @@ def test_C3_full_parity(csk):
     cfg = CONFIGS["C3"]
     p = make_config(cfg, "cuda")
     At, bt, nsq = _check_sketch(csk, p.A, p.b, cfg.d, cfg.sketch_seed)
-    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cfg.max_iters, trace=200, trace_x=True)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cfg.max_iters, trace=2000, trace_x=True,
+                      trace_r=2000)
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star),
-                     max_iters=cfg.max_iters)
+                     max_iters=cfg.max_iters, trace=2000)
     _free_running(g, o)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 40)
+    # every iteration of the full C3 solve: r_k within 1e-10, same i_k, x_{k+1} within 1e-12
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, g.iterations, g.r_trace)
+    n_same = min(len(g.idx_trace), len(o.idx_trace))
+    assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
+
+
+def test_residual_sum_complete(csk):
+    """Residual stop on one GPU: RES_k = ||r_k||^2/||b~||^2 is summed from the CTA partials beside
+    the arrival count and read with one 32-byte load (loop.cu: a hardware property, not a PTX
+    guarantee).  Every iteration, the kernel's RES_k must equal the sum over the traced r_k to
+    within rounding -- a CTA partial missing from the snapshot would be a ~1/148 deficit."""
+    cfg = CONFIGS["C3"]
+    p = make_config(cfg, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
+    bb = float(_np(bt) @ _np(bt))
+    for rep in range(3):
+        g = csk.csk_solve(At, bt, nsq, x_star=None, tol=1e-30, max_iters=600, trace=601, trace_r=601)
+        r = _np(g.r_trace)
+        want = np.einsum("ij,ij->i", r, r) / bb
+        got = _np(g.res_trace)
+        assert len(got) == len(want) == 601
+        assert np.all(np.abs(got - want) <= 1e-12 * want), (rep, np.max(np.abs(got - want) / want))
 
 
 def test_C4_full_size_sampled(csk):
-    """8 GB A: sampled buckets against the oracle's fold of exactly those rows, lockstep on the
-    first iterations, and properties over the whole 50k-iteration run (monotone RES, eq:A)."""
+    """8 GB A: sampled buckets against the oracle's fold of exactly those rows; the first 3 000
+    iterations free-running on both sides (the oracle on the GPU's A~, ~45 s): the same i_k
+    sequence, both MaxIters, RES within 1e-6 relative (SURVEY §8(c) acceptance 4 at a 3 000 cap);
+    lockstep with the r_k trace on the first iterations; and properties over the whole
+    50k-iteration run (monotone RES, eq:A).  The full 50k comparison against the oracle is the
+    committed artifact profiles/r02_parity_C4.txt (tools/parity_full.py)."""
     cfg = CONFIGS["C4"]
     p = make_config(cfg, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
@@ -461,9 +513,18 @@ def test_C4_full_size_sampled(csk):
     assert g.termination in (csk.CONVERGED, csk.MAX_ITERS)
     res = _np(g.res_trace)
     assert np.all(np.diff(res) <= 1e-12 * res[:-1])
-    g20 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=12, tol=1e-30, trace=13, trace_x=True)
-    _lockstep(At, bt, nsq, g20.x_trace, g20.idx_trace, 12)
+    g20 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=12, tol=1e-30, trace=13, trace_x=True, trace_r=13)
+    _lockstep(At, bt, nsq, g20.x_trace, g20.idx_trace, 12, g20.r_trace)
     assert np.array_equal(_np(g20.idx_trace), _np(g.idx_trace)[:12])
+    # free-running at a 3 000-iteration cap on both sides
+    cap = 3000
+    g3 = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, trace=cap + 1)
+    Atn, btn = _np(At), _np(bt)
+    o3 = oracle.solve(Atn, btn, oracle.row_norms(Atn), x_star=_np(p.x_star), max_iters=cap, trace=cap + 1)
+    assert g3.termination == o3.termination == csk.MAX_ITERS and g3.iterations == o3.iterations == cap
+    assert np.array_equal(_np(g3.idx_trace), o3.idx_trace)
+    assert abs(g3.final_res - o3.final_res) <= 1e-6 * o3.final_res
+    assert np.allclose(_np(g3.res_trace), o3.res_trace, rtol=1e-6, atol=0)
 
 
 # ---------------------------------------------------------------- CSR input (config C5)
@@ -525,9 +586,9 @@ def test_C5_full_size_sampled(csk):
         bs = _np(p.b[torch.as_tensor(rows, device="cuda")])
         a1, b1 = oracle.sketch_csr(sub_rp, cols, vals, bs, cfg.n, 1, h=np.zeros(len(rows), np.int32), s=s[rows])
         assert np.array_equal(_np(At[j]), a1[0]) and _np(bt[j]) == b1[0]
-    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=6, tol=1e-30, trace=7, trace_x=True)
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6)
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=6, tol=1e-30, trace=7, trace_x=True, trace_r=7)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6, g.r_trace)
     # the residual stop at full size (x* unknown): streamed rows through the RESMODE ring
-    g = csk.csk_solve(At, bt, nsq, x_star=None, max_iters=6, tol=1e-30, trace=7, trace_x=True)
+    g = csk.csk_solve(At, bt, nsq, x_star=None, max_iters=6, tol=1e-30, trace=7, trace_x=True, trace_r=7)
     assert g.stop_mode == csk.STOP_RESIDUAL and csk.csk_last_solve_tiers()["ring_stages"] >= 2
-    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 6, g.r_trace)

@@ -8,9 +8,14 @@
   reduce-scatter is an identity, so A~ must be bit-exact with the oracle.
 Real P > 1 NCCL runs need P GPUs (bench.py under torchrun).
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import oracle
 from csk_synth import CONFIGS, make_config, make_dense
@@ -32,17 +37,26 @@ def _np(t):
 
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
 def test_virtual_ranks_match_oracle(csk, P):
+    """The S10 decomposition (P virtual ranks, one launch) against the oracle step for step: the
+    same i_k sequence, every rank's r_k (traced by global row) within 1e-10 of the oracle's
+    r(x_k), x_{k+1} within 1e-12 (the lockstep bar of test_gpu_parity.py)."""
+    from test_gpu_parity import _lockstep
     cfg = CONFIGS["C2"]
     p = make_config(cfg, "cuda")
     At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
-    x, copies, rep = csk.csk_solve_virtual_ranks(At, bt, nsq, P, x_star=p.x_star, tol=cfg.tol,
-                                                 max_iters=cfg.max_iters)
+    x, copies, rep, tr = csk.csk_solve_virtual_ranks(At, bt, nsq, P, x_star=p.x_star, tol=cfg.tol,
+                                                     max_iters=cfg.max_iters, trace=2000, trace_x=True,
+                                                     trace_r=2000)
     assert all(torch.equal(copies[q], copies[0]) for q in range(P))
     assert torch.equal(x, copies[0])
     o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), tol=cfg.tol,
-                     max_iters=cfg.max_iters)
+                     max_iters=cfg.max_iters, trace=2000)
     assert rep.termination == csk.CONVERGED and rep.final_res <= cfg.tol
     assert abs(rep.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
+    n_same = min(len(tr.idx_trace), len(o.idx_trace))
+    assert np.array_equal(_np(tr.idx_trace)[:n_same], o.idx_trace[:n_same])
+    assert not np.isnan(_np(tr.r_trace)).any()  # every rank wrote its rows
+    _lockstep(At, bt, nsq, tr.x_trace, tr.idx_trace, rep.iterations, tr.r_trace)
     # the single-GPU persistent kernel and the sharded kernels agree on the trajectory length
     g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, tol=cfg.tol, max_iters=cfg.max_iters)
     assert abs(g.iterations - rep.iterations) <= max(1, 0.05 * o.iterations)
@@ -54,11 +68,14 @@ def test_virtual_ranks_streamed_rows(csk, P):
     inside the P-rank decomposition too (MWRK on a tall system, Remark 1)."""
     p = make_dense(90000, 128, "lognormal_rows", 31, "cuda")
     nsq = csk.csk_row_norms(p.A)
-    x, copies, rep = csk.csk_solve_virtual_ranks(p.A, p.b, nsq, P, x_star=p.x_star, tol=1e-6, max_iters=5000)
+    x, copies, rep, tr = csk.csk_solve_virtual_ranks(p.A, p.b, nsq, P, x_star=p.x_star, tol=1e-6, max_iters=5000,
+                                                     trace=5001)
     assert all(torch.equal(copies[q], copies[0]) for q in range(P))
-    o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), tol=1e-6, max_iters=5000)
+    o = oracle.mwrk(_np(p.A), _np(p.b), x_star=_np(p.x_star), tol=1e-6, max_iters=5000, trace=5001)
     assert rep.termination == csk.CONVERGED and rep.final_res <= 1e-6
     assert abs(rep.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
+    n_same = min(len(tr.idx_trace), len(o.idx_trace))
+    assert np.array_equal(_np(tr.idx_trace)[:n_same], o.idx_trace[:n_same])
     # the residual stop (x* unknown) through the ring's SYS twins: the partials cross ranks
     x, copies, rep = csk.csk_solve_virtual_ranks(p.A, p.b, nsq, P, x_star=None, tol=1e-12, max_iters=5000)
     assert all(torch.equal(copies[q], copies[0]) for q in range(P))

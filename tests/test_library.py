@@ -46,7 +46,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_version_and_status_strings(lib):
     lib.csk_abi_version.restype = ctypes.c_int
-    assert lib.csk_abi_version() == 1
+    assert lib.csk_abi_version() == 2
     lib.csk_status_string.restype = ctypes.c_char_p
     assert lib.csk_status_string(0) == b"CSK_OK"
     assert lib.csk_status_string(2) == b"CSK_E_ZERO_SKETCH"
