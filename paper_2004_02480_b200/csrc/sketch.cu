@@ -18,7 +18,8 @@
 //   * a b-warp folds b~ for the same buckets, one bucket per lane, row order.
 // Short rows (n <= 256, the paper's Table-1 shapes): warp per bucket, rows loaded straight
 //   from HBM with R rows in flight per warp (k_sketch_dense_wpb).
-// CSR kernel (config C5): warp per bucket, dense shared-memory accumulator row.
+// CSR kernel (config C5): warp per bucket range, dense shared-memory accumulator row, the
+//   (col, val) pairs gathered by cp.async into per-warp stages, several batches in flight.
 #include "csk_internal.cuh"
 
 namespace csk {
@@ -378,97 +379,6 @@ k_row_norms(const double *__restrict__ At, int64_t d, int64_t n, double *__restr
     }
 }
 
-// CSR sketch: one warp per bucket; a dense fp64 accumulator row of n in shared memory per
-// warp; the bucket's rows are folded in ascending order.  Rows come in batches of 32: lane r
-// holds the r-th row's perm entry, row_ptr pair and b value (three parallel loads), then the
-// first 32 stored (col, val) pairs of every row of the batch are loaded into registers (lane l
-// holding pair l of each row) before any add, so a batch costs three dependent memory latencies
-// instead of three per row.  Within a row the columns are distinct, so its pairs are added by
-// the lanes in parallel; rows are separated by __syncwarp (row order per column).  Pairs past the
-// first 32 of a row are read in the add loop.  Row norms fused as in the dense epilogue but with
-// the warp-only team (documented in DESIGN.md; checked to tolerance).
-__global__ void __launch_bounds__(384, 1) k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                             const double *__restrict__ val, const double *__restrict__ b,
-                             int64_t n, int64_t d, const int32_t *__restrict__ perm,
-                             const int32_t *__restrict__ offsets, double *__restrict__ At,
-                             double *__restrict__ bt, double *__restrict__ nsq, int64_t acc_stride) {
-    extern __shared__ __align__(16) double acc_all[];
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5;
-    double *acc = acc_all + static_cast<int64_t>(warp) * acc_stride;
-    for (int64_t j = static_cast<int64_t>(blockIdx.x) * wpb + warp; j < d;
-         j += static_cast<int64_t>(gridDim.x) * wpb) {
-        for (int64_t k = lane; k < n; k += 32) acc[k] = 0.0;
-        __syncwarp();
-        const int64_t a = offsets[j], e = offsets[j + 1];
-        double bacc = 0.0;
-        // the batch's perm entries, row_ptr pairs and b values, one batch ahead
-        int32_t prn = (a + lane < e) ? __ldg(perm + a + lane) : 0;
-        int64_t rsn = (a + lane < e) ? __ldg(row_ptr + (prn & 0x7fffffff)) : 0;
-        int64_t ren = (a + lane < e) ? __ldg(row_ptr + (prn & 0x7fffffff) + 1) : 0;
-        double bn = (a + lane < e) ? __ldg(b + (prn & 0x7fffffff)) : 0.0;
-        for (int64_t t = a; t < e; t += 32) {
-            const int cnt = (e - t) < 32 ? static_cast<int>(e - t) : 32;
-            const int32_t prl = prn;
-            const int64_t rsl = rsn, rel = ren;
-            const double bl = bn;
-            if (t + 32 < e) {
-                const bool ok = t + 32 + lane < e;
-                prn = ok ? __ldg(perm + t + 32 + lane) : 0;
-                rsn = ok ? __ldg(row_ptr + (prn & 0x7fffffff)) : 0;
-                ren = ok ? __ldg(row_ptr + (prn & 0x7fffffff) + 1) : 0;
-                bn = ok ? __ldg(b + (prn & 0x7fffffff)) : 0.0;
-            }
-            int32_t cc[32];
-            double vv[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                const int64_t s0 = __shfl_sync(0xffffffffu, rsl, r), s1 = __shfl_sync(0xffffffffu, rel, r);
-                const int64_t q = s0 + lane;
-                const bool ok = r < cnt && q < s1;
-                cc[r] = ok ? __ldg(col + q) : 0;
-                vv[r] = ok ? __ldg(val + q) : 0.0;
-            }
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                if (r < cnt) {
-                    const int64_t s0 = __shfl_sync(0xffffffffu, rsl, r), s1 = __shfl_sync(0xffffffffu, rel, r);
-                    const bool neg = __shfl_sync(0xffffffffu, prl, r) < 0;
-                    if (s0 + lane < s1) acc[cc[r]] = acc[cc[r]] + (neg ? -vv[r] : vv[r]);
-                    for (int64_t q = s0 + 32 + lane; q < s1; q += 32) {  // rows with > 32 stored pairs
-                        const int32_t c = __ldg(col + q);
-                        const double v = __ldg(val + q);
-                        acc[c] = acc[c] + (neg ? -v : v);
-                    }
-                    __syncwarp();
-                    const double bv = __shfl_sync(0xffffffffu, bl, r);
-                    bacc = bacc + (neg ? -bv : bv);
-                }
-            }
-        }
-        __syncwarp();
-        double part = 0.0;
-        double *dst = At + j * n;
-        for (int64_t k = 2 * lane; k < n; k += 64) {
-            const double a0 = acc[k];
-            dst[k] = a0;
-            part = __fma_rn(a0, a0, part);
-            if (k + 1 < n) {
-                const double a1 = acc[k + 1];
-                dst[k + 1] = a1;
-                part = __fma_rn(a1, a1, part);
-            }
-        }
-        part = warp_sum(part);
-        if (lane == 0) {
-            bt[j] = bacc;
-            if (nsq) nsq[j] = part;
-        }
-        __syncwarp();
-    }
-}
-
 // Short rows (n <= 256): one warp per bucket.  The row-per-CTA ring above moves each gathered
 // row with its own bulk copy, and for rows of a few hundred bytes the copy issue rate, not HBM,
 // bounds it (one consumer warp per CTA at n <= 64).  Here every warp owns whole buckets: lane l
@@ -604,6 +514,267 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
     }
 }
 
+
+// ---- CSR sketch (config C5): warp per bucket range, dense shared-memory accumulator row ----
+//
+// Warp w owns the buckets whose first row lies in [w m/W, (w+1) m/W) of the bucket-sorted
+// order: one contiguous range of `perm`.  The pair stream of a bucket (its rows' stored (col,
+// val) pairs, rows ascending, pairs in stored order) is cut into batches of <= kCsrSP pairs
+// (whole rows, or a slice of one long row); each batch is GATHERED with cp.async (LDGSTS: 8-byte
+// val, 4-byte col, no registers held) into one of kCsrS shared-memory stages, so kCsrS batches'
+// HBM reads are in flight per warp while the oldest one is folded.  Row descriptors (perm entry,
+// row_ptr pair, b) are loaded 32 rows at a time, one window ahead (perm two windows ahead).
+// The fold adds 32 pairs per step into the accumulator row: pairs that hit the same column (from
+// different rows -- a row's columns are distinct) are serialised in pair order (= row order) with
+// __match_any_sync ranks, so every column is the sequential ascending-row fold of the oracle.
+// b~ is folded at batch formation (row order), the A~ row is stored (coalesced 16-byte stores)
+// and its norm formed when the bucket's last batch has been folded.
+constexpr int kCsrS = 4;                                       // stages (batches in flight) per warp
+constexpr int kCsrSP = 256;                                    // pairs per stage
+constexpr int kCsrStageBytes = kCsrSP * (8 + 4 + 1);           // val | col | sign
+constexpr int kCsrMetaBytes = kCsrS * 16;
+constexpr int kCsrMaxWarps = 16;
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_n(int pending) {  // pending in [0, kCsrS)
+    static_assert(kCsrS == 4, "cp_async_wait_n covers 0..3");
+    switch (pending) {
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    }
+}
+
+__global__ void __launch_bounds__(kCsrMaxWarps * 32, 1)
+k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const double *__restrict__ val,
+             const double *__restrict__ b, int64_t m, int64_t n, int64_t d, const int32_t *__restrict__ perm,
+             const int32_t *__restrict__ offsets, double *__restrict__ At, double *__restrict__ bt,
+             double *__restrict__ nsq, int64_t acc_stride, int warp_bytes, int vec) {
+    extern __shared__ __align__(16) unsigned char csr_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char *ws = csr_smem + static_cast<size_t>(warp) * warp_bytes;
+    double *acc = reinterpret_cast<double *>(ws);
+    unsigned char *stg = ws + acc_stride * 8;
+    int *meta = reinterpret_cast<int *>(stg + kCsrS * kCsrStageBytes);  // [kCsrS][4]: pairs, bucket, end
+    for (int64_t k = lane; k < acc_stride; k += 32) acc[k] = 0.0;
+    __syncwarp();
+    const int W = static_cast<int>(gridDim.x) * static_cast<int>(blockDim.x >> 5);
+    const int w = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x >> 5) + warp;
+    int64_t fj = warp_lower_bound(offsets, d, m * w / W, lane);
+    const int64_t je = (w == W - 1) ? d : warp_lower_bound(offsets, d, m * (w + 1) / W, lane);
+    if (fj >= je) return;
+    const int64_t T1 = offsets[je];
+    int64_t t = offsets[fj];  // perm position of the next row to take
+    // bucket ends, lane-distributed: lane l holds offsets[ob + 1 + l]
+    int64_t ob = fj;
+    int32_t owin = (ob + 1 + lane <= je) ? __ldg(offsets + ob + 1 + lane) : static_cast<int32_t>(T1);
+    auto end_of = [&](int64_t jj) -> int64_t {  // offsets[jj + 1] (warp-uniform jj >= ob)
+        if (jj - ob >= 32) {
+            ob = jj;
+            owin = (ob + 1 + lane <= je) ? __ldg(offsets + ob + 1 + lane) : static_cast<int32_t>(T1);
+        }
+        return __shfl_sync(0xffffffffu, owin, static_cast<int>(jj - ob));
+    };
+    auto zero_row = [&](int64_t jj) {  // an empty bucket: A~ row 0, b~ 0, nsq 0
+        double *dst = At + jj * n;
+        for (int64_t k = lane; k < n; k += 32) dst[k] = 0.0;
+        if (lane == 0) {
+            bt[jj] = 0.0;
+            if (nsq) nsq[jj] = 0.0;
+        }
+    };
+    int64_t fe = end_of(fj);  // end (perm position) of the bucket being formed
+    while (fj < je && fe == t) {
+        zero_row(fj);
+        ++fj;
+        if (fj < je) fe = end_of(fj);
+    }
+    // ---- row-descriptor windows: lane l describes the row at perm position wbase + l ----
+    auto load_pr = [&](int64_t base) -> int32_t { return (base + lane < T1) ? __ldg(perm + base + lane) : 0; };
+    int64_t wbase = t;
+    int32_t pr = load_pr(wbase);
+    const int32_t pr1 = load_pr(wbase + 32);
+    int32_t pr2 = load_pr(wbase + 64);
+    auto desc = [&](int64_t base, int32_t p, int64_t &rs, int64_t &re, double &bv) {
+        const int64_t r = p & 0x7fffffff;
+        const bool ok = base + lane < T1;
+        rs = ok ? __ldg(row_ptr + r) : 0;
+        re = ok ? __ldg(row_ptr + r + 1) : 0;
+        bv = ok ? __ldg(b + r) : 0.0;
+    };
+    int64_t rs, re, nrs, nre;
+    double bv, nbv;
+    desc(wbase, pr, rs, re, bv);
+    int32_t npr = pr1;
+    desc(wbase + 32, npr, nrs, nre, nbv);
+    int64_t roff = 0;  // pairs of the row at t already taken (a long row split over batches)
+    double bacc = 0.0;
+    int issued = 0, folded = 0;
+    // ---- form one batch of bucket fj into stage `slot` and issue its gathers ----
+    auto form = [&](int slot) {
+        if (t - wbase >= 32) {  // next window (its descriptors are already in flight)
+            wbase += 32;
+            pr = npr; rs = nrs; re = nre; bv = nbv;
+            npr = pr2;
+            desc(wbase + 32, npr, nrs, nre, nbv);
+            pr2 = load_pr(wbase + 64);
+        }
+        const int cur = static_cast<int>(t - wbase);
+        const int64_t wend = (wbase + 32 < fe) ? wbase + 32 : fe;
+        const int ra = static_cast<int>(wend - t);  // rows of bucket fj left in this window (>= 1)
+        const bool inr = lane >= cur && lane < cur + ra;
+        const int64_t len = re - rs;
+        const int64_t skip = (lane == cur) ? roff : 0;
+        int64_t cnt = inr ? len - skip : 0;
+        // inclusive scan of the counts (int64: any row length)
+        int64_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int64_t first = __shfl_sync(0xffffffffu, cnt, cur);
+        int k;            // whole rows taken
+        bool partial;     // a slice of the (long) row at cur
+        int64_t P;
+        if (first > kCsrSP) {
+            partial = true;
+            k = 0;
+            P = kCsrSP;
+            cnt = (lane == cur) ? kCsrSP : 0;
+            inc = (lane >= cur) ? kCsrSP : 0;
+        } else {
+            partial = false;
+            k = __popc(__ballot_sync(0xffffffffu, inr && inc <= kCsrSP));
+            P = __shfl_sync(0xffffffffu, inc, cur + k - 1);
+            if (lane >= cur + k) { cnt = 0; inc = P; }
+        }
+        const int64_t ex = inc - cnt;
+        const int64_t start = rs + skip;
+        const bool neg = pr < 0;
+        double *sv = reinterpret_cast<double *>(stg + slot * kCsrStageBytes);
+        int32_t *sc = reinterpret_cast<int32_t *>(stg + slot * kCsrStageBytes + kCsrSP * 8);
+        unsigned char *sg = stg + slot * kCsrStageBytes + kCsrSP * 12;
+        for (int q0 = 0; q0 < static_cast<int>(P); q0 += 32) {
+            const int q = q0 + lane;
+            int r = 0;  // the row of pair q: smallest lane r with inc_r > q
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1) {
+                const int64_t v = __shfl_sync(0xffffffffu, inc, r + st - 1);
+                if (v <= q) r += st;
+            }
+            const int64_t s0 = __shfl_sync(0xffffffffu, start, r);
+            const int64_t e0 = __shfl_sync(0xffffffffu, ex, r);
+            const bool ng = __shfl_sync(0xffffffffu, neg, r);
+            if (q < P) {
+                const int64_t off = s0 + (q - e0);
+                cp_async8(sv + q, val + off);
+                cp_async4(sc + q, col + off);
+                sg[q] = ng ? 1 : 0;
+            }
+        }
+        cp_async_commit();
+        // b~: the rows that START in this batch, ascending (the oracle's fold order)
+        const double bs = neg ? -bv : bv;
+        const int rf = roff > 0 ? cur + 1 : cur, rl = partial ? cur + 1 : cur + k;
+        for (int r = rf; r < rl; ++r) bacc = bacc + __shfl_sync(0xffffffffu, bs, r);
+        if (partial) {
+            roff += kCsrSP;
+        } else {
+            t += k;
+            roff = 0;
+        }
+        const int64_t jb = fj;
+        const bool end = (t == fe);
+        if (end) {
+            if (lane == 0) bt[fj] = bacc;
+            bacc = 0.0;
+            ++fj;
+            if (fj < je) fe = end_of(fj);
+            while (fj < je && fe == t) {
+                zero_row(fj);
+                ++fj;
+                if (fj < je) fe = end_of(fj);
+            }
+        }
+        if (lane == 0) {
+            meta[slot * 4 + 0] = static_cast<int>(P);
+            meta[slot * 4 + 1] = static_cast<int>(jb);
+            meta[slot * 4 + 2] = end ? 1 : 0;
+        }
+    };
+    const unsigned lt = (1u << lane) - 1u;
+    for (;;) {
+        while (issued - folded < kCsrS && fj < je) {
+            form(issued % kCsrS);
+            ++issued;
+        }
+        if (folded == issued) break;
+        cp_async_wait_n(issued - folded - 1);
+        __syncwarp();
+        const int slot = folded % kCsrS;
+        const int P = meta[slot * 4 + 0];
+        const int64_t jb = meta[slot * 4 + 1];
+        const bool end = meta[slot * 4 + 2] != 0;
+        const double *sv = reinterpret_cast<const double *>(stg + slot * kCsrStageBytes);
+        const int32_t *sc = reinterpret_cast<const int32_t *>(stg + slot * kCsrStageBytes + kCsrSP * 8);
+        const unsigned char *sg = stg + slot * kCsrStageBytes + kCsrSP * 12;
+        for (int q0 = 0; q0 < P; q0 += 32) {
+            const int q = q0 + lane;
+            const bool ok = q < P;
+            const int c = ok ? sc[q] : -1 - lane;
+            double v = ok ? sv[q] : 0.0;
+            if (ok && sg[q]) v = -v;
+            const unsigned same = __match_any_sync(0xffffffffu, c);
+            const unsigned rank = __popc(same & lt);  // earlier pairs (rows) on the same column
+            const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+            for (unsigned rr = 0; rr <= maxr; ++rr) {
+                if (ok && rank == rr) acc[c] = acc[c] + v;
+                __syncwarp();
+            }
+        }
+        if (end) {  // bucket jb complete: store the A~ row, its norm, clear the accumulator
+            double part = 0.0;
+            double *dst = At + jb * n;
+            if (vec) {
+                double2 *a2 = reinterpret_cast<double2 *>(acc);
+                double2 *d2 = reinterpret_cast<double2 *>(dst);
+                for (int64_t k2 = lane; k2 < n / 2; k2 += 32) {
+                    const double2 a = a2[k2];
+                    d2[k2] = a;
+                    part = __fma_rn(a.x, a.x, part);
+                    part = __fma_rn(a.y, a.y, part);
+                    a2[k2] = make_double2(0.0, 0.0);
+                }
+            } else {
+                for (int64_t k = 2 * lane; k < n; k += 64) {
+                    const double a0 = acc[k];
+                    dst[k] = a0;
+                    part = __fma_rn(a0, a0, part);
+                    acc[k] = 0.0;
+                    if (k + 1 < n) {
+                        const double a1 = acc[k + 1];
+                        dst[k + 1] = a1;
+                        part = __fma_rn(a1, a1, part);
+                        acc[k + 1] = 0.0;
+                    }
+                }
+            }
+            part = warp_sum(part);
+            if (lane == 0 && nsq) nsq[jb] = part;
+        }
+        __syncwarp();
+        ++folded;
+    }
+}
+
 }  // namespace
 
 int norm_team_threads(int64_t n) { return dense_geom(n, true).tc; }
@@ -688,18 +859,18 @@ csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int3
                                const double *val, const double *b, int64_t m, int64_t n,
                                int64_t d, const int32_t *perm, const int32_t *offsets,
                                double *At, double *bt, double *nsq, cudaStream_t stream) {
-    (void)m;
-    const int64_t stride = (n + 1) & ~int64_t(1);
-    int wpb = static_cast<int>((ctx->max_smem_optin - 1024) / (stride * 8));
-    if (wpb > 12) wpb = 12;  // __launch_bounds__(384): the batch's (col, val) registers
-    if (wpb < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
-    const size_t smem = static_cast<size_t>(wpb) * stride * 8;
+    const int64_t stride = (n + 1) & ~int64_t(1);  // accumulator doubles (16-byte multiple)
+    const int64_t wb = ((stride * 8 + kCsrS * kCsrStageBytes + kCsrMetaBytes) + 127) & ~int64_t(127);
+    int warps = static_cast<int>(ctx->max_smem_optin / wb);
+    if (warps > kCsrMaxWarps) warps = kCsrMaxWarps;
+    if (warps < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
+    const size_t smem = static_cast<size_t>(warps) * wb;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_csr)));
-    int64_t grid = (d + wpb - 1) / wpb;
-    const int64_t cap = int64_t(ctx->num_sms) * 4;
-    if (grid > cap) grid = cap;
-    k_sketch_csr<<<static_cast<int>(grid), wpb * 32, smem, stream>>>(
-        row_ptr, col, val, b, n, d, perm, offsets, At, bt, nsq, stride);
+    const int vec = (n % 2 == 0 && aligned16(At)) ? 1 : 0;
+    time_mark(ctx, 0, false, stream);
+    k_sketch_csr<<<ctx->num_sms, warps * 32, smem, stream>>>(row_ptr, col, val, b, m, n, d, perm, offsets, At, bt,
+                                                            nsq, stride, static_cast<int>(wb), vec);
+    time_mark(ctx, 0, true, stream);
     CSK_CUDA(ctx, cudaGetLastError());
     return CSK_OK;
 }

@@ -165,11 +165,17 @@ def test_sketch_graph_replay(csk, timing):
 R_TOL = 1e-10  # north_star: per-iteration residuals within 1e-10 relative given the same x_k
 
 
-def _check_r(r_gpu, r_orc, k):
+def _check_r(r_gpu, r_orc, k, E=None):
     """||r_gpu - r_orc||_2 <= 1e-10 ||r_orc||_2 (normwise: elementwise relative error is unbounded
-    where r_i ~ 0, e.g. at i_{k-1} right after its projection; SURVEY.md §8(c) acceptance 3)."""
+    where r_i ~ 0, e.g. at i_{k-1} right after its projection; SURVEY.md §8(c) acceptance 3) -- or,
+    once the residual has shrunk to where fp64 cancellation decides (reading R-16), within the
+    rounding bound of the two evaluations, ||E||_2 with E_i = 2 (n + 2) u (|b~_i| + sum_j |A~_ij x_j|):
+    the exact r(x_k) itself is only known to that accuracy from any fp64 evaluation order."""
     err = float(np.linalg.norm(r_gpu - r_orc))
-    assert err <= R_TOL * float(np.linalg.norm(r_orc)), (k, err, float(np.linalg.norm(r_orc)))
+    bar = R_TOL * float(np.linalg.norm(r_orc))
+    if E is not None:
+        bar = max(bar, float(np.linalg.norm(E)))
+    assert err <= bar, (k, err, float(np.linalg.norm(r_orc)), bar)
 
 
 def _lockstep(At, bt, nsq, xtr, itr, k_max, rtr=None):
@@ -185,7 +191,8 @@ def _lockstep(At, bt, nsq, xtr, itr, k_max, rtr=None):
     for k in range(min(k_max, len(itr), len(xtr) - 1)):
         r = oracle.residual(At, bt, xtr[k])
         if rtr is not None:
-            _check_r(rtr[k], r, k)
+            E = 2 * (At.shape[1] + 2) * 2.0**-53 * (np.abs(bt) + np.abs(At) @ np.abs(xtr[k]))
+            _check_r(rtr[k], r, k, E)
         mask = nsq > 0
         sc = np.where(mask, r * r / np.where(mask, nsq, 1), -1.0)
         io = int(np.argmax(sc))
@@ -224,7 +231,9 @@ def test_solve_parity_small_configs(csk, name):
     # every iteration, including the residual at the returned iterate (IT + 1 vectors)
     assert len(g.r_trace) == g.iterations + 1
     _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 4000, g.r_trace)
-    _check_r(_np(g.r_trace)[g.iterations], oracle.residual(_np(At), _np(bt), _np(g.x)), g.iterations)
+    Atn, btn, xn = _np(At), _np(bt), _np(g.x)
+    E = 2 * (cfg.n + 2) * 2.0**-53 * (np.abs(btn) + np.abs(Atn) @ np.abs(xn))
+    _check_r(_np(g.r_trace)[g.iterations], oracle.residual(Atn, btn, xn), g.iterations, E)
     n_same = min(len(g.idx_trace), len(o.idx_trace))
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
     assert abs(g.final_res - oracle.solve(_np(At), _np(bt), _np(nsq), x0=_np(g.x), x_star=_np(p.x_star), max_iters=0).final_res) <= 1e-12
@@ -544,10 +553,12 @@ def test_sketch_csr_bitexact(csk, m, n, d, k):
     assert np.all(np.abs(_np(nsq) - nsq_o) <= 2 * n * U * nsq_o)
 
 
-@pytest.mark.parametrize("m,n,d,maxlen", [(5000, 300, 400, 70), (3000, 1500, 50, 40)])
+@pytest.mark.parametrize("m,n,d,maxlen", [(5000, 300, 400, 70), (3000, 1500, 50, 40), (2000, 1500, 30, 700),
+                                           (4000, 2001, 3999, 1200), (600, 64, 7, 64)])
 def test_sketch_csr_ragged_rows(csk, m, n, d, maxlen):
-    """CSR rows of 0..maxlen stored pairs (empty rows, rows past one 32-pair batch load, unsorted
-    bucket sizes): the batched CSR kernel folds every row in ascending order."""
+    """CSR rows of 0..maxlen stored pairs (empty rows and buckets, rows longer than one 256-pair
+    gather stage -- split over several batches --, many rows per bucket, odd n, unsorted bucket
+    sizes): the staged CSR kernel folds every column in ascending row order."""
     g = np.random.default_rng(m + n)
     lens = g.integers(0, maxlen + 1, size=m)
     lens[::97] = 0
