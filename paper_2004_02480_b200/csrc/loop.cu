@@ -105,14 +105,6 @@ __device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long
 __device__ __forceinline__ void red_add_release_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void red_add_relaxed_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -1057,6 +1049,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         if (stop < 0 && mx == 0ull) stop = -2;  // every row masked: zero sketch
                         if (stop >= 0 && wrow >= 0 && lane == 0) mbar_wait(mbar, mphase);  // drain the copy
                     } else {
+                    unsigned long long *pair = p.xch + static_cast<int>(k % 3) * kXchWords;
                     const size_t par_off = static_cast<size_t>(k & 1) * p.Gr * kSlotWords;
                     if (lane == 0) {
                         // (SYS: the slots are read by the other GPUs -- system-scope stores)
@@ -1065,21 +1058,18 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         ll_pack(cl_l, tag, h0, l0);
                         ll_pack(cl_s, tag, h1, l1);
                         if constexpr (!SYS) {
-                            // one GPU: the CTA's whole candidate goes into its own LL-tagged slot
-                            // {lambda, score, key, ||r||^2 partial}, then ONE relaxed arrival add on
-                            // a monotonic counter (target G (k+1): no reset, no release fence --
-                            // readers validate every slot they read by its tags)
-                            unsigned long long h2, l2;
-                            ll_pack(__longlong_as_double(static_cast<long long>(kc)), tag, h2, l2);
+                            if (lead) {
+                                st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords, 0ull, 0ull);
+                                if (RESMODE) st_relaxed_v2_u64(p.xch + ((k + 1) % 3) * kXchWords + 2, 0ull, 0ull);
+                            }
+                            red_max_u64(pair + 1, kc);
+                            // residual stop: ||r_k||^2 accumulates beside the count (one sum,
+                            // read by every CTA in the same load as the count)
+                            if (RESMODE) red_add_f64(reinterpret_cast<double *>(pair + 2), crr);
+                            red_add_release_u64(pair, 1ull);  // orders the max, sum (and reset) before the count
+                            // the slot needs no ordering: readers validate its LL tags
                             st_relaxed_v2_u64(my, h0, l0);
                             st_relaxed_v2_u64(my + 2, h1, l1);
-                            st_relaxed_v2_u64(my + 4, h2, l2);
-                            if (RESMODE) {
-                                unsigned long long h3, l3;
-                                ll_pack(crr, tag, h3, l3);
-                                st_relaxed_v2_u64(my + 6, h3, l3);
-                            }
-                            red_add_relaxed_u64(p.xch, 1ull);
                         } else {
                             // across GPUs, in two levels: this rank's CTAs meet on a pair in this
                             // rank's memory (GPU scope: a system-scope release costs microseconds);
@@ -1105,7 +1095,6 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
 #endif
                     unsigned long long c = 0ull, mx = 0ull, rsum = 0ull;
-                    int wslot = 0;  // (one GPU) the winning CTA's slot
                     unsigned long long t_spin = 0ull;
                     uint32_t spins = 0u;
                     bool timed_out = false;
@@ -1159,66 +1148,18 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         }
                         timed_out = __any_sync(0xffffffffu, timed_out);
                         c = static_cast<unsigned long long>(G);
-                    } else {
-                        // relaxed polls of the arrival count (an acquire load would invalidate L1
-                        // on every poll); G (k + 1) arrivals <=> every CTA published iteration k
-                        // (a CTA adds for k + 1 only after it saw all of iteration k's arrivals)
-                        const unsigned long long target = static_cast<unsigned long long>(k + 1) * static_cast<unsigned long long>(G);
-                        do {
-                            c = ld_relaxed_u64(p.xch);
-                            if (c < target && watchdog()) break;
-                        } while (c < target);
-                        // then every slot's key (and ||r||^2 partial): lane l reads the slots
-                        // l, l + 32, ... (all loads in flight at once), re-reading a slot whose
-                        // tags are stale (its stores may trail the count); the argmax key picks
-                        // the winning slot, and the partials add in slot order (fixed: identical
-                        // bits in every CTA and every run)
-                        constexpr int KU = 5;
-                        int wsl = 0;
-                        double rs_l = 0.0;
-                        const unsigned long long *sl0 = p.slots + par_off;
-                        for (int s0 = 0; s0 < G && !timed_out; s0 += 32 * KU) {
-                            unsigned long long kh[KU], kl[KU], rh[KU], rl[KU];
-#pragma unroll
-                            for (int u = 0; u < KU; ++u) {
-                                const int sidx = s0 + 32 * u + lane;
-                                kh[u] = kl[u] = rh[u] = rl[u] = 0ull;
-                                if (sidx < G) {
-                                    ld_relaxed_v2(sl0 + static_cast<size_t>(sidx) * kSlotWords + 4, kh[u], kl[u]);
-                                    if (RESMODE) ld_relaxed_v2(sl0 + static_cast<size_t>(sidx) * kSlotWords + 6, rh[u], rl[u]);
-                                }
-                            }
-#pragma unroll
-                            for (int u = 0; u < KU; ++u) {
-                                const int sidx = s0 + 32 * u + lane;
-                                if (sidx < G) {
-                                    const unsigned long long *sp = sl0 + static_cast<size_t>(sidx) * kSlotWords;
-                                    while (!ll_ok(kh[u], kl[u], tag) && !watchdog()) ld_relaxed_v2(sp + 4, kh[u], kl[u]);
-                                    const unsigned long long key =
-                                        static_cast<unsigned long long>(__double_as_longlong(ll_val(kh[u], kl[u])));
-                                    if (key > mx) { mx = key; wsl = sidx; }
-                                    if (RESMODE) {
-                                        while (!ll_ok(rh[u], rl[u], tag) && !watchdog()) ld_relaxed_v2(sp + 6, rh[u], rl[u]);
-                                        rs_l = rs_l + ll_val(rh[u], rl[u]);
-                                    }
-                                }
-                            }
-                        }
-                        timed_out = __any_sync(0xffffffffu, timed_out);
-                        unsigned long long gmx;
-                        const int wl = warp_max_key_lane(mx, gmx);
-                        wsl = __shfl_sync(0xffffffffu, wsl, wl);
-                        mx = gmx;
-                        wslot = wsl;
-                        if (RESMODE) rsum = static_cast<unsigned long long>(__double_as_longlong(lwarp_sum(rs_l)));
-                    }
+                    } else do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
+                        if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
+                        else ld_relaxed_v2(pair, c, mx);
+                        if (c < static_cast<unsigned long long>(G) && watchdog()) break;
+                    } while (c < static_cast<unsigned long long>(G));
                     if (timed_out) {
                         stop = -3;
                         mx = 0ull;
                     }
-                    // no acquire fence: A~, b~ are immutable and slots are LL-validated; (SYS) the
+                    // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the
                     // proxy fence orders this thread's generic view before its TMA reads
-                    if constexpr (SYS) fence_proxy_async_global();
+                    fence_proxy_async_global();
                     LP(3)
 #if CSK_PHASE_PROF
                     if (p.skew && lane == 0 && k >= 8 && k < 72) {
@@ -1234,8 +1175,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                             // owner: rank by the row ranges, then its CTA
                             const unsigned long long *oslot;
                             const double *orow;
-                            if constexpr (!SYS) {  // one GPU: the slot the key came from
-                                oslot = p.slots + par_off + static_cast<size_t>(wslot) * kSlotWords;
+                            if (p.rm_magic != 0ull) {  // one rank: CTA = row / RM by a multiply-shift
+                                const uint32_t olc = static_cast<uint32_t>((static_cast<unsigned long long>(wrow) * p.rm_magic) >> 40);
+                                oslot = p.slots + par_off + static_cast<size_t>(olc) * kSlotWords;
                                 orow = p.At + wrow * n;
                             } else {
                                 int orank = 0;
@@ -1272,13 +1214,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     }
                     LP(9)
                     if (RESMODE && stop == -1) {  // (not after a watchdog timeout: stop = -3 stands)
-                        // ||r_k||^2.  One GPU: the G CTA partials from the slots, in slot order.
-                        // Across ranks: each rank's CTA partials summed beside its count (arrival
-                        // order), then the ranks' sums in rank order; there the 32-byte poll reads
-                        // {count, max, sum} from one L2 sector in one access (a hardware property
-                        // relied on, not a PTX guarantee).  tests/test_gpu_parity.py
+                        // ||r_k||^2: each rank's CTA partials summed beside its count (arrival
+                        // order); across ranks the ranks' sums in rank order.  The 32-byte poll
+                        // reads {count, max, sum} from one L2 sector in one access (a hardware
+                        // property relied on here, not a PTX guarantee: the count reaching G comes
+                        // with every CTA's red.add of the sum); tests/test_gpu_parity.py
                         // test_residual_sum_complete checks RES_k against the traced r_k every
-                        // iteration, where a missing partial would show up as a ~1/G deficit
+                        // iteration, where a missing CTA partial would show up as a ~1/G deficit
                         const double t = __longlong_as_double(static_cast<long long>(rsum));
                         res = bb > 0.0 ? t / bb : t;
                         if (lead && lane == 0 && p.res_trace && k < p.trace_cap) p.res_trace[k] = res;

@@ -524,26 +524,28 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
 // val, 4-byte col, no registers held) into one of kCsrS shared-memory stages, so kCsrS batches'
 // HBM reads are in flight per warp while the oldest one is folded.  Row descriptors (perm entry,
 // row_ptr pair, b) are loaded 32 rows at a time, one window ahead (perm two windows ahead).
-// The fold adds 32 pairs per step into the accumulator row: pairs that hit the same column (from
-// different rows -- a row's columns are distinct) are serialised in pair order (= row order) with
-// __match_any_sync ranks, so every column is the sequential ascending-row fold of the oracle.
+// The fold adds 32 pairs per step into the accumulator row.  Two pairs of one step can hit the
+// same column only if they come from different rows (a row's columns are distinct): a per-warp
+// byte array of lane stamps (every lane writes its id at its column, then reads it back) detects
+// that case in four instructions, and only such steps take the ordered path (__match_any_sync
+// ranks, earlier pair = earlier row first), so every column is the ascending-row fold.
 // b~ is folded at batch formation (row order), the A~ row is stored (coalesced 16-byte stores)
 // and its norm formed when the bucket's last batch has been folded.
 constexpr int kCsrS = 4;                                       // stages (batches in flight) per warp
-constexpr int kCsrSP = 256;                                    // pairs per stage
+constexpr int kCsrSP = 128;                                    // pairs per stage
 constexpr int kCsrStageBytes = kCsrSP * (8 + 4 + 1);           // val | col | sign
 constexpr int kCsrMetaBytes = kCsrS * 16;
 constexpr int kCsrMaxWarps = 16;
 
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_n(int pending) {  // pending in [0, kCsrS)
-    static_assert(kCsrS == 4, "cp_async_wait_n covers 0..3");
+    static_assert(kCsrS <= 4, "cp_async_wait_n covers 0..3");
     switch (pending) {
         case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
         case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
@@ -556,12 +558,13 @@ __global__ void __launch_bounds__(kCsrMaxWarps * 32, 1)
 k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const double *__restrict__ val,
              const double *__restrict__ b, int64_t m, int64_t n, int64_t d, const int32_t *__restrict__ perm,
              const int32_t *__restrict__ offsets, double *__restrict__ At, double *__restrict__ bt,
-             double *__restrict__ nsq, int64_t acc_stride, int warp_bytes, int vec) {
+             double *__restrict__ nsq, int64_t acc_stride, int stamp_bytes, int warp_bytes, int vec) {
     extern __shared__ __align__(16) unsigned char csr_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char *ws = csr_smem + static_cast<size_t>(warp) * warp_bytes;
     double *acc = reinterpret_cast<double *>(ws);
-    unsigned char *stg = ws + acc_stride * 8;
+    unsigned char *stamp = ws + acc_stride * 8;  // [stamp_bytes]: lane id per column (conflict test)
+    unsigned char *stg = stamp + stamp_bytes;
     int *meta = reinterpret_cast<int *>(stg + kCsrS * kCsrStageBytes);  // [kCsrS][4]: pairs, bucket, end
     for (int64_t k = lane; k < acc_stride; k += 32) acc[k] = 0.0;
     __syncwarp();
@@ -630,61 +633,71 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
         const int64_t wend = (wbase + 32 < fe) ? wbase + 32 : fe;
         const int ra = static_cast<int>(wend - t);  // rows of bucket fj left in this window (>= 1)
         const bool inr = lane >= cur && lane < cur + ra;
-        const int64_t len = re - rs;
         const int64_t skip = (lane == cur) ? roff : 0;
-        int64_t cnt = inr ? len - skip : 0;
-        // inclusive scan of the counts (int64: any row length)
-        int64_t inc = cnt;
+        const int64_t rem = re - rs - skip;
+        // pair counts clamped to kCsrSP + 1 (a longer row is taken in kCsrSP slices), inclusive scan
+        int cnt = inr ? static_cast<int>(rem < kCsrSP + 1 ? rem : kCsrSP + 1) : 0;
+        int inc = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        const int64_t first = __shfl_sync(0xffffffffu, cnt, cur);
-        int k;            // whole rows taken
-        bool partial;     // a slice of the (long) row at cur
-        int64_t P;
-        if (first > kCsrSP) {
-            partial = true;
-            k = 0;
-            P = kCsrSP;
-            cnt = (lane == cur) ? kCsrSP : 0;
-            inc = (lane >= cur) ? kCsrSP : 0;
-        } else {
-            partial = false;
-            k = __popc(__ballot_sync(0xffffffffu, inr && inc <= kCsrSP));
-            P = __shfl_sync(0xffffffffu, inc, cur + k - 1);
-            if (lane >= cur + k) { cnt = 0; inc = P; }
-        }
-        const int64_t ex = inc - cnt;
-        const int64_t start = rs + skip;
+        const int first = __shfl_sync(0xffffffffu, cnt, cur);
+        const bool partial = first > kCsrSP;  // a slice of the (long) row at cur
+        const int k = partial ? 0 : __popc(__ballot_sync(0xffffffffu, inr && inc <= kCsrSP));  // whole rows
+        const int P = partial ? kCsrSP : __shfl_sync(0xffffffffu, inc, cur + k - 1);
+        const bool mine = lane >= cur && lane < cur + (partial ? 1 : k);
+        const int mcnt = mine ? (partial ? kCsrSP : cnt) : 0;
+        const int moff = inc - cnt;  // first stage slot of this lane's row
+        const int64_t mstart = rs + skip;
         const bool neg = pr < 0;
         double *sv = reinterpret_cast<double *>(stg + slot * kCsrStageBytes);
         int32_t *sc = reinterpret_cast<int32_t *>(stg + slot * kCsrStageBytes + kCsrSP * 8);
         unsigned char *sg = stg + slot * kCsrStageBytes + kCsrSP * 12;
-        for (int q0 = 0; q0 < static_cast<int>(P); q0 += 32) {
-            const int q = q0 + lane;
-            int r = 0;  // the row of pair q: smallest lane r with inc_r > q
-#pragma unroll
-            for (int st = 16; st >= 1; st >>= 1) {
-                const int64_t v = __shfl_sync(0xffffffffu, inc, r + st - 1);
-                if (v <= q) r += st;
+        const int maxc = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(mcnt)));
+        if (maxc <= 32) {
+            // short rows: lane r gathers the pairs of its own row (pair kk of every row per step;
+            // .ca: a row's later pairs come from the line the first one brought into L1)
+            const uint32_t dv = smem_u32(sv + moff), dc = smem_u32(sc + moff);
+            const double *gv = val + mstart;
+            const int32_t *gc = col + mstart;
+            unsigned char *gs = sg + moff;
+            const unsigned char ngb = neg ? 1 : 0;
+            for (int kk = 0; kk < maxc; ++kk) {
+                if (kk < mcnt) {
+                    cp_async8(dv + 8u * kk, gv + kk);
+                    cp_async4(dc + 4u * kk, gc + kk);
+                    gs[kk] = ngb;
+                }
             }
-            const int64_t s0 = __shfl_sync(0xffffffffu, start, r);
-            const int64_t e0 = __shfl_sync(0xffffffffu, ex, r);
-            const bool ng = __shfl_sync(0xffffffffu, neg, r);
-            if (q < P) {
-                const int64_t off = s0 + (q - e0);
-                cp_async8(sv + q, val + off);
-                cp_async4(sc + q, col + off);
-                sg[q] = ng ? 1 : 0;
+        } else {
+            // long rows: the warp strides over one row at a time
+            for (int r = cur; r < cur + (partial ? 1 : k); ++r) {
+                const int64_t s0 = __shfl_sync(0xffffffffu, mstart, r);
+                const int c0 = __shfl_sync(0xffffffffu, mcnt, r);
+                const int o0 = __shfl_sync(0xffffffffu, moff, r);
+                const bool ng = __shfl_sync(0xffffffffu, neg, r);
+                for (int q = lane; q < c0; q += 32) {
+                    cp_async8(smem_u32(sv + o0 + q), val + s0 + q);
+                    cp_async4(smem_u32(sc + o0 + q), col + s0 + q);
+                    sg[o0 + q] = ng ? 1 : 0;
+                }
             }
         }
         cp_async_commit();
-        // b~: the rows that START in this batch, ascending (the oracle's fold order)
+        // b~: the rows that START in this batch, ascending (the oracle's fold order); the
+        // shuffles are batched ahead of the dependent adds
         const double bs = neg ? -bv : bv;
         const int rf = roff > 0 ? cur + 1 : cur, rl = partial ? cur + 1 : cur + k;
-        for (int r = rf; r < rl; ++r) bacc = bacc + __shfl_sync(0xffffffffu, bs, r);
+        for (int r0 = rf; r0 < rl; r0 += 8) {
+            double bb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) bb[u] = __shfl_sync(0xffffffffu, bs, (r0 + u) & 31);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (r0 + u < rl) bacc = bacc + bb[u];
+        }
         if (partial) {
             roff += kCsrSP;
         } else {
@@ -726,19 +739,37 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
         const double *sv = reinterpret_cast<const double *>(stg + slot * kCsrStageBytes);
         const int32_t *sc = reinterpret_cast<const int32_t *>(stg + slot * kCsrStageBytes + kCsrSP * 8);
         const unsigned char *sg = stg + slot * kCsrStageBytes + kCsrSP * 12;
+        // 32 pairs per window; the next window's loads are issued before this window's adds
+        int c0 = lane < P ? sc[lane] : -1;
+        double v0 = lane < P ? sv[lane] : 0.0;
+        if (lane < P && sg[lane]) v0 = -v0;
         for (int q0 = 0; q0 < P; q0 += 32) {
-            const int q = q0 + lane;
-            const bool ok = q < P;
-            const int c = ok ? sc[q] : -1 - lane;
-            double v = ok ? sv[q] : 0.0;
-            if (ok && sg[q]) v = -v;
-            const unsigned same = __match_any_sync(0xffffffffu, c);
-            const unsigned rank = __popc(same & lt);  // earlier pairs (rows) on the same column
-            const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
-            for (unsigned rr = 0; rr <= maxr; ++rr) {
-                if (ok && rank == rr) acc[c] = acc[c] + v;
-                __syncwarp();
+            const int q1 = q0 + 32 + lane;
+            int c1 = -1;
+            double v1 = 0.0;
+            if (q1 < P) {
+                c1 = sc[q1];
+                v1 = sv[q1];
+                if (sg[q1]) v1 = -v1;
             }
+            if (c0 >= 0) stamp[c0] = static_cast<unsigned char>(lane);
+            __syncwarp();
+            const bool clash = c0 >= 0 && stamp[c0] != lane;
+            if (!__any_sync(0xffffffffu, clash)) {
+                if (c0 >= 0) acc[c0] = acc[c0] + v0;  // distinct columns: one step
+            } else {
+                // a column shared by pairs of different rows: ranks by pair (= row) order
+                const unsigned same = __match_any_sync(0xffffffffu, c0 >= 0 ? c0 : -1 - lane);
+                const unsigned rank = __popc(same & lt);
+                const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+                for (unsigned rr = 0; rr <= maxr; ++rr) {
+                    if (c0 >= 0 && rank == rr) acc[c0] = acc[c0] + v0;
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            c0 = c1;
+            v0 = v1;
         }
         if (end) {  // bucket jb complete: store the A~ row, its norm, clear the accumulator
             double part = 0.0;
@@ -860,16 +891,20 @@ csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int3
                                int64_t d, const int32_t *perm, const int32_t *offsets,
                                double *At, double *bt, double *nsq, cudaStream_t stream) {
     const int64_t stride = (n + 1) & ~int64_t(1);  // accumulator doubles (16-byte multiple)
-    const int64_t wb = ((stride * 8 + kCsrS * kCsrStageBytes + kCsrMetaBytes) + 127) & ~int64_t(127);
+    const int64_t stampb = (n + 15) & ~int64_t(15);  // conflict stamps: one byte per column
+    const int64_t wb = ((stride * 8 + stampb + kCsrS * kCsrStageBytes + kCsrMetaBytes) + 127) & ~int64_t(127);
     int warps = static_cast<int>(ctx->max_smem_optin / wb);
     if (warps > kCsrMaxWarps) warps = kCsrMaxWarps;
     if (warps < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
     const size_t smem = static_cast<size_t>(warps) * wb;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_csr)));
     const int vec = (n % 2 == 0 && aligned16(At)) ? 1 : 0;
+    // experiment knob: the L2 fetch granularity for the random (col, val) / row_ptr / b gathers
+    static const char *gran = getenv("CSK_L2_FETCH_GRAN");
+    if (gran) CSK_CUDA(ctx, cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(gran))));
     time_mark(ctx, 0, false, stream);
     k_sketch_csr<<<ctx->num_sms, warps * 32, smem, stream>>>(row_ptr, col, val, b, m, n, d, perm, offsets, At, bt,
-                                                            nsq, stride, static_cast<int>(wb), vec);
+                                                            nsq, stride, static_cast<int>(stampb), static_cast<int>(wb), vec);
     time_mark(ctx, 0, true, stream);
     CSK_CUDA(ctx, cudaGetLastError());
     return CSK_OK;

@@ -54,10 +54,15 @@ def main():
         if a.startswith("--configs="):
             configs = a.split("=", 1)[1]
         else:
-            libs.append(os.path.abspath(a))
+            path, sep, envs = a.partition(":")
+            libs.append(os.path.abspath(path) + sep + envs)
     res = {}
     for lib in libs:
-        env = dict(os.environ, CSK_LIB=lib)
+        path, _, envs = lib.partition(":")
+        env = dict(os.environ, CSK_LIB=path)
+        for kv in filter(None, envs.split(",")):
+            k, v = kv.split("=", 1)
+            env[k] = v
         o = subprocess.run([sys.executable, os.path.abspath(__file__), "--child", configs], env=env,
                            capture_output=True, text=True)
         line = [x for x in o.stdout.splitlines() if x.startswith("RESULT ")]

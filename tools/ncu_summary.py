@@ -42,6 +42,40 @@ def main(rep):
         rs = sorted([(int(x[I[c]] or 0), c) for c in stall_cols], reverse=True)[:2]
         print(f"  {s:8d} {100 * s / tot:5.1f}%  {x[1].strip()[:60]:60s} {rs}")
 
+    by_line(rep)
+
+
+def by_line(rep, top=25):
+    """Per CUDA source line (-lineinfo): instructions executed and stall samples, top lines."""
+    out = ncu(rep, "--page", "source", "--csv", "--print-source=cuda,sass")
+    fname, hdr, lines = "", None, []
+    for row in csv.reader(io.StringIO(out)):
+        if not row:
+            continue
+        if row[0] == "File Path":
+            fname = row[1].split("/")[-1]
+            continue
+        if row[0] == "Line No":
+            hdr = {k: i for i, k in enumerate(row)}
+            continue
+        if hdr is None or not row[0]:
+            continue
+        try:
+            ie = int(row[hdr["Instructions Executed"]] or 0)
+            sm = int(row[hdr["Warp Stall Sampling (All Samples)"]] or 0)
+        except (ValueError, KeyError, IndexError):
+            continue
+        lines.append((fname, int(row[0]), row[1].strip(), ie, sm))
+    if not lines:
+        return
+    ti = sum(x[3] for x in lines) or 1
+    ts = sum(x[4] for x in lines) or 1
+    print(f"\nby source line (instructions executed {ti}, stall samples {ts}):")
+    print("  inst%  stall%  file:line  source")
+    keep = sorted(lines, key=lambda x: -(x[3] / ti + x[4] / ts))[:top]
+    for f, ln, src, ie, sm in keep:
+        print(f"  {100 * ie / ti:5.1f}  {100 * sm / ts:5.1f}   {f}:{ln}  {src[:90]}")
+
 
 if __name__ == "__main__":
     main(sys.argv[1])
