@@ -792,8 +792,81 @@ def run_sharded(args, dist, rank, ws):
                       "d2h_bytes_per_step": 8 * cfg.n,
                       "api": "csk_sketch_sharded + csk_solve_sharded (binding over the C ABI), pinned host shards "
                              "per rank; max over ranks"}
+    if not args.no_extras:
+        out["per_config"] = sharded_extras(csk, ctx, dist, rank, ws)
     csk.comm_destroy(ctx)
     return out
+
+
+def sharded_extras(csk, ctx, dist, rank, ws, reps=2):
+    """N ranks on north_star's multi-GPU configs: C4 (dense 8 GB, S9 reduce-scatter + S10, the 50k
+    cap) and C5 (CSR, S9 by row routing -- bit-identical to one GPU -- + S10 to RES <= 1e-6).  Each
+    rank draws the same problem and keeps its row shard; CUDA events, max over ranks."""
+    from paper_2004_02480_b200.parallel import row_shard
+    hbm_peak, sm_max_mhz, _ = _peaks()
+    smem_peak = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
+    dev = torch.device("cuda", torch.cuda.current_device())
+    res = {}
+    for name in ("C4", "C5"):
+        cfg = CONFIGS[name]
+        p = make_config(cfg, dev)
+        lo, hi = row_shard(cfg.m, ws, rank)
+        if cfg.kind == "csr":
+            rp_l = p.row_ptr[lo:hi + 1].contiguous()
+            col, val = p.col, p.val
+            b_l = p.b[lo:hi].contiguous()
+            sk_bytes = 12 * (int(p.row_ptr[hi]) - int(p.row_ptr[lo])) + 16 * (hi - lo) + 8 * cfg.d * cfg.n // ws
+        else:
+            A_l = p.A[lo:hi].contiguous()
+            b_l = p.b[lo:hi].contiguous()
+            del p.A
+            sk_bytes = 8 * (hi - lo) * (cfg.n + 1) + 8 * cfg.d * cfg.n // ws
+        xs = p.x_star
+        torch.cuda.empty_cache()
+        rows = []
+        for k in range(reps + 1):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            _barrier(dist)
+            torch.cuda.synchronize()
+            e[0].record()
+            if cfg.kind == "csr":
+                At, bt, nsq, dlo, dhi = csk.csk_sketch_csr_sharded(rp_l, col, val, b_l, lo, cfg.m, cfg.n, cfg.d, ws,
+                                                                   rank, seed=cfg.sketch_seed,
+                                                                   mode=csk.SHARD_ROUTE_ROWS, ctx=ctx)
+            else:
+                At, bt, nsq, dlo, dhi = csk.csk_sketch_sharded(A_l, b_l, lo, cfg.m, cfg.d, ws, rank,
+                                                               seed=cfg.sketch_seed, ctx=ctx)
+            e[1].record()
+            x, rep = csk.csk_solve_sharded(At, bt, nsq, dlo, dhi, cfg.d, cfg.n, x_star=xs, tol=cfg.tol,
+                                           max_iters=cfg.max_iters, ctx=ctx)
+            e[2].record()
+            torch.cuda.synchronize()
+            kl = csk.csk_last_kernel_ms("loop", ctx=ctx)
+            if k:
+                rows.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), kl, rep))
+            del At, bt, nsq, x
+        sk = _max_over_ranks(dist, statistics.median(r[0] for r in rows))
+        sv = _max_over_ranks(dist, statistics.median(r[1] for r in rows))
+        kl = _max_over_ranks(dist, statistics.median(r[2] for r in rows))
+        rep = rows[-1][3]
+        it = max(rep.iterations, 1)
+        loc_rows = -(-cfg.d // ws)
+        loop_gbs = (8 * loc_rows * cfg.n + 16 * loc_rows) * it / (kl * 1e-3) / 1e9
+        res[name] = {"ms_per_step": round(sk + sv, 4), "sketch_ms": round(sk, 4), "solve_ms": round(sv, 4),
+                     "iterations": rep.iterations, "final_res": rep.final_res,
+                     "termination": ["converged", "max_iters", "stagnated"][rep.termination],
+                     "us_per_iteration": round(sv * 1e3 / it, 3),
+                     "sketch": {"mode": "row routing (bit-identical to 1 GPU)" if cfg.kind == "csr" else
+                                "reduce-scatter of partial A~", "bytes_per_rank": sk_bytes,
+                                "achieved_gbs_per_rank": round(sk_bytes / (sk * 1e-3) / 1e9, 1),
+                                "frac_of_hbm": round(sk_bytes / (sk * 1e-3) / 1e9 / hbm_peak, 4)},
+                     "loop_roofline_per_rank": {"bound": "smem", "achieved": round(loop_gbs, 1),
+                                                "peak": round(smem_peak, 1), "unit": "GB/s",
+                                                "frac": round(loop_gbs / smem_peak, 4), "kernel_ms": round(kl, 4)},
+                     "note": "S9 + S10 at N ranks; the loop's exchange is one key per rank over NVLink per iteration"}
+        del p
+        torch.cuda.empty_cache()
+    return res
 
 
 def main():

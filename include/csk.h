@@ -263,6 +263,37 @@ CSK_API csk_status_t csk_sketch_sharded(csk_ctx_t ctx, const double *A_local, in
                                         double *nsq_local, int64_t *d_lo, int64_t *d_hi,
                                         void *stream);
 
+/* S9 for CSR input (config C5: "sketch and iteration row-sharded").  This rank holds rows
+ * [row_offset, row_offset + m_local) of the CSR matrix: row_ptr (int64[m_local + 1]) indexes the
+ * given col (int32) / val (fp64) arrays (absolute offsets; any base), b_local fp64[m_local].  Rows
+ * are hashed with their GLOBAL index.  On return this rank owns A~ rows [*d_lo, *d_hi) =
+ * csk_shard_range(d, P, rank) in A_tilde_local ((d_hi - d_lo) x n), b~ in b_tilde_local and, if
+ * nsq_local != NULL, their norms.  mode:
+ *   CSK_SHARD_REDUCE_SCATTER  partial (A~ | b~) over all d buckets, ncclReduceScatter(sum)
+ *                             (north_star; equal to P = 1 up to summation order);
+ *   CSK_SHARD_ROUTE_ROWS      every row is sent to the owner of its bucket (grouped ncclSend /
+ *                             ncclRecv: the CSR bytes, not d x n partials) and the owner folds
+ *                             its buckets in ascending global row order: BIT-IDENTICAL to P = 1
+ *                             (the C5 variant).
+ * Collective: every rank must call it with the same mode.  Blocks (a count exchange). */
+#define CSK_SHARD_REDUCE_SCATTER 0
+#define CSK_SHARD_ROUTE_ROWS 1
+CSK_API csk_status_t csk_sketch_csr_sharded(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col,
+                                            const double *val, const double *b_local, int64_t m_local,
+                                            int64_t row_offset, int64_t m, int64_t n, int64_t d,
+                                            uint64_t seed, int32_t mode, double *A_tilde_local,
+                                            double *b_tilde_local, double *nsq_local, int64_t *d_lo,
+                                            int64_t *d_hi, void *stream);
+
+/* The row-routing decomposition with `nranks` virtual ranks on this one GPU (test hook): the rows
+ * are split into nranks contiguous shards, each shard packed by destination owner (the buffers
+ * CSK_SHARD_ROUTE_ROWS hands to NCCL), moved by device copies, and every owner's bucket range
+ * sketched into A_tilde (d x n) / b_tilde / nsq (full size).  Must equal csk_sketch_csr bit for bit. */
+CSK_API csk_status_t csk_sketch_csr_routed_virtual(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col,
+                                                   const double *val, const double *b, int64_t m, int64_t n,
+                                                   int64_t d, uint64_t seed, int32_t nranks, double *A_tilde,
+                                                   double *b_tilde, double *nsq, void *stream);
+
 /* S10: Algorithm 1 with the rows of A~ sharded across ranks (rows [d_lo, d_hi) here) and x
  * replicated.  Per iteration: local GEMV + argmax, one ncclAllGather of (score, global row,
  * lambda, sum r^2, winning local row), identical winner/update on every rank (ties -> lowest

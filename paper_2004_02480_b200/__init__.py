@@ -117,6 +117,8 @@ def _extend_sharded(lib):
         "csk_solve_virtual_ranks": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P, ctypes.POINTER(Report), P], i32),
         "csk_solve_virtual_ranks_ex": ([P, P, P, P, i64, i64, i32, P, P, dbl, i64, P, ctypes.POINTER(SolveOpts),
                                         ctypes.POINTER(Report), P], i32),
+        "csk_sketch_csr_sharded": ([P, P, P, P, P, i64, i64, i64, i64, i64, u64, i32, P, P, P, pi64, pi64, P], i32),
+        "csk_sketch_csr_routed_virtual": ([P, P, P, P, P, i64, i64, i64, u64, i32, P, P, P, P], i32),
     }
     for name, (args, res) in extra.items():
         fn = getattr(lib, name)
@@ -500,6 +502,53 @@ def csk_sketch_sharded(A_local, b_local, row_offset: int, m: int, d: int, nranks
                                      ml, row_offset, m, n, d, seed & (2**64 - 1), _ptr(At), _ptr(bt), _ptr(nsq),
                                      ctypes.byref(dlo), ctypes.byref(dhi), _stream()))
     return At[:rows], bt[:rows], nsq[:rows], dlo.value, dhi.value
+
+
+SHARD_REDUCE_SCATTER, SHARD_ROUTE_ROWS = 0, 1
+
+
+def csk_sketch_csr_sharded(row_ptr, col, val, b_local, row_offset: int, m: int, n: int, d: int, nranks: int,
+                           rank: int, seed: int = 0, mode: int = SHARD_ROUTE_ROWS, ctx: Context | None = None):
+    """S9 for CSR input: this rank's rows [row_offset, row_offset + len(b_local)) -> its bucket rows of
+    (A~, b~, nsq).  mode SHARD_ROUTE_ROWS (rows to their bucket owners; bit-identical to one GPU) or
+    SHARD_REDUCE_SCATTER (partial A~ + ncclReduceScatter)."""
+    ctx = ctx or default_context()
+    _need(row_ptr, torch.int64, "row_ptr", 1)
+    _need(col, torch.int32, "col", 1)
+    _need(val, torch.float64, "val", 1)
+    _need(b_local, torch.float64, "b_local", 1)
+    ml = row_ptr.shape[0] - 1
+    lo, hi = shard_range(d, nranks, rank)
+    rows = max(hi - lo, 0)
+    dev = val.device
+    At = torch.empty(max(rows, 1), n, dtype=torch.float64, device=dev)
+    bt = torch.empty(max(rows, 1), dtype=torch.float64, device=dev)
+    nsq = torch.empty(max(rows, 1), dtype=torch.float64, device=dev)
+    dlo, dhi = ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(lib.csk_sketch_csr_sharded(ctx.handle, _ptr(row_ptr.contiguous()), _ptr(col.contiguous()),
+                                         _ptr(val.contiguous()), _ptr(b_local.contiguous()), ml, row_offset, m, n, d,
+                                         seed & (2**64 - 1), int(mode), _ptr(At), _ptr(bt), _ptr(nsq),
+                                         ctypes.byref(dlo), ctypes.byref(dhi), _stream()))
+    return At[:rows], bt[:rows], nsq[:rows], dlo.value, dhi.value
+
+
+def csk_sketch_csr_routed_virtual(row_ptr, col, val, b, n: int, d: int, nranks: int, seed: int = 0,
+                                  ctx: Context | None = None):
+    """The row-routing decomposition of S9 with `nranks` virtual ranks on this GPU (test hook)."""
+    ctx = ctx or default_context()
+    _need(row_ptr, torch.int64, "row_ptr", 1)
+    _need(col, torch.int32, "col", 1)
+    _need(val, torch.float64, "val", 1)
+    _need(b, torch.float64, "b", 1)
+    m = row_ptr.shape[0] - 1
+    At = torch.empty(d, n, dtype=torch.float64, device=val.device)
+    bt = torch.empty(d, dtype=torch.float64, device=val.device)
+    nsq = torch.empty(d, dtype=torch.float64, device=val.device)
+    ctx.check(lib.csk_sketch_csr_routed_virtual(ctx.handle, _ptr(row_ptr.contiguous()), _ptr(col.contiguous()),
+                                                _ptr(val.contiguous()), _ptr(b.contiguous()), m, n, d,
+                                                seed & (2**64 - 1), int(nranks), _ptr(At), _ptr(bt), _ptr(nsq),
+                                                _stream()))
+    return At, bt, nsq
 
 
 def csk_solve_sharded(At_local, bt_local, nsq_local, d_lo: int, d_hi: int, d: int, n: int,

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcsk.so")
 PROF_LIB = os.path.join(PKG, "libcsk_prof.so")  # debug build with the in-kernel phase profiler
-SOURCES = ["api.cu", "plan.cu", "sketch.cu", "loop.cu", "comm.cu"]
+SOURCES = ["api.cu", "plan.cu", "sketch.cu", "loop.cu", "comm.cu", "route.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -465,6 +465,113 @@ csk_status_t csk_sketch_sharded(csk_ctx_t ctx, const double *A_local, int64_t ld
     return CSK_OK;
 }
 
+// S9 for CSR input.  CSK_SHARD_REDUCE_SCATTER: this rank's rows folded into a partial (A~ | b~)
+// over all d buckets (global hashing), then the same grouped ncclReduceScatter as the dense path.
+// CSK_SHARD_ROUTE_ROWS: every row goes to its bucket's owner (route.cu): the counts by an
+// ncclAllGather, the rows and their pairs by grouped ncclSend/ncclRecv (self included), then the
+// owner's plan + CSR sketch over its bucket range -- bit-identical to one GPU.
+csk_status_t csk_sketch_csr_sharded(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col, const double *val,
+                                    const double *b_local, int64_t m_local, int64_t row_offset, int64_t m, int64_t n,
+                                    int64_t d, uint64_t seed, int32_t mode, double *A_tilde_local,
+                                    double *b_tilde_local, double *nsq_local, int64_t *d_lo, int64_t *d_hi,
+                                    void *stream) {
+    if (!ctx || !ctx->comm) return ctx ? fail(ctx, CSK_E_ARG, "csk_sketch_csr_sharded: call csk_comm_create first") : CSK_E_ARG;
+    if (!row_ptr || !col || !val || !b_local || !A_tilde_local || !b_tilde_local || !d_lo || !d_hi || m_local < 0 ||
+        row_offset < 0 || row_offset + m_local > m || m >= (int64_t(1) << 31) || n < 1 || d < 1 || d >= m ||
+        (mode != CSK_SHARD_REDUCE_SCATTER && mode != CSK_SHARD_ROUTE_ROWS))
+        return fail(ctx, CSK_E_ARG, "csk_sketch_csr_sharded: bad arguments (need 1 <= d < m < 2^31, shard inside [0, m))");
+    CSK_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = as_stream(stream);
+    Comm *c = ctx->comm;
+    const int P = c->nranks, me = c->rank;
+    if (P > kMaxRanks || d < P) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr_sharded: need P <= 8 and d >= P");
+    int64_t lo, hi;
+    csk_shard_range(d, P, me, &lo, &hi);
+    *d_lo = lo;
+    *d_hi = hi;
+    if (mode == CSK_SHARD_REDUCE_SCATTER) {
+        const int64_t chunk = (d + P - 1) / P;
+        const int64_t dpad = chunk * P;
+        CSK_CHECK(ensure(ctx, ctx->a_tilde, static_cast<size_t>(dpad) * n * 8 + static_cast<size_t>(chunk) * n * 8));
+        CSK_CHECK(ensure(ctx, ctx->b_tilde, static_cast<size_t>(dpad) * 8 + static_cast<size_t>(chunk) * 8));
+        double *partA = static_cast<double *>(ctx->a_tilde.ptr);
+        double *recvA = partA + dpad * n;
+        double *partb = static_cast<double *>(ctx->b_tilde.ptr);
+        double *recvb = partb + dpad;
+        if (dpad > d) {
+            k_zero_rows<<<64, 256, 0, s>>>(partA + d * n, (dpad - d) * n);
+            k_zero_rows<<<1, 256, 0, s>>>(partb + d, dpad - d);
+        }
+        if (m_local > 0) {
+            int32_t *perm = nullptr, *offsets = nullptr;
+            CSK_CHECK(build_plan(ctx, seed, row_offset, m_local, d, nullptr, nullptr, &perm, &offsets, s));
+            CSK_CHECK(launch_sketch_csr(ctx, row_ptr, col, val, b_local, m_local, n, d, perm, offsets, partA, partb,
+                                        nullptr, s));
+        } else {
+            k_zero_rows<<<64, 256, 0, s>>>(partA, d * n);
+            k_zero_rows<<<1, 256, 0, s>>>(partb, d);
+        }
+        CSK_NCCL(ctx, ncclGroupStart());
+        CSK_NCCL(ctx, ncclReduceScatter(partA, recvA, chunk * n, ncclFloat64, ncclSum, c->nccl, s));
+        CSK_NCCL(ctx, ncclReduceScatter(partb, recvb, chunk, ncclFloat64, ncclSum, c->nccl, s));
+        CSK_NCCL(ctx, ncclGroupEnd());
+        if (hi > lo) {
+            CSK_CUDA(ctx, cudaMemcpyAsync(A_tilde_local, recvA, static_cast<size_t>(hi - lo) * n * 8, cudaMemcpyDeviceToDevice, s));
+            CSK_CUDA(ctx, cudaMemcpyAsync(b_tilde_local, recvb, static_cast<size_t>(hi - lo) * 8, cudaMemcpyDeviceToDevice, s));
+            if (nsq_local) CSK_CHECK(launch_row_norms(ctx, A_tilde_local, hi - lo, n, nsq_local, s));
+        }
+        return CSK_OK;
+    }
+    // ---- row routing ----
+    RoutePack pk;
+    CSK_CHECK(route_pack(ctx, row_ptr, col, val, b_local, m_local, row_offset, d, seed, P, pk, s));
+    int64_t *cnts = nullptr;  // [P][2P] every rank's per-destination counts, + this rank's at the end
+    CSK_CUDA(ctx, cudaMallocAsync(reinterpret_cast<void **>(&cnts), static_cast<size_t>(P + 1) * 2 * P * 8, s));
+    CSK_CUDA(ctx, cudaMemcpyAsync(cnts + static_cast<size_t>(P) * 2 * P, pk.cnt, static_cast<size_t>(2 * P) * 8,
+                                  cudaMemcpyHostToDevice, s));
+    CSK_NCCL(ctx, ncclAllGather(cnts + static_cast<size_t>(P) * 2 * P, cnts, 2 * P, ncclInt64, c->nccl, s));
+    std::vector<int64_t> all(static_cast<size_t>(P) * 2 * P);
+    CSK_CUDA(ctx, cudaMemcpyAsync(all.data(), cnts, all.size() * 8, cudaMemcpyDeviceToHost, s));
+    CSK_CUDA(ctx, cudaStreamSynchronize(s));
+    CSK_CUDA(ctx, cudaFreeAsync(cnts, s));
+    RouteRecv rv;
+    rv.P = P;
+    for (int q = 0; q < P; ++q) {
+        rv.rbase[q + 1] = rv.rbase[q] + all[static_cast<size_t>(q) * 2 * P + 2 * me];
+        rv.pbase[q + 1] = rv.pbase[q] + all[static_cast<size_t>(q) * 2 * P + 2 * me + 1];
+    }
+    const int64_t M = rv.rbase[P], NNZ = rv.pbase[P];
+    void *buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    const size_t sz[5] = {static_cast<size_t>(M) * 4, static_cast<size_t>(M) * 8, static_cast<size_t>(M) * 8,
+                          static_cast<size_t>(NNZ) * 4, static_cast<size_t>(NNZ) * 8};
+    for (int a = 0; a < 5; ++a) CSK_CUDA(ctx, cudaMallocAsync(&buf[a], sz[a] > 0 ? sz[a] : 16, s));
+    CSK_NCCL(ctx, ncclGroupStart());
+    for (int q = 0; q < P; ++q) {
+        const int64_t sr = pk.seg[2 * q], nr = pk.cnt[2 * q], sp = pk.seg[2 * q + 1], np = pk.cnt[2 * q + 1];
+        const int64_t rr = rv.rbase[q], mr = rv.rbase[q + 1] - rr, rp = rv.pbase[q], mp = rv.pbase[q + 1] - rp;
+        CSK_NCCL(ctx, ncclSend(pk.row + sr, nr, ncclInt32, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclSend(pk.b + sr, nr, ncclFloat64, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclSend(pk.off + sr, nr, ncclInt64, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclSend(pk.col + sp, np, ncclInt32, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclSend(pk.val + sp, np, ncclFloat64, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclRecv(static_cast<int32_t *>(buf[0]) + rr, mr, ncclInt32, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclRecv(static_cast<double *>(buf[1]) + rr, mr, ncclFloat64, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclRecv(static_cast<int64_t *>(buf[2]) + rr, mr, ncclInt64, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclRecv(static_cast<int32_t *>(buf[3]) + rp, mp, ncclInt32, q, c->nccl, s));
+        CSK_NCCL(ctx, ncclRecv(static_cast<double *>(buf[4]) + rp, mp, ncclFloat64, q, c->nccl, s));
+    }
+    CSK_NCCL(ctx, ncclGroupEnd());
+    rv.row = static_cast<int32_t *>(buf[0]);
+    rv.b = static_cast<double *>(buf[1]);
+    rv.off = static_cast<int64_t *>(buf[2]);
+    rv.col = static_cast<int32_t *>(buf[3]);
+    rv.val = static_cast<double *>(buf[4]);
+    csk_status_t st = route_unpack_sketch(ctx, rv, n, d, lo, hi, seed, A_tilde_local, b_tilde_local, nsq_local, s);
+    for (void *p : buf) cudaFreeAsync(p, s);
+    route_free(pk, s);
+    return st;
+}
+
 // ---- S10 fused across GPUs: every rank runs the persistent k_loop on its rows; all P x Gr
 //      CTAs take part in ONE exchange whose {count, max} pair lives in rank 0's memory and is
 //      updated with system-scope atomics over NVLink; the winner's slot and row are read from

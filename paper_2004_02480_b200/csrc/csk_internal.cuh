@@ -9,6 +9,7 @@
 #include <set>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "../../include/csk.h"
 
@@ -140,6 +141,38 @@ struct RankSetup {
     bool exchange_zeroed = false;                 // the caller zeroed xch/slots (and synchronised the ranks)
 };
 size_t loop_exchange_bytes(int total_ctas);  // bytes of ctx->slots a launch of total_ctas needs
+
+// ---------------------------------------------------------------- CSR row routing (route.cu)
+// A rank's rows packed by destination owner (ascending row inside each segment): segment q holds
+// cnt[2q] rows starting at seg[2q] (global row, b, pair offset in the segment) and cnt[2q+1]
+// (col, val) pairs starting at seg[2q+1].  Device buffers (cudaMallocAsync) freed by route_free.
+struct RoutePack {
+    int P = 0;
+    int64_t cnt[2 * kMaxRanks] = {}, seg[2 * kMaxRanks] = {};
+    int32_t *row = nullptr;
+    double *b = nullptr;
+    int64_t *off = nullptr;
+    int32_t *col = nullptr;
+    double *val = nullptr;
+    std::vector<void *> owned;
+};
+// What an owner received: the segments of sources 0..P-1 concatenated in source order (rows of
+// source q at [rbase[q], rbase[q+1]), their pairs at [pbase[q], pbase[q+1])).
+struct RouteRecv {
+    int P = 0;
+    int64_t rbase[kMaxRanks + 1] = {}, pbase[kMaxRanks + 1] = {};
+    const int32_t *row = nullptr;
+    const double *b = nullptr;
+    const int64_t *off = nullptr;
+    const int32_t *col = nullptr;
+    const double *val = nullptr;
+};
+csk_status_t route_pack(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col, const double *val, const double *b,
+                        int64_t m_local, int64_t row_offset, int64_t d, uint64_t seed, int P, RoutePack &pk,
+                        cudaStream_t s);
+csk_status_t route_unpack_sketch(csk_ctx_t ctx, const RouteRecv &rv, int64_t n, int64_t d, int64_t d_lo, int64_t d_hi,
+                                 uint64_t seed, double *At_local, double *bt_local, double *nsq_local, cudaStream_t s);
+void route_free(RoutePack &pk, cudaStream_t s);
 csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const double *nsq, int64_t d,
                       int64_t n, double *x, const double *x_star, double tol, int64_t max_iters,
                       const csk_solve_opts_t *opts, csk_report_t *report, cudaStream_t stream,

@@ -147,3 +147,74 @@ def test_bench_sharded_path_one_rank(csk):
                 "gpu_launches"):
         assert key in d, key
     assert d["roofline"]["kernel_ms"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+# ---------------------------------------------------------------- S9 for CSR (config C5)
+def _csr(m, n, d, k, seed, ragged=False):
+    from csk_synth import make_csr
+    if not ragged:
+        p = make_csr(m, n, k, seed=seed, device="cuda")
+        return p.row_ptr, p.col, p.val, p.b
+    g = np.random.default_rng(seed)
+    lens = g.integers(0, k + 1, size=m)
+    lens[::53] = 0
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(g.choice(n, size=int(x), replace=False)) for x in lens]).astype(np.int32)
+    val = g.standard_normal(int(rp[-1]))
+    b = g.standard_normal(m)
+    return (torch.from_numpy(rp).cuda(), torch.from_numpy(col).cuda(), torch.from_numpy(val).cuda(),
+            torch.from_numpy(b).cuda())
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("m,n,d,k,ragged", [(20000, 300, 1000, 10, False), (5000, 200, 61, 40, True),
+                                           (3000, 64, 8, 12, True)])
+def test_csr_row_routing_virtual_bitexact(csk, P, m, n, d, k, ragged):
+    """S9 by row routing: P contiguous row shards, every row sent to its bucket's
+    owner, owners fold in ascending global row order -> A~, b~ identical to the single-GPU sketch and
+    to the oracle (P virtual ranks on this GPU: the packing, segment order and owner-side plan are
+    the production kernels; only the transport is a device copy instead of NCCL)."""
+    rp, col, val, b = _csr(m, n, d, k, 100 + m + P, ragged)
+    At, bt, nsq = csk.csk_sketch_csr_routed_virtual(rp, col, val, b, n, d, P, seed=7)
+    At1, bt1, nsq1 = csk.csk_sketch_csr(rp, col, val, b, n, d, seed=7)
+    assert torch.equal(At, At1) and torch.equal(bt, bt1) and torch.equal(nsq, nsq1)
+    At_o, bt_o = oracle.sketch_csr(_np(rp), _np(col), _np(val), _np(b), n, d, seed=7)
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_one_rank_nccl_csr_sharded(csk, mode):
+    """csk_sketch_csr_sharded through a real 1-rank NCCL communicator, both modes (reduce-scatter
+    of partial A~; row routing with ncclSend/ncclRecv to self): bit-exact with the oracle at P = 1,
+    for a shard that is a row slice of a larger matrix (global hashing via row_offset)."""
+    m, n, d = 12000, 250, 700
+    rp, col, val, b = _csr(m, n, d, 10, 5)
+    ctx = csk.Context()
+    csk.comm_create(csk.comm_unique_id(), 1, 0, ctx=ctx)
+    lo, hi = 2500, 9100  # this "rank" holds rows [lo, hi) of the global matrix
+    At, bt, nsq, dlo, dhi = csk.csk_sketch_csr_sharded(rp[lo:hi + 1], col, val, b[lo:hi], lo, m, n, d, 1, 0,
+                                                       seed=3, mode=mode, ctx=ctx)
+    assert (dlo, dhi) == (0, d)
+    h, s = oracle.hash_map(3, m, d)
+    sub_rp = (_np(rp)[lo:hi + 1] - _np(rp)[lo]).astype(np.int64)
+    a0 = int(_np(rp)[lo])
+    At_o, bt_o = oracle.sketch_csr(sub_rp, _np(col)[a0:], _np(val)[a0:], _np(b)[lo:hi], n, d, h=h[lo:hi], s=s[lo:hi])
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+    csk.comm_destroy(ctx)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (real NCCL peers)")
+def test_two_gpu_nccl_parity():
+    """>= 2 GPUs: torchrun the sharded bench path at N = 2 (S9 dense + CSR routing, S10 over peer
+    memory) and check its solves reach the oracle-equivalent stop (the bench asserts parity flags)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-extras",
+                          "--no-cpu", "--no-e2e"], cwd=root, capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stderr[-3000:]
+    dd = json.loads(out.stdout.strip().splitlines()[-1])
+    assert dd["n_gpus"] == 2 and dd["termination"] == "converged"

@@ -142,7 +142,46 @@ def _w_loop_decomposition(rank, world):
     assert abs(it - ref.iterations) <= 1
 
 
-@pytest.mark.parametrize("fn", [_w_uid, _w_ranges, _w_sketch_decomposition, _w_loop_decomposition],
-                         ids=["uid_bootstrap", "ownership", "sketch_reduce_scatter", "loop_allgather"])
+def _w_csr_routing(rank, world):
+    """S9 for CSR by row routing (csk_sketch_csr_sharded, CSK_SHARD_ROUTE_ROWS): every input row goes
+    to the owner of its bucket (owner = h // ceil(d/P), csk_shard_range), rows leave each rank in
+    ascending order and are concatenated in source-rank order; each owner's fold of what it received
+    equals the single-process sketch of its bucket rows BIT FOR BIT (ragged CSR, empty rows)."""
+    import paper_2004_02480_b200 as csk
+    from paper_2004_02480_b200.parallel import row_shard
+    m, n, d, seed = 2500, 40, 97, 21
+    g = np.random.default_rng(77)
+    lens = g.integers(0, 12, size=m)
+    lens[::41] = 0
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(g.choice(n, size=int(x), replace=False)) for x in lens]).astype(np.int32)
+    val = g.standard_normal(int(rp[-1]))
+    b = g.standard_normal(m)
+    h, sg = oracle.hash_map(seed, m, d)
+    chunk = -(-d // world)
+    lo, hi = row_shard(m, world, rank)
+    send = [[(i, b[i], col[rp[i]:rp[i + 1]].tolist(), val[rp[i]:rp[i + 1]].tolist())
+             for i in range(lo, hi) if h[i] // chunk == q] for q in range(world)]
+    allsend = [None] * world
+    dist.all_gather_object(allsend, send)          # stands in for the grouped ncclSend/ncclRecv
+    recv = [r for src in range(world) for r in allsend[src][rank]]
+    rows = np.array([r[0] for r in recv], np.int64)
+    assert np.all(np.diff(rows) > 0)               # ascending global rows at the owner
+    dlo, dhi = csk.shard_range(d, world, rank)
+    sub_rp = np.zeros(len(recv) + 1, np.int64)
+    sub_rp[1:] = np.cumsum([len(r[2]) for r in recv])
+    scol = np.array([c for r in recv for c in r[2]], np.int32)
+    sval = np.array([v for r in recv for v in r[3]], np.float64)
+    sb = np.array([r[1] for r in recv], np.float64)
+    At_o, bt_o = oracle.sketch_csr(sub_rp, scol, sval, sb, n, dhi - dlo,
+                                   h=(h[rows] - dlo).astype(np.int32), s=sg[rows])
+    At_full, bt_full = oracle.sketch_csr(rp, col, val, b, n, d, seed=seed)
+    assert np.array_equal(At_o, At_full[dlo:dhi]) and np.array_equal(bt_o, bt_full[dlo:dhi])
+
+
+@pytest.mark.parametrize("fn", [_w_uid, _w_ranges, _w_sketch_decomposition, _w_loop_decomposition, _w_csr_routing],
+                         ids=["uid_bootstrap", "ownership", "sketch_reduce_scatter", "loop_allgather",
+                              "csr_row_routing"])
 def test_two_rank_gloo(fn):
     _run(fn, _free_port())
