@@ -333,12 +333,10 @@ def run_ours(args, dist, rank, ws):
                                           "frac": round(sketch_gbs / hbm_peak, 4),
                                           "note": "whole csk_sketch call: plan (S1 hash + S2 stable bucketing) + sketch kernel"}},
         "clocks": clocks,
-        "gpu_launches": (3 if 8192 < cfg.m <= 200000 and cfg.m <= 256 * cfg.d else 4) * args.steps,
-        "gpu_launches_note": ("per step: k_plan_fused (one cooperative launch: hash, bucket counts, scan, scatter, "
-                              "per-bucket sort), k_sketch_dense, k_loop (+ one memset)"
-                              if 8192 < cfg.m <= 200000 and cfg.m <= 256 * cfg.d else
-                              "per step: k_hash_keys, k_offsets, k_sketch_dense, k_loop (+ CUB onesweep radix-sort "
-                              "kernels and one memset)"),
+        "gpu_launches": 3 * args.steps,
+        "gpu_launches_note": "per step: k_plan_fused (one cooperative launch: hash, bucket counts, scan, scatter, "
+                             "per-bucket sort), k_sketch_dense (or k_sketch_dense_wpb / k_sketch_csr), k_loop "
+                             "(+ one memset of the bucket counts); libcsk's own kernels only",
     }
 
     # ---- e2e: the public API with HOST buffers, copies inside the timed region
@@ -759,7 +757,7 @@ def run_sharded(args, dist, rank, ws):
         "clocks": sampler.summary(t0, t1),
         "roofline": _sharded_roofline(dist, cfg, ws, it, kloop, ksk),
         "gpu_launches": args.steps * 4,
-        "gpu_launches_note": "per step: the plan (k_plan_fused, or k_hash_keys + CUB radix sort + k_offsets), "
+        "gpu_launches_note": "per step: the plan (k_plan_fused), "
                              "k_sketch_dense, k_loop (+ the NCCL reduce-scatter of S9 and the NCCL handle/barrier "
                              "collectives of S10)",
     }

@@ -5,10 +5,11 @@
 // DESIGN.md): z_h = SM64(seed, 2c), z_s = SM64(seed, 2c+1) for GLOBAL row c,
 // h = floor(z_h * d / 2^64) (one UMULHI), sign = top bit of z_s.
 //
-// Bucketing = a stable LSD radix sort of (key = h, value = row | sign<<31) over the
-// ceil(log2 d) key bits (CUB onesweep), so rows of one bucket stay in ascending row
-// order -- the order Algorithm 1's sketch sums in.  offsets[j] = first
-// position of bucket j (lower_bound), offsets[d] = m.
+// Bucketing (S2): perm lists the rows grouped by bucket, ascending row index inside each
+// bucket -- the order Algorithm 1's sketch sums in; offsets[j] = first position of
+// bucket j, offsets[d] = m.  Default: the one-launch counting plan k_plan_fused below.  Only
+// when buckets average > 512 rows (m > 512 d, e.g. d = 1) a stable LSD radix sort of
+// (key = h, value = row | sign<<31) (CUB onesweep) is used instead.
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
@@ -55,26 +56,88 @@ __global__ void k_offsets(const uint32_t *sorted_keys, int32_t m, int32_t d, int
     }
 }
 
-// One-launch plan (default for the seeded hash): a cooperative kernel, one CTA per SM.
-//   P1  count[h(i)] += 1 for every row (global atomics; count zeroed by the caller)
-//   P2  CTA 0: offsets = exclusive scan of count, cursor = offsets
+// One-launch plan (the default): a cooperative kernel over G CTAs (one per SM; fewer for small m).
+//   P1  count[h(i)] += 1 for every row (global atomics; count zeroed by the caller); with an
+//       explicit map (csk_sketch_with_map, the routing receiver) h/sign are read and validated
+//   P2  offsets = exclusive scan of count: CTA c scans its slice of the d counts, the CTA
+//       totals are added in CTA order; cursor = offsets
 //   P3  perm[atomicAdd(cursor[h(i)], 1)] = i | sign << 31   (arbitrary order within a bucket)
-//   P4  each bucket's segment sorted by row (warp per bucket; rows are distinct keys, so the
-//       result is unique: exactly the stable order the radix sort produces)
-// Three grid barriers instead of the ~6 launches (and their gaps) of the CUB path.
-constexpr int kPlanThreads = 1024;
-constexpr int kPlanSegSmem = 1024;  // bucket sizes sorted in shared memory (ints per warp)
+//   P4  each bucket's segment sorted by row (warp bitonic sort per bucket; rows are distinct
+//       keys, so the result is unique: exactly the stable order a radix sort produces)
+// Four grid barriers in one launch instead of the ~6 launches (and their gaps) of a radix sort.
+// Warp bitonic sort of N = 32 EPL unsigned keys (element g = lane EPL + e), ascending.
+template <int EPL>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[EPL], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * EPL; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= EPL) {  // partner in lane ^ (j / EPL), same slot
+                const int lj = j / EPL;
+                const bool lower = (lane & lj) == 0;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[e], lj);
+                    const bool up = ((lane * EPL + e) & k) == 0;
+                    v[e] = (lower == up) ? min(v[e], o) : max(v[e], o);
+                }
+            } else {  // partner slot e | j in this lane
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    if ((e & j) == 0) {
+                        const bool up = ((lane * EPL + e) & k) == 0;
+                        const uint32_t a = v[e], b = v[e | j];
+                        v[e] = up ? min(a, b) : max(a, b);
+                        v[e | j] = up ? max(a, b) : min(a, b);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// One bucket segment perm[a, a + sz) (sz <= 32 EPL) sorted by row: the entry is rotated so the
+// row index is in the high 31 bits and the sign bit in bit 0 (distinct rows: a total order).
+template <int EPL>
+__device__ __forceinline__ void sort_segment(int32_t *perm, int32_t a, int32_t sz, int lane) {
+    uint32_t v[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        const int g = lane * EPL + e;
+        const uint32_t x = g < sz ? static_cast<uint32_t>(perm[a + g]) : 0xffffffffu;
+        v[e] = g < sz ? ((x << 1) | (x >> 31)) : 0xffffffffu;
+    }
+    warp_bitonic<EPL>(v, lane);
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        const int g = lane * EPL + e;
+        if (g < sz) perm[a + g] = static_cast<int32_t>((v[e] >> 1) | (v[e] << 31));
+    }
+}
+
+constexpr int kPlanThreads = 512;
 __global__ void __launch_bounds__(kPlanThreads, 1)
-k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, int32_t *count, int32_t *cursor,
-             int32_t *offsets, int32_t *perm, int32_t *scratch) {
+k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int32_t *h_in, const int8_t *sign_in,
+             int32_t *count, int32_t *cursor, int32_t *offsets, int32_t *perm, int32_t *scratch, int32_t *ctot,
+             int *bad) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ int32_t seg_all[];  // [warps][kPlanSegSmem]
     __shared__ int32_t wsum[32];
+    __shared__ int32_t sbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
     const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    auto bucket = [&](int32_t i, uint32_t &neg) {
+    auto bucket = [&](int32_t i, uint32_t &neg) -> uint32_t {
+        if (h_in) {
+            const int32_t hi = h_in[i];
+            const int8_t si = sign_in[i];
+            neg = si < 0 ? 1u : 0u;
+            if (hi < 0 || hi >= static_cast<int32_t>(d) || (si != 1 && si != -1)) {
+                *bad = 1;
+                return hi < 0 ? 0u : d - 1u;
+            }
+            return static_cast<uint32_t>(hi);
+        }
         const uint64_t c = static_cast<uint64_t>(row_offset) + static_cast<uint64_t>(i);
         neg = static_cast<uint32_t>(sm64(seed, 2 * c + 1) >> 63);
         return static_cast<uint32_t>(__umul64hi(sm64(seed, 2 * c), static_cast<uint64_t>(d)));
@@ -85,74 +148,84 @@ k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, int32_t *
         atomicAdd(count + bucket(static_cast<int32_t>(i), neg), 1);
     }
     grid.sync();
-    // P2: one CTA scans d counts (each thread a contiguous run, block scan of the run sums)
-    if (blockIdx.x == 0) {
-        const int64_t per = (static_cast<int64_t>(d) + kPlanThreads - 1) / kPlanThreads;
-        const int64_t j0 = per * tid, j1 = (j0 + per < d) ? j0 + per : d;
-        int32_t run = 0;
-        for (int64_t j = j0; j < j1; ++j) run += count[j];
-        int32_t incl = run;  // inclusive warp scan, then warps
+    // P2: CTA c scans the counts [j0, j1) (each thread a contiguous run, block scan of the runs)
+    const int64_t G = gridDim.x;
+    const int64_t j0 = static_cast<int64_t>(d) * blockIdx.x / G, j1 = static_cast<int64_t>(d) * (blockIdx.x + 1) / G;
+    const int64_t per = (j1 - j0 + kPlanThreads - 1) / kPlanThreads;
+    const int64_t r0 = j0 + per * tid, r1 = (r0 + per < j1) ? r0 + per : j1;
+    int32_t run = 0;
+    for (int64_t j = r0; j < r1; ++j) run += count[j];
+    int32_t incl = run;  // inclusive warp scan, then warps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = lane < kPlanThreads / 32 ? wsum[lane] : 0, wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
         }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            int32_t w = wsum[lane], wi = w;
+        wsum[lane] = wi - w;  // exclusive over warps
+        if (lane == 31) ctot[blockIdx.x] = wi;  // this CTA's total
+    }
+    __syncthreads();
+    const int32_t local = wsum[warp] + incl - run;
+    grid.sync();
+    if (tid == 0) {  // base of this CTA's slice: the totals of the CTAs before it, in CTA order
+        int32_t bsum = 0;
+        for (int c = 0; c < static_cast<int>(blockIdx.x); ++c) bsum += ctot[c];
+        sbase = bsum;
+    }
+    __syncthreads();
+    int32_t base = sbase + local;
+    for (int64_t j = r0; j < r1; ++j) {
+        offsets[j] = base;
+        cursor[j] = base;
+        base += count[j];
+    }
+    if (gtid == 0) offsets[d] = m;
+    grid.sync();
+    // P3 (four rows per thread per step: four cursor round trips in flight)
+    for (int64_t i0 = gtid; i0 < m; i0 += 4 * gthreads) {
+        uint32_t hh[4], ng[4];
+        int32_t pos[4];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += y;
-            }
-            wsum[lane] = wi - w;  // exclusive over warps
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * gthreads;
+            hh[u] = i < m ? bucket(static_cast<int32_t>(i), ng[u]) : 0u;
         }
-        __syncthreads();
-        int32_t base = wsum[warp] + incl - run;
-        for (int64_t j = j0; j < j1; ++j) {
-            offsets[j] = base;
-            cursor[j] = base;
-            base += count[j];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * gthreads < m) pos[u] = atomicAdd(cursor + hh[u], 1);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * gthreads;
+            if (i < m) perm[pos[u]] = static_cast<int32_t>(static_cast<uint32_t>(i) | (ng[u] << 31));
         }
-        if (tid == 0) offsets[d] = m;
     }
     grid.sync();
-    // P3
-    for (int64_t i = gtid; i < m; i += gthreads) {
-        uint32_t neg;
-        const uint32_t h = bucket(static_cast<int32_t>(i), neg);
-        const int32_t pos = atomicAdd(cursor + h, 1);
-        perm[pos] = static_cast<int32_t>(static_cast<uint32_t>(i) | (neg << 31));
-    }
-    grid.sync();
-    // P4: rank sort of each bucket by row (keys distinct)
+    // P4: sort each bucket by row (keys distinct): a warp bitonic sort in registers for up to
+    // 1024 rows, a rank sort through global scratch beyond (degenerate inputs only)
     const int64_t gw = gtid >> 5, nw = gthreads >> 5;
-    int32_t *sw = seg_all + static_cast<size_t>(warp) * kPlanSegSmem;
     for (int64_t j = gw; j < d; j += nw) {
         const int32_t a = offsets[j], e = offsets[j + 1], sz = e - a;
         if (sz <= 1) continue;
-        if (sz <= 32) {
-            const int32_t v = lane < sz ? perm[a + lane] : 0x7fffffff;
-            const int32_t key = v & 0x7fffffff;
-            int32_t rank = 0;
-            for (int l = 0; l < sz; ++l) {
-                const int32_t kl = __shfl_sync(0xffffffffu, key, l);
-                rank += kl < key ? 1 : 0;
-            }
-            if (lane < sz) perm[a + rank] = v;
-        } else {
-            const int32_t *src;
-            if (sz <= kPlanSegSmem) {
-                for (int t = lane; t < sz; t += 32) sw[t] = perm[a + t];
-                __syncwarp();
-                src = sw;
-            } else {  // rare (a bucket of > 1024 rows): stage in global scratch
-                for (int t = lane; t < sz; t += 32) scratch[a + t] = perm[a + t];
-                __syncwarp();
-                __threadfence_block();
-                src = scratch + a;
-            }
+        if (sz <= 32) sort_segment<1>(perm, a, sz, lane);
+        else if (sz <= 64) sort_segment<2>(perm, a, sz, lane);
+        else if (sz <= 128) sort_segment<4>(perm, a, sz, lane);
+        else if (sz <= 256) sort_segment<8>(perm, a, sz, lane);
+        else if (sz <= 512) sort_segment<16>(perm, a, sz, lane);
+        else if (sz <= 1024) sort_segment<32>(perm, a, sz, lane);
+        else {
+            for (int t = lane; t < sz; t += 32) scratch[a + t] = perm[a + t];
+            __syncwarp();
+            __threadfence_block();
+            const int32_t *src = scratch + a;
             for (int t = lane; t < sz; t += 32) {
                 const int32_t v = src[t], key = v & 0x7fffffff;
                 int32_t rank = 0;
@@ -189,31 +262,44 @@ csk_status_t build_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_
     const int threads = 256;
     const int grid = grid_for(m, threads, ctx->num_sms);
 
-    // the one-launch plan wins in the middle (measured, tools/plan_time.py: 14 vs ~30 us of CUB
-    // kernels at m = 2e4, 26 vs ~38 at 1e5); below ~1e4 rows its three grid barriers cost more
-    // than the small CUB passes, above ~2e5 its bucket atomics and per-bucket sorts do
+    // the one-launch plan (hand-written, deterministic) for every input whose buckets average
+    // <= 512 rows (its per-bucket rank sort is quadratic in the bucket size); the CUB radix sort
+    // only for the degenerate m >> d case (e.g. d = 1) or on request (CSK_PLAN_CUB=1, A/B)
     static const bool use_cub = getenv("CSK_PLAN_CUB") != nullptr;
-    static const bool use_fused = getenv("CSK_PLAN_FUSED") != nullptr;
-    if (h_in == nullptr && !use_cub && ((m > 8192 && m <= 200000 && m <= 256 * d) || use_fused)) {
-        CSK_CHECK(ensure(ctx, ctx->keys_in, static_cast<size_t>(d + 1) * 4));  // count[d]
+    if (!use_cub && m <= 512 * d) {
+        CSK_CHECK(ensure(ctx, ctx->keys_in, static_cast<size_t>(d + 1) * 4 + 2 * static_cast<size_t>(ctx->num_sms) * 4 + 64));
         int32_t *count = static_cast<int32_t *>(ctx->keys_in.ptr);
-        int32_t *cursor = reinterpret_cast<int32_t *>(vals_in);  // m >= d
+        int32_t *ctot = count + d + 1;
+        int *bad = reinterpret_cast<int *>(ctot + ctx->num_sms + 1);
+        CSK_CHECK(ensure(ctx, ctx->vals_in, static_cast<size_t>(d > m ? d : m) * 4));
+        int32_t *cursor = static_cast<int32_t *>(ctx->vals_in.ptr);
         int32_t *perm = reinterpret_cast<int32_t *>(vals_out);
         int32_t *scratch = reinterpret_cast<int32_t *>(keys_out);
         CSK_CUDA(ctx, cudaMemsetAsync(count, 0, static_cast<size_t>(d) * 4, stream));
+        if (h_in) CSK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), stream));
+        // grid: one CTA per SM, fewer for small m (a grid barrier over fewer CTAs is cheaper)
+        int G = static_cast<int>((m + 255) / 256);
+        if (G > ctx->num_sms) G = ctx->num_sms;
+        if (G < 1) G = 1;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
-        cfg.gridDim = dim3(ctx->num_sms);  // every SM: P4 is one latency chain per bucket per warp
+        cfg.gridDim = dim3(G);
         cfg.blockDim = dim3(kPlanThreads);
-        cfg.dynamicSmemBytes = static_cast<size_t>(kPlanThreads / 32) * kPlanSegSmem * 4;
+        cfg.dynamicSmemBytes = 0;
         cfg.stream = stream;
-        CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_plan_fused)));
         cfg.attrs = at;
         cfg.numAttrs = 1;
         CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, k_plan_fused, seed, row_offset, static_cast<int32_t>(m),
-                                         static_cast<uint32_t>(d), count, cursor, offsets, perm, scratch));
+                                         static_cast<uint32_t>(d), h_in, sign_in, count, cursor, offsets, perm,
+                                         scratch, ctot, bad));
+        if (h_in) {
+            int bad_h = 0;
+            CSK_CUDA(ctx, cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CSK_CUDA(ctx, cudaStreamSynchronize(stream));
+            if (bad_h) return fail(ctx, CSK_E_ARG, "explicit map: h outside [0,d) or sign not +-1");
+        }
         *perm_out = perm;
         *offsets_out = offsets;
         return CSK_OK;
