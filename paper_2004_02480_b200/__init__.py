@@ -19,11 +19,12 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# CSK_LIB=prof selects the debug build with the in-kernel phase profiler (tools/phase_probe.py)
+# CSK_LIB=prof selects the debug build with the in-kernel phase profiler (tools/loop_probe.py),
+# CSK_LIB=checked the build with device-side bounds checks (CSK_DCHECK)
 # CSK_LIB=/path/to/libcsk_*.so loads another build of the same ABI (A/B timing of kernel versions)
 _lib_env = os.environ.get("CSK_LIB", "")
 LIB_PATH = (_lib_env if _lib_env.endswith(".so") else
-            os.path.join(_PKG, "libcsk_prof.so" if _lib_env == "prof" else "libcsk.so"))
+            os.path.join(_PKG, {"prof": "libcsk_prof.so", "checked": "libcsk_checked.so"}.get(_lib_env, "libcsk.so")))
 
 CSK_OK, CSK_E_ARG, CSK_E_ZERO_SKETCH, CSK_E_UNSUPPORTED, CSK_E_CUDA, CSK_E_NCCL, CSK_E_NOMEM = range(7)
 CONVERGED, MAX_ITERS, STAGNATED = 0, 1, 2

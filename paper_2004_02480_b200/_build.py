@@ -10,6 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcsk.so")
 PROF_LIB = os.path.join(PKG, "libcsk_prof.so")  # debug build with the in-kernel phase profiler
+CHECKED_LIB = os.path.join(PKG, "libcsk_checked.so")  # debug build with device-side bounds checks
 SOURCES = ["api.cu", "plan.cu", "sketch.cu", "loop.cu", "comm.cu", "route.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -55,17 +56,18 @@ def needs_build(lib: str = LIB) -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
-    lib = PROF_LIB if prof else LIB
+def build(force: bool = False, verbose: bool = False, prof: bool = False, checked: bool = False) -> str:
+    lib = PROF_LIB if prof else CHECKED_LIB if checked else LIB
     if not force and not needs_build(lib):
         return lib
-    objdir = os.path.join(PKG, "build_prof" if prof else "build")
+    objdir = os.path.join(PKG, "build_prof" if prof else "build_checked" if checked else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        extra = (["-Xptxas", "-v"] if verbose else []) + (["-DCSK_PHASE_PROF=1"] if prof else [])
+        extra = ((["-Xptxas", "-v"] if verbose else []) + (["-DCSK_PHASE_PROF=1"] if prof else [])
+                 + (["-DCSK_CHECKED=1"] if checked else []))
         cmd = [NVCC, "-c", src, "-o", obj] + flags(extra)
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
@@ -84,4 +86,5 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, prof="--prof" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, prof="--prof" in sys.argv,
+                checked="--checked" in sys.argv))

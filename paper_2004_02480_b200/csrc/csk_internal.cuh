@@ -13,6 +13,20 @@
 
 #include "../../include/csk.h"
 
+// Device-side bounds checks of the checked build (libcsk_checked.so, -DCSK_CHECKED=1; compute-
+// sanitizer is not available on the GPU pool): a failed check traps the kernel, which surfaces
+// as a CUDA error in the calling test.  Compiled out of the product library.
+#if defined(CSK_CHECKED) && CSK_CHECKED
+#define CSK_DCHECK(cond)       \
+    do {                       \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define CSK_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace csk {
 
 // ---------------------------------------------------------------- context

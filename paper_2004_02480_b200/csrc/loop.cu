@@ -1171,12 +1171,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                     LP(8)
                     if (mx != 0ull) {
                         wrow = static_cast<int64_t>(kmask - (mx & kmask));
+                        CSK_DCHECK(wrow >= 0 && wrow < p.d_glob);
                         if (lane == 0) {
                             // owner: rank by the row ranges, then its CTA
                             const unsigned long long *oslot;
                             const double *orow;
                             if (p.rm_magic != 0ull) {  // one rank: CTA = row / RM by a multiply-shift
                                 const uint32_t olc = static_cast<uint32_t>((static_cast<unsigned long long>(wrow) * p.rm_magic) >> 40);
+                                CSK_DCHECK(olc < static_cast<uint32_t>(G));
                                 oslot = p.slots + par_off + static_cast<size_t>(olc) * kSlotWords;
                                 orow = p.At + wrow * n;
                             } else {

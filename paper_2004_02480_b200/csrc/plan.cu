@@ -189,6 +189,7 @@ k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int
         base += count[j];
     }
     if (gtid == 0) offsets[d] = m;
+    if (blockIdx.x == gridDim.x - 1 && tid == kPlanThreads - 1) CSK_DCHECK(base == m || r1 < j1);  // counts sum to m
     grid.sync();
     // P3 (four rows per thread per step: four cursor round trips in flight)
     for (int64_t i0 = gtid; i0 < m; i0 += 4 * gthreads) {
@@ -205,7 +206,10 @@ k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int64_t i = i0 + u * gthreads;
-            if (i < m) perm[pos[u]] = static_cast<int32_t>(static_cast<uint32_t>(i) | (ng[u] << 31));
+            if (i < m) {
+                CSK_DCHECK(pos[u] >= 0 && pos[u] < m && hh[u] < d);
+                perm[pos[u]] = static_cast<int32_t>(static_cast<uint32_t>(i) | (ng[u] << 31));
+            }
         }
     }
     grid.sync();

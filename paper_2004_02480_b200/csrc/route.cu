@@ -107,6 +107,7 @@ __global__ void k_route_scatter(const int64_t *__restrict__ row_ptr, const int32
         if (o == q) {
             const int64_t* bo = blk + static_cast<int64_t>(blockIdx.x) * 2 * P + 2 * q;
             const int64_t pr = seg[2 * q] + bo[0] + er;   // row slot in the send buffer
+            CSK_DCHECK(pr >= seg[2 * q] && (q + 1 == P || pr < seg[2 * q + 2]));
             const int64_t pin = bo[1] + ep;               // pair offset within q's segment
             srow[pr] = static_cast<int32_t>(row_offset + i);
             sb[pr] = b[i];

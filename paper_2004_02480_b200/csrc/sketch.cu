@@ -117,13 +117,12 @@ __global__ void __launch_bounds__(kMaxConsumers + 64, 1)
 k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m,
                int64_t n, int64_t d, const int32_t *__restrict__ perm,
                const int32_t *__restrict__ offsets, double *__restrict__ At,
-               double *__restrict__ bt, double *__restrict__ nsq, int tc, int chunk_cols,
+               double *__restrict__ bt, int tc, int chunk_cols,
                int chunks, int slot_bytes, int rb, int stages, int header) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + stages;
     int32_t *meta = reinterpret_cast<int32_t *>(empty + stages);   // [stages][kMaxRB] row | sign bit
-    double *red = reinterpret_cast<double *>(smem + header) - 16;  // [2][8] (end of header)
     unsigned char *ring = smem + header;
     const int stage_bytes = rb * slot_bytes;
 
@@ -220,7 +219,6 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
     // ---------------------------------------------------- consumer warps
     int s = 0;
     uint32_t ph = 0;
-    int red_parity = 0;
     for (int c = 0; c < chunks; ++c) {
         const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
         const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
@@ -233,7 +231,6 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
 
         // bucket epilogue: store the row of A~ and (fused S4) its squared norm
         auto flush = [&](int64_t jj) {
-            double part = 0.0;
             double *dst = At + jj * n;
 #pragma unroll
             for (int q = 0; q < P; ++q) {
@@ -246,24 +243,10 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
                         dst[col] = acc[q].x;
                         dst[col + 1] = acc[q].y;
                     }
-                    part = __fma_rn(acc[q].x, acc[q].x, part);
-                    part = __fma_rn(acc[q].y, acc[q].y, part);
                 } else if (col < c1) {
                     dst[col] = acc[q].x;
-                    part = __fma_rn(acc[q].x, acc[q].x, part);
                 }
                 acc[q] = make_double2(0.0, 0.0);
-            }
-            if (nsq != nullptr) {
-                part = warp_sum(part);
-                if (lane == 0) red[red_parity * 8 + warp] = part;
-                asm volatile("bar.sync 1, %0;" ::"r"(tc) : "memory");
-                if (tid == 0) {
-                    double tot = red[red_parity * 8];
-                    for (int w = 1; w < wc; ++w) tot = tot + red[red_parity * 8 + w];
-                    nsq[jj] = (c == 0) ? tot : nsq[jj] + tot;
-                }
-                red_parity ^= 1;
             }
         };
 
@@ -341,43 +324,6 @@ k_sketch_dense(const double *__restrict__ A, int64_t lda, const double *__restri
 // Standalone S4: the same per-row arithmetic as the fused epilogue above
 // (thread t sums pairs t + tc*p, p ascending, then warp butterfly, then warps in
 // order, then chunks in order), one CTA of `tc` threads per row.
-template <int P>
-__global__ void __launch_bounds__(kMaxConsumers)
-k_row_norms(const double *__restrict__ At, int64_t d, int64_t n, double *__restrict__ nsq,
-            int chunk_cols, int chunks) {
-    __shared__ double red[8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tc = blockDim.x;
-    for (int64_t j = blockIdx.x; j < d; j += gridDim.x) {
-        double total = 0.0;
-        for (int c = 0; c < chunks; ++c) {
-            const int64_t c0 = static_cast<int64_t>(c) * chunk_cols;
-            const int64_t c1 = (c0 + chunk_cols < n) ? c0 + chunk_cols : n;
-            double part = 0.0;
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const int64_t col = c0 + 2 * static_cast<int64_t>(tid + tc * p);
-                if (col + 1 < c1) {
-                    const double a0 = At[j * n + col], a1 = At[j * n + col + 1];
-                    part = __fma_rn(a0, a0, part);
-                    part = __fma_rn(a1, a1, part);
-                } else if (col < c1) {
-                    const double a0 = At[j * n + col];
-                    part = __fma_rn(a0, a0, part);
-                }
-            }
-            part = warp_sum(part);
-            if (lane == 0) red[warp] = part;
-            __syncthreads();
-            if (tid == 0) {
-                double tot = red[0];
-                for (int w = 1; w < (tc >> 5); ++w) tot = tot + red[w];
-                total = (c == 0) ? tot : total + tot;
-            }
-            __syncthreads();
-        }
-        if (tid == 0) nsq[j] = total;
-    }
-}
 
 // Short rows (n <= 256): one warp per bucket.  The row-per-CTA ring above moves each gathered
 // row with its own bulk copy, and for rows of a few hundred bytes the copy issue rate, not HBM,
@@ -408,7 +354,7 @@ template <int V, bool VEC>
 __global__ void __launch_bounds__(256, 2)
 k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__restrict__ b, int64_t m, int64_t n, int64_t d,
                    const int32_t *__restrict__ perm, const int32_t *__restrict__ offsets, double *__restrict__ At,
-                   double *__restrict__ bt, double *__restrict__ nsq, int tcw) {
+                   double *__restrict__ bt, int tcw) {
     constexpr int R = V == 1 ? 16 : V == 2 ? 8 : 4;  // rows in flight per warp
     const int lane = threadIdx.x & 31;
     const int W = static_cast<int>((static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
@@ -439,30 +385,18 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
     // bucket epilogue: the row of A~, b~_j, and the fused norm in the standalone order
     auto flush = [&]() {
         double *dst = At + j * n;
-        double tot = 0.0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int64_t col = 2 * static_cast<int64_t>(lane + 32 * v);
-            double part = 0.0;
             if (col + 1 < n) {
                 if (VEC) *reinterpret_cast<double2 *>(dst + col) = acc[v];
                 else { dst[col] = acc[v].x; dst[col + 1] = acc[v].y; }
-                part = __fma_rn(acc[v].x, acc[v].x, part);
-                part = __fma_rn(acc[v].y, acc[v].y, part);
             } else if (col < n) {
                 dst[col] = acc[v].x;
-                part = __fma_rn(acc[v].x, acc[v].x, part);
-            }
-            if (v < tcw) {
-                part = warp_sum(part);
-                tot = (v == 0) ? part : tot + part;
             }
             acc[v] = make_double2(0.0, 0.0);
         }
-        if (lane == 0) {
-            bt[j] = bacc;
-            if (nsq) nsq[j] = tot;
-        }
+        if (lane == 0) bt[j] = bacc;
         bacc = 0.0;
         ++j;
         e = (j < je) ? end_of(j) : T1;
@@ -558,7 +492,7 @@ __global__ void __launch_bounds__(kCsrMaxWarps * 32, 1)
 k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const double *__restrict__ val,
              const double *__restrict__ b, int64_t m, int64_t n, int64_t d, const int32_t *__restrict__ perm,
              const int32_t *__restrict__ offsets, double *__restrict__ At, double *__restrict__ bt,
-             double *__restrict__ nsq, int64_t acc_stride, int stamp_bytes, int warp_bytes, int vec) {
+             int64_t acc_stride, int stamp_bytes, int warp_bytes, int vec) {
     extern __shared__ __align__(16) unsigned char csr_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char *ws = csr_smem + static_cast<size_t>(warp) * warp_bytes;
@@ -590,7 +524,6 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
         for (int64_t k = lane; k < n; k += 32) dst[k] = 0.0;
         if (lane == 0) {
             bt[jj] = 0.0;
-            if (nsq) nsq[jj] = 0.0;
         }
     };
     int64_t fe = end_of(fj);  // end (perm position) of the bucket being formed
@@ -666,6 +599,7 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
             const unsigned char ngb = neg ? 1 : 0;
             for (int kk = 0; kk < maxc; ++kk) {
                 if (kk < mcnt) {
+                    CSK_DCHECK(moff + kk < kCsrSP && mstart + kk < row_ptr[m]);
                     cp_async8(dv + 8u * kk, gv + kk);
                     cp_async4(dc + 4u * kk, gc + kk);
                     gs[kk] = ngb;
@@ -756,6 +690,7 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
             __syncwarp();
             const bool clash = c0 >= 0 && stamp[c0] != lane;
             if (!__any_sync(0xffffffffu, clash)) {
+                CSK_DCHECK(c0 < static_cast<int>(n));
                 if (c0 >= 0) acc[c0] = acc[c0] + v0;  // distinct columns: one step
             } else {
                 // a column shared by pairs of different rows: ranks by pair (= row) order
@@ -771,39 +706,82 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
             c0 = c1;
             v0 = v1;
         }
-        if (end) {  // bucket jb complete: store the A~ row, its norm, clear the accumulator
-            double part = 0.0;
+        if (end) {  // bucket jb complete: store the A~ row, clear the accumulator
             double *dst = At + jb * n;
             if (vec) {
                 double2 *a2 = reinterpret_cast<double2 *>(acc);
                 double2 *d2 = reinterpret_cast<double2 *>(dst);
                 for (int64_t k2 = lane; k2 < n / 2; k2 += 32) {
-                    const double2 a = a2[k2];
-                    d2[k2] = a;
-                    part = __fma_rn(a.x, a.x, part);
-                    part = __fma_rn(a.y, a.y, part);
+                    d2[k2] = a2[k2];
                     a2[k2] = make_double2(0.0, 0.0);
                 }
             } else {
                 for (int64_t k = 2 * lane; k < n; k += 64) {
-                    const double a0 = acc[k];
-                    dst[k] = a0;
-                    part = __fma_rn(a0, a0, part);
+                    dst[k] = acc[k];
                     acc[k] = 0.0;
                     if (k + 1 < n) {
-                        const double a1 = acc[k + 1];
-                        dst[k + 1] = a1;
-                        part = __fma_rn(a1, a1, part);
+                        dst[k + 1] = acc[k + 1];
                         acc[k + 1] = 0.0;
                     }
                 }
             }
-            part = warp_sum(part);
-            if (lane == 0 && nsq) nsq[jb] = part;
         }
         __syncwarp();
         ++folded;
     }
+}
+
+// S4 in the oracle's exact order (SURVEY §8(c) acceptance 2): nsq_j = fma-accumulated
+// a_j0^2, a_j1^2, ... left to right from +0.0, one thread per row (the chain is sequential by
+// definition; rows run in parallel).  The row streams through four 16-double register stages
+// (16-byte loads): the loads of the stage three ahead are in flight while one stage is folded,
+// so the n-long fma chain, not the load latency, bounds a thread.
+__device__ __forceinline__ void norm_stage_load(const double *r, int64_t k, int64_t n, double2 (&v)[8]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        v[u] = (k + 2 * u + 1 < n) ? __ldg(reinterpret_cast<const double2 *>(r + k + 2 * u)) : make_double2(0.0, 0.0);
+}
+__device__ __forceinline__ double norm_stage_fold(const double2 (&v)[8], int64_t k, int64_t n, double acc) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (k + 2 * u + 1 < n) {  // (a zero pad would not change acc, but keep the chain exact: skip it)
+            acc = __fma_rn(v[u].x, v[u].x, acc);
+            acc = __fma_rn(v[u].y, v[u].y, acc);
+        }
+    }
+    return acc;
+}
+__global__ void __launch_bounds__(32) k_row_norms_exact(const double *__restrict__ At, int64_t d, int64_t n,
+                                                        double *__restrict__ nsq) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= d) return;
+    const double *r = At + j * n;
+    double acc = 0.0;
+    int64_t k = 0;
+    if ((reinterpret_cast<uintptr_t>(r) & 15) == 0 && n >= 64) {
+        const int64_t ne = n & ~int64_t(15);  // whole 16-double stages
+        double2 s0[8], s1[8], s2[8], s3[8];
+        norm_stage_load(r, 0, ne, s0);
+        norm_stage_load(r, 16, ne, s1);
+        norm_stage_load(r, 32, ne, s2);
+        norm_stage_load(r, 48, ne, s3);
+        for (; k < ne; k += 64) {
+            acc = norm_stage_fold(s0, k, ne, acc);
+            norm_stage_load(r, k + 64, ne, s0);
+            acc = norm_stage_fold(s1, k + 16, ne, acc);
+            norm_stage_load(r, k + 80, ne, s1);
+            acc = norm_stage_fold(s2, k + 32, ne, acc);
+            norm_stage_load(r, k + 96, ne, s2);
+            acc = norm_stage_fold(s3, k + 48, ne, acc);
+            norm_stage_load(r, k + 112, ne, s3);
+        }
+        k = ne;
+    }
+    for (; k < n; ++k) {
+        const double v = __ldg(r + k);
+        acc = __fma_rn(v, v, acc);
+    }
+    nsq[j] = acc;
 }
 
 }  // namespace
@@ -824,9 +802,9 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
         time_mark(ctx, 0, false, stream);
 #define CSK_WPB(VV)                                                                                       \
         if (tma) k_sketch_dense_wpb<VV, true><<<static_cast<int>(grid), 256, 0, stream>>>(                 \
-            A, lda, b, m, n, d, perm, offsets, At, bt, nsq, tcw);                                         \
+            A, lda, b, m, n, d, perm, offsets, At, bt, tcw);                                              \
         else k_sketch_dense_wpb<VV, false><<<static_cast<int>(grid), 256, 0, stream>>>(                   \
-            A, lda, b, m, n, d, perm, offsets, At, bt, nsq, tcw);
+            A, lda, b, m, n, d, perm, offsets, At, bt, tcw);
         switch (V) {
             case 1: CSK_WPB(1) break;
             case 2: CSK_WPB(2) break;
@@ -836,7 +814,7 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
 #undef CSK_WPB
         time_mark(ctx, 0, true, stream);
         CSK_CUDA(ctx, cudaGetLastError());
-        return CSK_OK;
+        return nsq ? launch_row_norms(ctx, At, d, n, nsq, stream) : CSK_OK;  // S4, the oracle's order
     }
     int grid = ctx->num_sms;
     if (grid > d) grid = static_cast<int>(d);
@@ -846,7 +824,7 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
         CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_dense<PP, T, R>)));           \
         time_mark(ctx, 0, false, stream);                                                              \
         k_sketch_dense<PP, T, R><<<grid, threads, g.smem, stream>>>(                                    \
-            A, lda, b, m, n, d, perm, offsets, At, bt, nsq, g.tc, g.chunk_cols, g.chunks,               \
+            A, lda, b, m, n, d, perm, offsets, At, bt, g.tc, g.chunk_cols, g.chunks,                    \
             g.slot_bytes, g.rb, g.stages, static_cast<int>(g.header));                                  \
     }
 #define CSK_LAUNCH_DENSE(PP, T)                                        \
@@ -869,19 +847,13 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
 #undef CSK_LAUNCH_DENSE_RB
     time_mark(ctx, 0, true, stream);
     CSK_CUDA(ctx, cudaGetLastError());
-    return CSK_OK;
+    return nsq ? launch_row_norms(ctx, At, d, n, nsq, stream) : CSK_OK;  // S4, the oracle's order
 }
 
 csk_status_t launch_row_norms(csk_ctx_t ctx, const double *At, int64_t d, int64_t n, double *nsq,
                               cudaStream_t stream) {
-    const DenseGeom g = dense_geom(n, true);
-    int64_t grid = d < int64_t(ctx->num_sms) * 8 ? d : int64_t(ctx->num_sms) * 8;
-    switch (g.p) {
-        case 1: k_row_norms<1><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
-        case 2: k_row_norms<2><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
-        case 4: k_row_norms<4><<<grid, g.tc, 0, stream>>>(At, d, n, nsq, g.chunk_cols, g.chunks); break;
-        default: return fail(ctx, CSK_E_UNSUPPORTED, "row-norm geometry");
-    }
+    // S4 in the oracle's order (bit-exact): one thread per row, sequential fma chain
+    k_row_norms_exact<<<static_cast<unsigned>((d + 31) / 32), 32, 0, stream>>>(At, d, n, nsq);
     CSK_CUDA(ctx, cudaGetLastError());
     return CSK_OK;
 }
@@ -904,10 +876,10 @@ csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int3
     if (gran) CSK_CUDA(ctx, cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(gran))));
     time_mark(ctx, 0, false, stream);
     k_sketch_csr<<<ctx->num_sms, warps * 32, smem, stream>>>(row_ptr, col, val, b, m, n, d, perm, offsets, At, bt,
-                                                            nsq, stride, static_cast<int>(stampb), static_cast<int>(wb), vec);
+                                                            stride, static_cast<int>(stampb), static_cast<int>(wb), vec);
     time_mark(ctx, 0, true, stream);
     CSK_CUDA(ctx, cudaGetLastError());
-    return CSK_OK;
+    return nsq ? launch_row_norms(ctx, At, d, n, nsq, stream) : CSK_OK;  // S4, the oracle's order
 }
 
 }  // namespace csk
