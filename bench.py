@@ -339,6 +339,28 @@ def run_ours(args, dist, rank, ws):
                              "(+ one memset of the bucket counts); libcsk's own kernels only",
     }
 
+    # ---- the sketch with a cached plan (csk_plan once, csk_sketch_planned per step): the plan depends
+    #      only on (seed, m, d), so a caller solving many right-hand sides / matrices of one shape
+    #      pays it once
+    perm_c, offs_c = csk.csk_plan(cfg.m, cfg.d, seed=cfg.sketch_seed, ctx=ctx)
+    cp = []
+    for k in range(6):
+        if do_flush:
+            flush.fill_(1.0)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record(stream)
+        csk.csk_sketch_planned(p.A, p.b, d, perm_c, offs_c, ctx=ctx, out=(At, bt, nsq))
+        e[1].record(stream)
+        torch.cuda.synchronize()
+        if k:
+            cp.append(e[0].elapsed_time(e[1]))
+    cp_ms = statistics.median(cp)
+    out["roofline_sketch"]["cached_plan"] = {
+        "ms": round(cp_ms, 5), "achieved": round(alg_bytes_sketch(cfg) / (cp_ms * 1e-3) / 1e9, 1),
+        "frac": round(alg_bytes_sketch(cfg) / (cp_ms * 1e-3) / 1e9 / hbm_peak, 4),
+        "note": "csk_sketch_planned with a plan from csk_plan (computed once): sketch kernel + exact-order norms"}
+    del perm_c, offs_c
+
     # ---- e2e: the public API with HOST buffers, copies inside the timed region
     if not args.no_e2e:
         Ah = p.A.cpu().pin_memory()

@@ -169,6 +169,14 @@ CSK_API csk_status_t csk_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const
                             int64_t m, int64_t n, int64_t d, uint64_t seed,
                             double *A_tilde, double *b_tilde, double *nsq, void *stream);
 
+/* The sketch with a plan computed once by csk_plan for (seed, m, d) and reused (a cached plan:
+ * the plan depends only on the map, not on A).  perm int32[m], offsets int32[d+1] as csk_plan
+ * returns them (device).  Same results as csk_sketch with that seed. */
+CSK_API csk_status_t csk_sketch_planned(csk_ctx_t ctx, const double *A, int64_t lda, const double *b,
+                                        int64_t m, int64_t n, int64_t d, const int32_t *perm,
+                                        const int32_t *offsets, double *A_tilde, double *b_tilde,
+                                        double *nsq, void *stream);
+
 /* nsq[j] = ||A~^(j)||_2^2 for j < d (P:62 / P:122).  Fixed summation order:
  * thread t of a row's team sums columns {2t, 2t+1} + 2T*q with fma, then a
  * fixed-shape tree -- bit-identical to the fused sketch epilogue.  A~: ld = n. */

@@ -83,6 +83,7 @@ def _load():
         "csk_sketch": ([P, P, i64, P, i64, i64, i64, u64, P, P, P, P], i32),
         "csk_sketch_with_map": ([P, P, i64, P, i64, i64, i64, P, P, P, P, P, P], i32),
         "csk_sketch_csr": ([P, P, P, P, P, i64, i64, i64, u64, P, P, P, P], i32),
+        "csk_sketch_planned": ([P, P, i64, P, i64, i64, i64, P, P, P, P, P, P], i32),
         "csk_row_norms": ([P, P, i64, i64, P, P], i32),
         "csk_solve": ([P, P, P, P, i64, i64, P, P, dbl, i64, ctypes.POINTER(Report), P], i32),
         "csk_solve_ex": ([P, P, P, P, i64, i64, P, P, dbl, i64, ctypes.POINTER(SolveOpts),
@@ -228,6 +229,28 @@ def csk_sketch(A: torch.Tensor, b: torch.Tensor, d: int, seed: int = 0, with_nor
         At, bt, nsq = out
     ctx.check(lib.csk_sketch(ctx.handle, _ptr(A), A.stride(0), _ptr(b.contiguous()), m, n, d,
                              seed & (2**64 - 1), _ptr(At), _ptr(bt), _ptr(nsq), _stream()))
+    return At, bt, nsq
+
+
+def csk_sketch_planned(A: torch.Tensor, b: torch.Tensor, d: int, perm: torch.Tensor, offsets: torch.Tensor,
+                       with_norms: bool = True, ctx: Context | None = None, out=None):
+    """Sketch with a cached plan (perm, offsets from csk_plan for the same seed, m, d)."""
+    ctx = ctx or default_context()
+    _need(A, torch.float64, "A", 2)
+    _need(b, torch.float64, "b", 1)
+    _need(perm, torch.int32, "perm", 1)
+    _need(offsets, torch.int32, "offsets", 1)
+    if A.stride(1) != 1:
+        raise ValueError("A must be row-major (stride(1) == 1)")
+    m, n = A.shape
+    if out is None:
+        At = torch.empty(d, n, dtype=torch.float64, device=A.device)
+        bt = torch.empty(d, dtype=torch.float64, device=A.device)
+        nsq = torch.empty(d, dtype=torch.float64, device=A.device) if with_norms else None
+    else:
+        At, bt, nsq = out
+    ctx.check(lib.csk_sketch_planned(ctx.handle, _ptr(A), A.stride(0), _ptr(b.contiguous()), m, n, d, _ptr(perm),
+                                     _ptr(offsets), _ptr(At), _ptr(bt), _ptr(nsq), _stream()))
     return At, bt, nsq
 
 

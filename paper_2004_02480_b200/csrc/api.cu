@@ -289,6 +289,16 @@ csk_status_t csk_sketch_with_map(csk_ctx_t ctx, const double *A, int64_t lda, co
     return launch_sketch_dense(ctx, A, lda, b, m, n, d, perm, offsets, A_tilde, b_tilde, nsq, s);
 }
 
+csk_status_t csk_sketch_planned(csk_ctx_t ctx, const double *A, int64_t lda, const double *b, int64_t m,
+                                int64_t n, int64_t d, const int32_t *perm, const int32_t *offsets,
+                                double *A_tilde, double *b_tilde, double *nsq, void *stream) {
+    if (!ctx) return CSK_E_ARG;
+    CSK_CHECK(check_dense(ctx, "csk_sketch_planned", A, lda, b, m, n, d, true, A_tilde, b_tilde));
+    if (!perm || !offsets) return fail(ctx, CSK_E_ARG, "csk_sketch_planned: null plan");
+    CSK_CUDA(ctx, cudaSetDevice(ctx->device));
+    return launch_sketch_dense(ctx, A, lda, b, m, n, d, perm, offsets, A_tilde, b_tilde, nsq, as_stream(stream));
+}
+
 csk_status_t csk_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t *col,
                             const double *val, const double *b, int64_t m, int64_t n, int64_t d,
                             uint64_t seed, double *A_tilde, double *b_tilde, double *nsq,

@@ -135,6 +135,17 @@ def test_sketch_argument_errors(csk):
         csk.csk_sketch(p.A.cpu(), p.b.cpu(), 10)
 
 
+def test_sketch_with_cached_plan(csk):
+    """csk_sketch_planned with a plan from csk_plan (computed once, reused): bit-exact."""
+    p = make_dense(30000, 120, "lognormal_rows", 3, "cuda")
+    perm, offs = csk.csk_plan(30000, 900, seed=8)
+    for _ in range(2):
+        At, bt, nsq = csk.csk_sketch_planned(p.A, p.b, 900, perm, offs)
+        At_o, bt_o = oracle.sketch_dense(_np(p.A), _np(p.b), 900, seed=8)
+        assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+        assert np.array_equal(_np(nsq), oracle.row_norms(At_o))
+
+
 @pytest.mark.parametrize("timing", [False, True])
 def test_sketch_graph_replay(csk, timing):
     """Repeated identical csk_sketch calls replay a captured CUDA graph (api.cu): every replay is

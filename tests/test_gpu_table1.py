@@ -86,3 +86,42 @@ def test_theorem2_rate_on_gpu(csk, spec):
     k = min(r.iterations, 299)
     e2 = ((r.x_trace[: k + 1] - xs[None, :]) ** 2).sum(dim=1)
     assert float((e2[1:] / e2[:-1]).max()) <= rho
+
+
+@pytest.mark.parametrize("spec", ["C1", "C2"])
+def test_lemma1_theorem2_remark2_vs_oracle(csk, spec):
+    """NEXT #4 against the oracle side: Lemma 1's distortion eps and Theorem 2's factor
+     from the GPU sketch (libcsk) + torch.linalg, and the same from the ORACLE's sketch of
+    numpy's orthonormal basis + numpy SVD, must agree (singular values of S Q depend only on the
+    subspace, so the two bases may differ); Remark 2: CSK's factor is at least MWRK's
+    (reading R-17: the printed '<' contradicts the text's 'a little lager' and
+    ||A||_F^2 <= n ||A||_2^2; the math fixes >=)."""
+    import importlib.util, os
+    spec_mod = importlib.util.spec_from_file_location(
+        "distortion", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "distortion.py"))
+    dist = importlib.util.module_from_spec(spec_mod)
+    spec_mod.loader.exec_module(dist)
+    A, b, xs, d, seed = dist.problem(spec)
+    m, n = A.shape
+    # GPU: libcsk sketch of a torch QR basis
+    Q, R = torch.linalg.qr(A, mode="reduced")
+    SQ, _, _ = csk.csk_sketch(Q.contiguous(), torch.zeros(m, dtype=torch.float64, device="cuda"), d, seed=seed)
+    s_g = torch.linalg.svdvals(SQ).cpu().numpy()
+    sA_g = torch.linalg.svdvals(R).cpu().numpy()
+    eps_g = max(s_g[0] ** 2 - 1.0, 1.0 - s_g[-1] ** 2)
+    rho_g = 1.0 - (1.0 - eps_g) ** 3 / n * sA_g[-1] ** 2 / sA_g[0] ** 2
+    # oracle side: numpy QR, the oracle's count sketch, numpy SVD
+    An = A.cpu().numpy()
+    Qn, Rn = np.linalg.qr(An)
+    SQo, _ = oracle.sketch_dense(Qn, np.zeros(m), d, seed=seed)
+    s_o = np.linalg.svd(SQo, compute_uv=False)
+    sA_o = np.linalg.svd(Rn, compute_uv=False)
+    eps_o = max(s_o[0] ** 2 - 1.0, 1.0 - s_o[-1] ** 2)
+    rho_o = 1.0 - (1.0 - eps_o) ** 3 / n * sA_o[-1] ** 2 / sA_o[0] ** 2
+    assert 0.0 < eps_o < 1.0
+    assert abs(eps_g - eps_o) <= 1e-10 * max(1.0, eps_o), (eps_g, eps_o)
+    assert abs(rho_g - rho_o) <= 1e-12, (rho_g, rho_o)
+    # Remark 2: MWRK's factor 1 - s_r^2 / max_i sum_{j != i} ||A^(j)||^2 (oracle row norms)
+    rn = oracle.row_norms(An)
+    rho_mwrk = 1.0 - sA_o[-1] ** 2 / (rn.sum() - rn.min())
+    assert rho_o >= rho_mwrk, (rho_o, rho_mwrk)
