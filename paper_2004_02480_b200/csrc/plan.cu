@@ -241,6 +241,149 @@ k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int
     }
 }
 
+
+// Histogram plan (default when the d bucket counts fit in shared memory): CTA c owns the
+// contiguous rows [c m/G, (c+1) m/G).  Because a CTA's rows are consecutive, placing every
+// (bucket, CTA) group after the groups of lower CTAs already yields ascending rows inside each
+// bucket; only rows of one CTA that share a bucket need ordering, and those groups are tiny.
+//   P1  per-CTA histogram of its rows' buckets in shared memory (shared atomics), stored as
+//       hist[c][j] (coalesced)
+//   P2  hist[c][j] := sum_{c' < c} hist[c'][j] (column prefix, one thread per bucket), bucket
+//       totals -> offsets by the multi-CTA scan of k_plan_fused
+//   P3  cursors in shared memory start at offsets[j] + hist[c][j]; each row takes a slot by a
+//       shared atomic; then every (bucket, CTA) group of >= 2 rows is insertion-sorted by row
+// Three grid barriers, no global atomics, no per-bucket sort pass.
+__global__ void __launch_bounds__(kPlanThreads, 1)
+k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int32_t *h_in, const int8_t *sign_in,
+            int32_t *hist, int32_t *count, int32_t *offsets, int32_t *perm, int32_t *ctot, int *bad) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int32_t sh[];  // [d]: histogram, then cursors
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t sbase;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t gtid = static_cast<int64_t>(c) * blockDim.x + tid;
+    const int64_t gthreads = static_cast<int64_t>(G) * blockDim.x;
+    const int32_t i0 = static_cast<int32_t>(static_cast<int64_t>(m) * c / G);
+    const int32_t i1 = static_cast<int32_t>(static_cast<int64_t>(m) * (c + 1) / G);
+    auto bucket = [&](int32_t i, uint32_t &neg) -> uint32_t {
+        if (h_in) {
+            const int32_t hi = h_in[i];
+            const int8_t si = sign_in[i];
+            neg = si < 0 ? 1u : 0u;
+            if (hi < 0 || hi >= static_cast<int32_t>(d) || (si != 1 && si != -1)) {
+                *bad = 1;
+                return hi < 0 ? 0u : d - 1u;
+            }
+            return static_cast<uint32_t>(hi);
+        }
+        const uint64_t cc = static_cast<uint64_t>(row_offset) + static_cast<uint64_t>(i);
+        neg = static_cast<uint32_t>(sm64(seed, 2 * cc + 1) >> 63);
+        return static_cast<uint32_t>(__umul64hi(sm64(seed, 2 * cc), static_cast<uint64_t>(d)));
+    };
+    // P1
+    for (int64_t j = tid; j < d; j += kPlanThreads) sh[j] = 0;
+    __syncthreads();
+    for (int32_t i = i0 + tid; i < i1; i += kPlanThreads) {
+        uint32_t neg;
+        atomicAdd(&sh[bucket(i, neg)], 1);
+    }
+    __syncthreads();
+    int32_t *hc = hist + static_cast<int64_t>(c) * d;
+    for (int64_t j = tid; j < d; j += kPlanThreads) hc[j] = sh[j];
+    grid.sync();
+    // P2a: column prefix over the CTAs, bucket totals
+    for (int64_t j = gtid; j < d; j += gthreads) {
+        int32_t run = 0;
+        for (int q0 = 0; q0 < G; q0 += 16) {  // 16 loads in flight, then the prefix and the stores
+            int32_t v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = q0 + u < G ? hist[static_cast<int64_t>(q0 + u) * d + j] : 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                if (q0 + u < G) hist[static_cast<int64_t>(q0 + u) * d + j] = run;
+                run += v[u];
+            }
+        }
+        count[j] = run;
+    }
+    grid.sync();
+    // P2b: offsets = exclusive scan of the totals (CTA c scans its slice, CTA totals in order)
+    const int64_t j0 = static_cast<int64_t>(d) * c / G, j1 = static_cast<int64_t>(d) * (c + 1) / G;
+    const int64_t per = (j1 - j0 + kPlanThreads - 1) / kPlanThreads;
+    const int64_t r0 = j0 + per * tid, r1 = (r0 + per < j1) ? r0 + per : j1;
+    int32_t run = 0;
+    for (int64_t j = r0; j < r1; ++j) run += count[j];
+    int32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = lane < kPlanThreads / 32 ? wsum[lane] : 0, wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        wsum[lane] = wi - w;
+        if (lane == 31) ctot[c] = wi;
+    }
+    __syncthreads();
+    const int32_t local = wsum[warp] + incl - run;
+    grid.sync();
+    if (tid == 0) {
+        int32_t bsum = 0;
+        for (int q = 0; q < c; ++q) bsum += ctot[q];
+        sbase = bsum;
+    }
+    __syncthreads();
+    int32_t base = sbase + local;
+    for (int64_t j = r0; j < r1; ++j) {
+        offsets[j] = base;
+        base += count[j];
+    }
+    if (gtid == 0) offsets[d] = m;
+    grid.sync();
+    // P3: this CTA's slots, then its (bucket, CTA) groups of >= 2 rows sorted by row
+    for (int64_t j = tid; j < d; j += kPlanThreads) sh[j] = offsets[j] + hc[j];
+    __syncthreads();
+    for (int32_t i = i0 + tid; i < i1; i += kPlanThreads) {
+        uint32_t neg;
+        const uint32_t h = bucket(i, neg);
+        const int32_t pos = atomicAdd(&sh[h], 1);
+        CSK_DCHECK(pos >= 0 && pos < m);
+        perm[pos] = static_cast<int32_t>(static_cast<uint32_t>(i) | (neg << 31));
+    }
+    __syncthreads();
+    for (int64_t j0 = tid; j0 < d; j0 += 8 * kPlanThreads) {
+        int32_t ga[8], ge[8];  // group bounds of 8 buckets (their loads in flight together)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t j = j0 + static_cast<int64_t>(u) * kPlanThreads;
+            ga[u] = j < d ? offsets[j] + hc[j] : 0;
+            ge[u] = j < d ? sh[j] : 0;
+        }
+#pragma unroll 1
+        for (int u = 0; u < 8; ++u) {
+        const int32_t a = ga[u], e = ge[u];
+        for (int32_t t = a + 1; t < e; ++t) {  // insertion sort of the group (rows are distinct)
+            const int32_t v = perm[t], key = v & 0x7fffffff;
+            int32_t s = t - 1;
+            while (s >= a && (perm[s] & 0x7fffffff) > key) {
+                perm[s + 1] = perm[s];
+                --s;
+            }
+            perm[s + 1] = v;
+        }
+        }
+    }
+}
+
 static int grid_for(int64_t items, int threads, int num_sms) {
     int64_t g = (items + threads - 1) / threads;
     const int64_t cap = static_cast<int64_t>(num_sms) * 16;
@@ -270,6 +413,45 @@ csk_status_t build_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_
     // <= 512 rows (its per-bucket rank sort is quadratic in the bucket size); the CUB radix sort
     // only for the degenerate m >> d case (e.g. d = 1) or on request (CSK_PLAN_CUB=1, A/B)
     static const bool use_cub = getenv("CSK_PLAN_CUB") != nullptr;
+    static const bool no_hist = getenv("CSK_PLAN_ATOMIC") != nullptr;  // A/B: the global-atomic plan
+    // histogram plan: the d counts fit in shared memory and the CTA groups stay small
+    const size_t hist_smem = static_cast<size_t>(d) * 4;
+    if (!use_cub && !no_hist && hist_smem + 1024 <= static_cast<size_t>(ctx->max_smem_optin) && m <= 512 * d) {
+        int G = static_cast<int>((m + 255) / 256);
+        if (G > ctx->num_sms) G = ctx->num_sms;
+        if (G < 1) G = 1;
+        CSK_CHECK(ensure(ctx, ctx->keys_in, static_cast<size_t>(d + 1) * 4 + 2 * static_cast<size_t>(ctx->num_sms) * 4 + 64));
+        int32_t *count = static_cast<int32_t *>(ctx->keys_in.ptr);
+        int32_t *ctot = count + d + 1;
+        int *bad = reinterpret_cast<int *>(ctot + ctx->num_sms + 1);
+        CSK_CHECK(ensure(ctx, ctx->cub_tmp, static_cast<size_t>(G) * d * 4));  // hist[G][d]
+        int32_t *hist = static_cast<int32_t *>(ctx->cub_tmp.ptr);
+        int32_t *perm = reinterpret_cast<int32_t *>(static_cast<uint32_t *>(ctx->vals_out.ptr));
+        if (h_in) CSK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), stream));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(kPlanThreads);
+        cfg.dynamicSmemBytes = hist_smem;
+        cfg.stream = stream;
+        CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_plan_hist)));
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CSK_CUDA(ctx, cudaLaunchKernelEx(&cfg, k_plan_hist, seed, row_offset, static_cast<int32_t>(m),
+                                         static_cast<uint32_t>(d), h_in, sign_in, hist, count, offsets, perm, ctot,
+                                         bad));
+        if (h_in) {
+            int bad_h = 0;
+            CSK_CUDA(ctx, cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CSK_CUDA(ctx, cudaStreamSynchronize(stream));
+            if (bad_h) return fail(ctx, CSK_E_ARG, "explicit map: h outside [0,d) or sign not +-1");
+        }
+        *perm_out = perm;
+        *offsets_out = offsets;
+        return CSK_OK;
+    }
     if (!use_cub && m <= 512 * d) {
         CSK_CHECK(ensure(ctx, ctx->keys_in, static_cast<size_t>(d + 1) * 4 + 2 * static_cast<size_t>(ctx->num_sms) * 4 + 64));
         int32_t *count = static_cast<int32_t *>(ctx->keys_in.ptr);
