@@ -31,6 +31,8 @@ def flags(extra=()):
          "-I", os.path.join(ROOT, "include")]
     if inc:
         f += ["-I", inc]
+    # experiment knob (A/B builds only): extra nvcc flags, e.g. -DCSK_CSR_STAGE_PAIRS=64
+    f += os.environ.get("CSK_EXTRA_NVCC", "").split()
     return f + list(extra)
 
 

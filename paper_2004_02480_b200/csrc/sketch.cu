@@ -465,8 +465,14 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
 // ranks, earlier pair = earlier row first), so every column is the ascending-row fold.
 // b~ is folded at batch formation (row order), the A~ row is stored (coalesced 16-byte stores)
 // and its norm formed when the bucket's last batch has been folded.
-constexpr int kCsrS = 4;                                       // stages (batches in flight) per warp
-constexpr int kCsrSP = 128;                                    // pairs per stage
+#ifndef CSK_CSR_STAGES
+#define CSK_CSR_STAGES 3
+#endif
+#ifndef CSK_CSR_STAGE_PAIRS
+#define CSK_CSR_STAGE_PAIRS 128
+#endif
+constexpr int kCsrS = CSK_CSR_STAGES;                          // stages (batches in flight) per warp
+constexpr int kCsrSP = CSK_CSR_STAGE_PAIRS;                    // pairs per stage
 constexpr int kCsrStageBytes = kCsrSP * (8 + 4 + 1);           // val | col | sign
 constexpr int kCsrMetaBytes = kCsrS * 16;
 constexpr int kCsrMaxWarps = 16;
