@@ -333,10 +333,11 @@ def run_ours(args, dist, rank, ws):
                                           "frac": round(sketch_gbs / hbm_peak, 4),
                                           "note": "whole csk_sketch call: plan (S1 hash + S2 stable bucketing) + sketch kernel"}},
         "clocks": clocks,
-        "gpu_launches": 3 * args.steps,
-        "gpu_launches_note": "per step: k_plan_fused (one cooperative launch: hash, bucket counts, scan, scatter, "
-                             "per-bucket sort), k_sketch_dense (or k_sketch_dense_wpb / k_sketch_csr), k_loop "
-                             "(+ one memset of the bucket counts); libcsk's own kernels only",
+        "gpu_launches": 4 * args.steps,
+        "gpu_launches_note": "per step: k_plan_hist (one cooperative launch: hash, per-CTA histograms, scan, "
+                             "slots, group sorts), k_sketch_dense (or k_sketch_dense_wpb / k_sketch_csr), "
+                             "k_row_norms_exact, k_loop; libcsk's own kernels only (profiles/r02_launches_C3.csv: "
+                             "k_loop 91 % of their GPU time)",
     }
 
     # ---- the sketch with a cached plan (csk_plan once, csk_sketch_planned per step): the plan depends
@@ -779,7 +780,7 @@ def run_sharded(args, dist, rank, ws):
         "clocks": sampler.summary(t0, t1),
         "roofline": _sharded_roofline(dist, cfg, ws, it, kloop, ksk),
         "gpu_launches": args.steps * 4,
-        "gpu_launches_note": "per step: the plan (k_plan_fused), "
+        "gpu_launches_note": "per step: the plan (k_plan_hist), "
                              "k_sketch_dense, k_loop (+ the NCCL reduce-scatter of S9 and the NCCL handle/barrier "
                              "collectives of S10)",
     }

@@ -111,8 +111,10 @@ def main():
         T = len(r["csk_it"])
         ci = sum(r["csk_it"]) / T
         mi = sum(r["mwrk_it"]) / T
-        cm = sum(r["csk_ms"]) / T
-        mm = sum(r["mwrk_ms"]) / T
+        # times: the median over trials (the first measured trial of a size can include the one-off
+        # capture of the plan's CUDA graph); iteration counts: the mean, as the paper reports them
+        cm = sorted(r["csk_ms"])[T // 2]
+        mm = sorted(r["mwrk_ms"])[T // 2]
         # MWRK reads all of A every iteration: its floor is IT x 8 m n / (measured HBM peak)
         gbs = 8.0 * m * n * mi / (mm * 1e-3) / 1e9
         floor_ms = mi * 8.0 * m * n / (peak * 1e9) * 1e3
