@@ -60,10 +60,12 @@ def test_hash_bitexact(csk, seed, m, d, off):
 
 
 @pytest.mark.parametrize("m,d", [(1000, 500), (100000, 5000), (77777, 1), (4096, 4095), (20000, 2000),
-                                 (60000, 400), (199999, 40000), (8193, 8000)])
+                                 (60000, 400), (199999, 40000), (8193, 8000), (150000, 70000), (300000, 1000),
+                                 (5, 2)])
 def test_plan_bitexact(csk, m, d):
-    """Both plan paths (plan.cu: the one-launch cooperative plan for 8192 < m <= 2e5 with small
-    buckets, the CUB radix sort otherwise) give the oracle's stable bucketing."""
+    """Every plan path gives the oracle's stable bucketing (plan.cu): the histogram plan (d counts in
+    shared memory; groups of one CTA sharing a bucket sorted), the global-atomic plan with the warp
+    bitonic sort (d = 70000 > shared memory), the CUB radix sort (m > 512 d: d = 1)."""
     perm, offs = csk.csk_plan(m, d, seed=11)
     h, s = oracle.hash_map(11, m, d)
     order = np.argsort(h, kind="stable")
