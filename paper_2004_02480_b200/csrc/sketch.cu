@@ -449,33 +449,38 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
 }
 
 
-// ---- CSR sketch (config C5): warp per bucket range, dense shared-memory accumulator row ----
+// ---- CSR sketch (config C5): warp pair per bucket range, dense shared-memory accumulator row ----
 //
-// Warp w owns the buckets whose first row lies in [w m/W, (w+1) m/W) of the bucket-sorted
-// order: one contiguous range of `perm`.  The pair stream of a bucket (its rows' stored (col,
-// val) pairs, rows ascending, pairs in stored order) is cut into batches of <= kCsrSP pairs
-// (whole rows, or a slice of one long row); each batch is GATHERED with cp.async (LDGSTS: 8-byte
-// val, 4-byte col, no registers held) into one of kCsrS shared-memory stages, so kCsrS batches'
-// HBM reads are in flight per warp while the oldest one is folded.  Row descriptors (perm entry,
-// row_ptr pair, b) are loaded 32 rows at a time, one window ahead (perm two windows ahead).
-// The fold adds 32 pairs per step into the accumulator row.  Two pairs of one step can hit the
-// same column only if they come from different rows (a row's columns are distinct): a per-warp
-// byte array of lane stamps (every lane writes its id at its column, then reads it back) detects
-// that case in four instructions, and only such steps take the ordered path (__match_any_sync
-// ranks, earlier pair = earlier row first), so every column is the ascending-row fold.
-// b~ is folded at batch formation (row order), the A~ row is stored (coalesced 16-byte stores)
-// and its norm formed when the bucket's last batch has been folded.
+// Pair w (a producer warp and a consumer warp) owns the buckets whose first row lies in
+// [w m/W, (w+1) m/W) of the bucket-sorted order: one contiguous range of `perm`.  The pair stream
+// of a bucket (its rows' stored (col, val) pairs, rows ascending, pairs in stored order) is cut
+// into batches of <= kCsrSP pairs (whole rows, or a slice of one long row).  The PRODUCER forms
+// each batch: row descriptors (perm entry, row_ptr pair, b) 32 rows at a time, one window ahead
+// (perm two windows ahead), a scan of the rows' pair counts, and the GATHER with cp.async (LDGSTS:
+// 8-byte val, 4-byte col, no registers held) into one of kCsrS shared-memory stages; it folds b~
+// (row order) and writes empty buckets itself.  The stage's `full` mbarrier completes when every
+// producer lane's copies have landed (cp.async.mbarrier.arrive.noinc) and its meta is written.
+// The CONSUMER folds 32 pairs per step into its accumulator row and releases the stage (`empty`).
+// Two pairs of one step can hit the same column only if they come from different rows (a row's
+// columns are distinct): a per-pair byte array of lane stamps (every lane writes its id at its
+// column, then reads it back) detects that case in four instructions, and only such steps take
+// the ordered path (__match_any_sync ranks, earlier pair = earlier row first), so every column is
+// the ascending-row fold.  At a bucket's last batch the consumer stores the A~ row (coalesced
+// 16-byte stores) and clears the accumulator; the norms follow in k_row_norms_exact.
+// Round 2 split the former single-warp loop (formation and fold interleaved in one warp, at most
+// 16 warps per SM) into this pair: the fold's add chain no longer waits behind the formation's
+// descriptor loads, 0.90 -> 0.60 ms at C5.
 #ifndef CSK_CSR_STAGES
 #define CSK_CSR_STAGES 3
 #endif
 #ifndef CSK_CSR_STAGE_PAIRS
 #define CSK_CSR_STAGE_PAIRS 128
 #endif
-constexpr int kCsrS = CSK_CSR_STAGES;                          // stages (batches in flight) per warp
+constexpr int kCsrS = CSK_CSR_STAGES;                          // stages (batches in flight) per pair
 constexpr int kCsrSP = CSK_CSR_STAGE_PAIRS;                    // pairs per stage
 constexpr int kCsrStageBytes = kCsrSP * (8 + 4 + 1);           // val | col | sign
-constexpr int kCsrMetaBytes = kCsrS * 16;
-constexpr int kCsrMaxWarps = 16;
+constexpr int kCsrMetaBytes = kCsrS * 16 + kCsrS * 16;  // batch meta + the full / empty mbarriers
+constexpr int kCsrMaxWarps = 16;                                 // 8 pairs
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
@@ -483,15 +488,9 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src) {
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_n(int pending) {  // pending in [0, kCsrS)
-    static_assert(kCsrS <= 4, "cp_async_wait_n covers 0..3");
-    switch (pending) {
-        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-        default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-    }
+// the mbarrier receives one arrival once all of this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __global__ void __launch_bounds__(kCsrMaxWarps * 32, 1)
@@ -499,20 +498,115 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
              const double *__restrict__ b, int64_t m, int64_t n, int64_t d, const int32_t *__restrict__ perm,
              const int32_t *__restrict__ offsets, double *__restrict__ At, double *__restrict__ bt,
              int64_t acc_stride, int stamp_bytes, int warp_bytes, int vec) {
+    // warp specialisation: warp p < NP forms and issues batches (producer), warp NP + p folds them
+    // into its accumulator row (consumer); they meet on kCsrS stages with a full / empty mbarrier
+    // pair each, so the formation (descriptor loads, gathers, b~) overlaps the fold's add chain
     extern __shared__ __align__(16) unsigned char csr_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char *ws = csr_smem + static_cast<size_t>(warp) * warp_bytes;
+    const int NP = static_cast<int>(blockDim.x >> 6);
+    const bool producer = warp < NP;
+    const int pw = producer ? warp : warp - NP;  // the pair
+    unsigned char *ws = csr_smem + static_cast<size_t>(pw) * warp_bytes;
     double *acc = reinterpret_cast<double *>(ws);
     unsigned char *stamp = ws + acc_stride * 8;  // [stamp_bytes]: lane id per column (conflict test)
     unsigned char *stg = stamp + stamp_bytes;
     int *meta = reinterpret_cast<int *>(stg + kCsrS * kCsrStageBytes);  // [kCsrS][4]: pairs, bucket, end
-    for (int64_t k = lane; k < acc_stride; k += 32) acc[k] = 0.0;
-    __syncwarp();
-    const int W = static_cast<int>(gridDim.x) * static_cast<int>(blockDim.x >> 5);
-    const int w = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x >> 5) + warp;
+    uint64_t *full = reinterpret_cast<uint64_t *>(meta + kCsrS * 4);   // [kCsrS]: 32 gather + 32 plain arrivals
+    uint64_t *empty = full + kCsrS;                                    // [kCsrS]: the consumer's release
+    if (!producer) {
+        for (int64_t k = lane; k < acc_stride; k += 32) acc[k] = 0.0;
+    } else if (lane == 0) {
+        for (int q = 0; q < kCsrS; ++q) {
+            mbar_init(full + q, 64);
+            mbar_init(empty + q, 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    if (!producer) {
+        // ---- consumer: fold batch after batch until the producer's sentinel (pairs = -1) ----
+        for (int folded = 0;; ++folded) {
+            const int slot = folded % kCsrS;
+            mbar_wait(full + slot, static_cast<uint32_t>((folded / kCsrS) & 1));
+            const int P = meta[slot * 4 + 0];
+            if (P < 0) break;
+            const int64_t jb = meta[slot * 4 + 1];
+            const bool end = meta[slot * 4 + 2] != 0;
+            const double *sv = reinterpret_cast<const double *>(stg + slot * kCsrStageBytes);
+            const int32_t *sc = reinterpret_cast<const int32_t *>(stg + slot * kCsrStageBytes + kCsrSP * 8);
+            const unsigned char *sg = stg + slot * kCsrStageBytes + kCsrSP * 12;
+            int c0 = lane < P ? sc[lane] : -1;
+            double v0 = lane < P ? sv[lane] : 0.0;
+            if (lane < P && sg[lane]) v0 = -v0;
+            for (int q0 = 0; q0 < P; q0 += 32) {
+                const int q1 = q0 + 32 + lane;
+                int c1 = -1;
+                double v1 = 0.0;
+                if (q1 < P) {
+                    c1 = sc[q1];
+                    v1 = sv[q1];
+                    if (sg[q1]) v1 = -v1;
+                }
+                if (c0 >= 0) stamp[c0] = static_cast<unsigned char>(lane);
+                __syncwarp();
+                const bool clash = c0 >= 0 && stamp[c0] != lane;
+                CSK_DCHECK(c0 < static_cast<int>(n));
+                if (!__any_sync(0xffffffffu, clash)) {
+                    if (c0 >= 0) acc[c0] = acc[c0] + v0;  // distinct columns: one step
+                } else {
+                    const unsigned same = __match_any_sync(0xffffffffu, c0 >= 0 ? c0 : -1 - lane);
+                    const unsigned rank = __popc(same & lt);
+                    const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+                    for (unsigned rr = 0; rr <= maxr; ++rr) {
+                        if (c0 >= 0 && rank == rr) acc[c0] = acc[c0] + v0;
+                        __syncwarp();
+                    }
+                }
+                __syncwarp();
+                c0 = c1;
+                v0 = v1;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + slot);  // the stage may be refilled
+            if (end) {  // bucket jb complete: store the A~ row, clear the accumulator
+                double *dst = At + jb * n;
+                if (vec) {
+                    double2 *a2 = reinterpret_cast<double2 *>(acc);
+                    double2 *d2 = reinterpret_cast<double2 *>(dst);
+                    for (int64_t k2 = lane; k2 < n / 2; k2 += 32) {
+                        d2[k2] = a2[k2];
+                        a2[k2] = make_double2(0.0, 0.0);
+                    }
+                } else {
+                    for (int64_t k = 2 * lane; k < n; k += 64) {
+                        dst[k] = acc[k];
+                        acc[k] = 0.0;
+                        if (k + 1 < n) {
+                            dst[k + 1] = acc[k + 1];
+                            acc[k + 1] = 0.0;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+    // ---- producer ----
+    const int W = static_cast<int>(gridDim.x) * NP;
+    const int w = static_cast<int>(blockIdx.x) * NP + pw;
     int64_t fj = warp_lower_bound(offsets, d, m * w / W, lane);
     const int64_t je = (w == W - 1) ? d : warp_lower_bound(offsets, d, m * (w + 1) / W, lane);
-    if (fj >= je) return;
+    auto finish = [&](int slot) {  // the sentinel: this pair has no more batches
+        if (lane == 0) meta[slot * 4 + 0] = -1;
+        cp_async_arrive_noinc(full + slot);
+        mbar_arrive(full + slot);
+    };
+    if (fj >= je) {
+        finish(0);
+        return;
+    }
     const int64_t T1 = offsets[je];
     int64_t t = offsets[fj];  // perm position of the next row to take
     // bucket ends, lane-distributed: lane l holds offsets[ob + 1 + l]
@@ -558,7 +652,7 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
     desc(wbase + 32, npr, nrs, nre, nbv);
     int64_t roff = 0;  // pairs of the row at t already taken (a long row split over batches)
     double bacc = 0.0;
-    int issued = 0, folded = 0;
+    int issued = 0;
     // ---- form one batch of bucket fj into stage `slot` and issue its gathers ----
     auto form = [&](int slot) {
         if (t - wbase >= 32) {  // next window (its descriptors are already in flight)
@@ -625,7 +719,6 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
                 }
             }
         }
-        cp_async_commit();
         // b~: the rows that START in this batch, ascending (the oracle's fold order); the
         // shuffles are batched ahead of the dependent adds
         const double bs = neg ? -bv : bv;
@@ -663,77 +756,16 @@ k_sketch_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ co
             meta[slot * 4 + 2] = end ? 1 : 0;
         }
     };
-    const unsigned lt = (1u << lane) - 1u;
-    for (;;) {
-        while (issued - folded < kCsrS && fj < je) {
-            form(issued % kCsrS);
-            ++issued;
+    for (issued = 0;; ++issued) {
+        const int slot = issued % kCsrS;
+        if (issued >= kCsrS) mbar_wait(empty + slot, static_cast<uint32_t>(((issued / kCsrS) - 1) & 1));
+        if (fj >= je) {
+            finish(slot);
+            break;
         }
-        if (folded == issued) break;
-        cp_async_wait_n(issued - folded - 1);
-        __syncwarp();
-        const int slot = folded % kCsrS;
-        const int P = meta[slot * 4 + 0];
-        const int64_t jb = meta[slot * 4 + 1];
-        const bool end = meta[slot * 4 + 2] != 0;
-        const double *sv = reinterpret_cast<const double *>(stg + slot * kCsrStageBytes);
-        const int32_t *sc = reinterpret_cast<const int32_t *>(stg + slot * kCsrStageBytes + kCsrSP * 8);
-        const unsigned char *sg = stg + slot * kCsrStageBytes + kCsrSP * 12;
-        // 32 pairs per window; the next window's loads are issued before this window's adds
-        int c0 = lane < P ? sc[lane] : -1;
-        double v0 = lane < P ? sv[lane] : 0.0;
-        if (lane < P && sg[lane]) v0 = -v0;
-        for (int q0 = 0; q0 < P; q0 += 32) {
-            const int q1 = q0 + 32 + lane;
-            int c1 = -1;
-            double v1 = 0.0;
-            if (q1 < P) {
-                c1 = sc[q1];
-                v1 = sv[q1];
-                if (sg[q1]) v1 = -v1;
-            }
-            if (c0 >= 0) stamp[c0] = static_cast<unsigned char>(lane);
-            __syncwarp();
-            const bool clash = c0 >= 0 && stamp[c0] != lane;
-            if (!__any_sync(0xffffffffu, clash)) {
-                CSK_DCHECK(c0 < static_cast<int>(n));
-                if (c0 >= 0) acc[c0] = acc[c0] + v0;  // distinct columns: one step
-            } else {
-                // a column shared by pairs of different rows: ranks by pair (= row) order
-                const unsigned same = __match_any_sync(0xffffffffu, c0 >= 0 ? c0 : -1 - lane);
-                const unsigned rank = __popc(same & lt);
-                const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
-                for (unsigned rr = 0; rr <= maxr; ++rr) {
-                    if (c0 >= 0 && rank == rr) acc[c0] = acc[c0] + v0;
-                    __syncwarp();
-                }
-            }
-            __syncwarp();
-            c0 = c1;
-            v0 = v1;
-        }
-        if (end) {  // bucket jb complete: store the A~ row, clear the accumulator
-            double *dst = At + jb * n;
-            if (vec) {
-                double2 *a2 = reinterpret_cast<double2 *>(acc);
-                double2 *d2 = reinterpret_cast<double2 *>(dst);
-                for (int64_t k2 = lane; k2 < n / 2; k2 += 32) {
-                    d2[k2] = a2[k2];
-                    a2[k2] = make_double2(0.0, 0.0);
-                }
-            } else {
-                for (int64_t k = 2 * lane; k < n; k += 64) {
-                    dst[k] = acc[k];
-                    acc[k] = 0.0;
-                    if (k + 1 < n) {
-                        dst[k + 1] = acc[k + 1];
-                        acc[k + 1] = 0.0;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        ++folded;
+        form(slot);
+        cp_async_arrive_noinc(full + slot);  // the gathers of this lane
+        mbar_arrive(full + slot);            // the meta / sign bytes of this lane (release)
     }
 }
 
@@ -871,10 +903,11 @@ csk_status_t launch_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int3
     const int64_t stride = (n + 1) & ~int64_t(1);  // accumulator doubles (16-byte multiple)
     const int64_t stampb = (n + 15) & ~int64_t(15);  // conflict stamps: one byte per column
     const int64_t wb = ((stride * 8 + stampb + kCsrS * kCsrStageBytes + kCsrMetaBytes) + 127) & ~int64_t(127);
-    int warps = static_cast<int>(ctx->max_smem_optin / wb);
-    if (warps > kCsrMaxWarps) warps = kCsrMaxWarps;
-    if (warps < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
-    const size_t smem = static_cast<size_t>(warps) * wb;
+    int pairs = static_cast<int>(ctx->max_smem_optin / wb);  // producer / consumer warp pairs per CTA
+    if (pairs > kCsrMaxWarps / 2) pairs = kCsrMaxWarps / 2;
+    if (pairs < 1) return fail(ctx, CSK_E_UNSUPPORTED, "csk_sketch_csr: n too large for shared accumulators");
+    const int warps = 2 * pairs;
+    const size_t smem = static_cast<size_t>(pairs) * wb;
     CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_sketch_csr)));
     const int vec = (n % 2 == 0 && aligned16(At)) ? 1 : 0;
     // experiment knob: the L2 fetch granularity for the random (col, val) / row_ptr / b gathers
