@@ -225,6 +225,7 @@ const char *csk_last_error(csk_ctx_t ctx) { return ctx ? ctx->last_error.c_str()
 csk_status_t csk_sketch(csk_ctx_t ctx, const double *A, int64_t lda, const double *b, int64_t m,
                         int64_t n, int64_t d, uint64_t seed, double *A_tilde, double *b_tilde,
                         double *nsq, void *stream) {
+    CSK_NVTX("csk_sketch");
     if (!ctx) return CSK_E_ARG;
     CSK_CHECK(check_dense(ctx, "csk_sketch", A, lda, b, m, n, d, false, A_tilde, b_tilde));
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -279,6 +280,7 @@ csk_status_t csk_sketch_with_map(csk_ctx_t ctx, const double *A, int64_t lda, co
                                  int64_t m, int64_t n, int64_t d, const int32_t *h,
                                  const int8_t *sign, double *A_tilde, double *b_tilde, double *nsq,
                                  void *stream) {
+    CSK_NVTX("csk_sketch_with_map");
     if (!ctx) return CSK_E_ARG;
     CSK_CHECK(check_dense(ctx, "csk_sketch_with_map", A, lda, b, m, n, d, true, A_tilde, b_tilde));
     if (!h || !sign) return fail(ctx, CSK_E_ARG, "csk_sketch_with_map: null map");
@@ -292,6 +294,7 @@ csk_status_t csk_sketch_with_map(csk_ctx_t ctx, const double *A, int64_t lda, co
 csk_status_t csk_sketch_planned(csk_ctx_t ctx, const double *A, int64_t lda, const double *b, int64_t m,
                                 int64_t n, int64_t d, const int32_t *perm, const int32_t *offsets,
                                 double *A_tilde, double *b_tilde, double *nsq, void *stream) {
+    CSK_NVTX("csk_sketch_planned");
     if (!ctx) return CSK_E_ARG;
     CSK_CHECK(check_dense(ctx, "csk_sketch_planned", A, lda, b, m, n, d, true, A_tilde, b_tilde));
     if (!perm || !offsets) return fail(ctx, CSK_E_ARG, "csk_sketch_planned: null plan");
@@ -303,6 +306,7 @@ csk_status_t csk_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t
                             const double *val, const double *b, int64_t m, int64_t n, int64_t d,
                             uint64_t seed, double *A_tilde, double *b_tilde, double *nsq,
                             void *stream) {
+    CSK_NVTX("csk_sketch_csr");
     if (!ctx) return CSK_E_ARG;
     if (!row_ptr || !col || !val || !b || !A_tilde || !b_tilde)
         return fail(ctx, CSK_E_ARG, "csk_sketch_csr: null pointer argument");
@@ -317,6 +321,7 @@ csk_status_t csk_sketch_csr(csk_ctx_t ctx, const int64_t *row_ptr, const int32_t
 
 csk_status_t csk_row_norms(csk_ctx_t ctx, const double *A_tilde, int64_t d, int64_t n, double *nsq,
                            void *stream) {
+    CSK_NVTX("csk_row_norms");
     if (!ctx) return CSK_E_ARG;
     if (!A_tilde || !nsq || d < 1 || n < 1) return fail(ctx, CSK_E_ARG, "csk_row_norms: bad arguments");
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -333,6 +338,7 @@ csk_status_t csk_solve_ex(csk_ctx_t ctx, const double *A_tilde, const double *b_
                           const double *nsq, int64_t d, int64_t n, double *x, const double *x_star,
                           double tol, int64_t max_iters, const csk_solve_opts_t *opts,
                           csk_report_t *report, void *stream) {
+    CSK_NVTX("csk_solve_ex");
     if (!ctx) return CSK_E_ARG;
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     return run_solve(ctx, A_tilde, b_tilde, nsq, d, n, x, x_star, tol, max_iters, opts, report,
@@ -340,6 +346,7 @@ csk_status_t csk_solve_ex(csk_ctx_t ctx, const double *A_tilde, const double *b_
 }
 
 csk_status_t csk_solve_wait(csk_ctx_t ctx, csk_report_t *report) {
+    CSK_NVTX("csk_solve_wait");
     if (!ctx) return CSK_E_ARG;
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     return finish_solve(ctx, report);
@@ -381,6 +388,7 @@ csk_status_t csk_last_solve_tiers(csk_ctx_t ctx, int32_t *out) {
 csk_status_t csk_run(csk_ctx_t ctx, const double *A, int64_t lda, const double *b, int64_t m,
                      int64_t n, int64_t d, uint64_t seed, double *x, const double *x_star,
                      double tol, int64_t max_iters, csk_report_t *report, void *stream) {
+    CSK_NVTX("csk_run");
     if (!ctx) return CSK_E_ARG;
     CSK_CUDA(ctx, cudaSetDevice(ctx->device));
     CSK_CHECK(ensure(ctx, ctx->a_tilde, static_cast<size_t>(d) * n * 8));
@@ -397,6 +405,7 @@ csk_status_t csk_run_host(csk_ctx_t ctx, const double *A_host, int64_t lda, cons
                           int64_t m, int64_t n, int64_t d, uint64_t seed, double *x_host,
                           const double *x_star_host, double tol, int64_t max_iters,
                           csk_report_t *report, void *stream) {
+    CSK_NVTX("csk_run_host");
     if (!ctx) return CSK_E_ARG;
     if (!A_host || !b_host || !x_host) return fail(ctx, CSK_E_ARG, "csk_run_host: null host buffer");
     if (m < 1 || n < 1 || lda < n) return fail(ctx, CSK_E_ARG, "csk_run_host: bad sizes");

@@ -425,6 +425,7 @@ csk_status_t csk_sketch_sharded(csk_ctx_t ctx, const double *A_local, int64_t ld
                                 int64_t m_local, int64_t row_offset, int64_t m, int64_t n, int64_t d,
                                 uint64_t seed, double *A_tilde_local, double *b_tilde_local,
                                 double *nsq_local, int64_t *d_lo, int64_t *d_hi, void *stream) {
+    CSK_NVTX("csk_sketch_sharded");
     if (!ctx || !ctx->comm) return ctx ? fail(ctx, CSK_E_ARG, "csk_sketch_sharded: call csk_comm_create first") : CSK_E_ARG;
     if (!A_local || !b_local || !A_tilde_local || !b_tilde_local || !d_lo || !d_hi || m_local < 1 ||
         row_offset < 0 || row_offset + m_local > m || n < 1 || d < 1 || d >= m || lda < n)
@@ -475,6 +476,7 @@ csk_status_t csk_sketch_csr_sharded(csk_ctx_t ctx, const int64_t *row_ptr, const
                                     int64_t d, uint64_t seed, int32_t mode, double *A_tilde_local,
                                     double *b_tilde_local, double *nsq_local, int64_t *d_lo, int64_t *d_hi,
                                     void *stream) {
+    CSK_NVTX("csk_sketch_csr_sharded");
     if (!ctx || !ctx->comm) return ctx ? fail(ctx, CSK_E_ARG, "csk_sketch_csr_sharded: call csk_comm_create first") : CSK_E_ARG;
     if (!row_ptr || !col || !val || !b_local || !A_tilde_local || !b_tilde_local || !d_lo || !d_hi || m_local < 0 ||
         row_offset < 0 || row_offset + m_local > m || m >= (int64_t(1) << 31) || n < 1 || d < 1 || d >= m ||
@@ -808,6 +810,7 @@ csk_status_t csk_solve_sharded(csk_ctx_t ctx, const double *A_tilde_local, const
                                const double *nsq_local, int64_t d_lo, int64_t d_hi, int64_t d, int64_t n,
                                double *x, const double *x_star, double tol, int64_t max_iters,
                                csk_report_t *report, void *stream) {
+    CSK_NVTX("csk_solve_sharded");
     if (!ctx || !ctx->comm) return ctx ? fail(ctx, CSK_E_ARG, "csk_solve_sharded: call csk_comm_create first") : CSK_E_ARG;
     if (!report || !x || n < 1 || d < 1 || d_lo < 0 || d_hi < d_lo || d_hi > d || !(tol > 0.0) || max_iters < 0 ||
         (d_hi > d_lo && (!A_tilde_local || !b_tilde_local || !nsq_local)))
@@ -848,6 +851,7 @@ csk_status_t csk_solve_virtual_ranks_ex(csk_ctx_t ctx, const double *A_tilde, co
                                         const double *x_star, double tol, int64_t max_iters,
                                         double *x_copies, const csk_solve_opts_t *opts, csk_report_t *report,
                                         void *stream) {
+    CSK_NVTX("csk_solve_virtual_ranks_ex");
     if (!ctx || !A_tilde || !b_tilde || !nsq || !x || !report || nranks < 1 || d < 1 || n < 1 || !(tol > 0.0) ||
         max_iters < 0)
         return ctx ? fail(ctx, CSK_E_ARG, "csk_solve_virtual_ranks: bad arguments") : CSK_E_ARG;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <map>
@@ -12,6 +13,16 @@
 #include <vector>
 
 #include "../../include/csk.h"
+
+// NVTX range over one public entry point (SURVEY section 5 tracing): the host span of the call,
+// visible in nsys / ncu --nvtx timelines; a no-op unless a tool is attached
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define CSK_NVTX(name) ::NvtxRange csk_nvtx_range_(name)
 
 // Device-side bounds checks of the checked build (libcsk_checked.so, -DCSK_CHECKED=1; compute-
 // sanitizer is not available on the GPU pool): a failed check traps the kernel, which surfaces

@@ -554,6 +554,7 @@ extern "C" csk_status_t csk_hash(csk_ctx_t ctx, uint64_t seed, int64_t row_offse
 extern "C" csk_status_t csk_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_t m,
                                  int64_t d, const int32_t *h_in, const int8_t *sign_in,
                                  int32_t *perm, int32_t *offsets, void *stream) {
+    CSK_NVTX("csk_plan");
     if (!ctx) return CSK_E_ARG;
     if (m < 1 || m >= (int64_t(1) << 31) || d < 1 || d > m || row_offset < 0)
         return fail(ctx, CSK_E_ARG, "csk_plan: need 1 <= d <= m < 2^31");

@@ -263,6 +263,7 @@ extern "C" csk_status_t csk_sketch_csr_routed_virtual(csk_ctx_t ctx, const int64
                                                       const double *val, const double *b, int64_t m, int64_t n,
                                                       int64_t d, uint64_t seed, int32_t nranks, double *A_tilde,
                                                       double *b_tilde, double *nsq, void *stream) {
+    CSK_NVTX("csk_sketch_csr_routed_virtual");
     if (!ctx) return CSK_E_ARG;
     if (!row_ptr || !col || !val || !b || !A_tilde || !b_tilde || m < 1 || m >= (int64_t(1) << 31) || n < 1 || d < 1 ||
         d >= m || nranks < 1 || nranks > kMaxRanks || d < nranks)
