@@ -471,10 +471,10 @@ k_sketch_dense_wpb(const double *__restrict__ A, int64_t lda, const double *__re
 // 16 warps per SM) into this pair: the fold's add chain no longer waits behind the formation's
 // descriptor loads, 0.90 -> 0.60 ms at C5.
 #ifndef CSK_CSR_STAGES
-#define CSK_CSR_STAGES 3
+#define CSK_CSR_STAGES 2
 #endif
 #ifndef CSK_CSR_STAGE_PAIRS
-#define CSK_CSR_STAGE_PAIRS 128
+#define CSK_CSR_STAGE_PAIRS 256
 #endif
 constexpr int kCsrS = CSK_CSR_STAGES;                          // stages (batches in flight) per pair
 constexpr int kCsrSP = CSK_CSR_STAGE_PAIRS;                    // pairs per stage
