@@ -822,6 +822,87 @@ __global__ void __launch_bounds__(32) k_row_norms_exact(const double *__restrict
     nsq[j] = acc;
 }
 
+#ifndef CSK_NORM_COLS
+#define CSK_NORM_COLS 64
+#endif
+#ifndef CSK_NORM_STAGES
+#define CSK_NORM_STAGES 4
+#endif
+// The same chains with the rows staged through shared memory: CTA = one warp = 32 consecutive
+// rows, lane l the chain of row r0 + l.  A stage holds kNC = 64 columns of the 32 rows, copied by
+// cp.async (LDGSTS, 16 bytes per lane: one coalesced 512-byte row chunk per warp instruction);
+// the stage's mbarrier completes when every lane's copies have landed
+// (cp.async.mbarrier.arrive.noinc), and kNS stages are in flight, so the HBM stream runs ahead of
+// the chains.  (One 1-D bulk copy per row chunk instead was bound by the TMA issue rate for
+// 512-byte copies: C3 16 us, C5 131 us.)  Rows sit kNP doubles apart, kNP / 2 odd: the 32 lanes'
+// 16-byte reads of one column pair fall in distinct bank groups (4 wavefronts for 512 bytes, the
+// minimum).  Needs n even and a 16-byte aligned A~.
+constexpr int kNC = CSK_NORM_COLS, kNS = CSK_NORM_STAGES, kNP = kNC + 2;
+static_assert((kNP / 2) % 2 == 1, "conflict-free row stride");
+static_assert(kNC == 64, "one 16-byte copy per lane per row chunk");
+constexpr size_t kNormSmem = static_cast<size_t>(kNS) * 32 * kNP * 8 + kNS * 8;
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__global__ void __launch_bounds__(32) k_row_norms_staged(const double *__restrict__ At, int64_t d, int64_t n,
+                                                         double *__restrict__ nsq) {
+    extern __shared__ __align__(16) unsigned char norm_smem[];
+    double *buf = reinterpret_cast<double *>(norm_smem);  // [kNS][32][kNP]
+    uint64_t *full = reinterpret_cast<uint64_t *>(norm_smem + static_cast<size_t>(kNS) * 32 * kNP * 8);
+    const int lane = threadIdx.x;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int rows = static_cast<int>(d - r0 < 32 ? d - r0 : 32);
+    const bool act = lane < rows;
+    const int nch = static_cast<int>((n + kNC - 1) / kNC);
+    if (lane == 0) {
+        for (int q = 0; q < kNS; ++q) mbar_init(full + q, 32);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int ch) {
+        const int st = ch % kNS;
+        const int64_t c0 = static_cast<int64_t>(ch) * kNC;
+        const int cw = static_cast<int>(n - c0 < kNC ? n - c0 : kNC);
+        if (2 * lane < cw) {
+            const double *src = At + r0 * n + c0 + 2 * lane;
+            const uint32_t dst = smem_u32(buf + static_cast<size_t>(st) * 32 * kNP + 2 * lane);
+            for (int r = 0; r < rows; ++r) cp_async16(dst + static_cast<uint32_t>(r * kNP * 8), src + r * n);
+        }
+        cp_async_arrive_noinc(full + st);
+    };
+    for (int ch = 0; ch < kNS && ch < nch; ++ch) issue(ch);
+    double acc = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+        const int st = ch % kNS;
+        mbar_wait(full + st, static_cast<uint32_t>((ch / kNS) & 1));
+        const int cw = static_cast<int>(n - static_cast<int64_t>(ch) * kNC < kNC ? n - static_cast<int64_t>(ch) * kNC : kNC);
+        const double2 *rp = reinterpret_cast<const double2 *>(buf + (static_cast<size_t>(st) * 32 + lane) * kNP);
+        if (act) {
+            if (cw == kNC) {
+                // the next pair's load is issued before this pair's two fmas (the chain, not the
+                // shared-memory latency, sets the pace)
+                double2 v = rp[0];
+#pragma unroll
+                for (int u = 0; u < kNC / 2; ++u) {
+                    const double2 w = rp[u + 1 < kNC / 2 ? u + 1 : u];
+                    acc = __fma_rn(v.x, v.x, acc);
+                    acc = __fma_rn(v.y, v.y, acc);
+                    v = w;
+                }
+            } else {
+                for (int u = 0; u < cw / 2; ++u) {
+                    const double2 v = rp[u];
+                    acc = __fma_rn(v.x, v.x, acc);
+                    acc = __fma_rn(v.y, v.y, acc);
+                }
+            }
+        }
+        __syncwarp();  // every lane is done with stage st before it is refilled
+        if (ch + kNS < nch) issue(ch + kNS);
+    }
+    if (act) nsq[r0 + lane] = acc;
+}
+
 }  // namespace
 
 int norm_team_threads(int64_t n) { return dense_geom(n, true).tc; }
@@ -890,8 +971,16 @@ csk_status_t launch_sketch_dense(csk_ctx_t ctx, const double *A, int64_t lda, co
 
 csk_status_t launch_row_norms(csk_ctx_t ctx, const double *At, int64_t d, int64_t n, double *nsq,
                               cudaStream_t stream) {
-    // S4 in the oracle's order (bit-exact): one thread per row, sequential fma chain
-    k_row_norms_exact<<<static_cast<unsigned>((d + 31) / 32), 32, 0, stream>>>(At, d, n, nsq);
+    // S4 in the oracle's order (bit-exact): one thread per row, sequential fma chain; the rows
+    // staged through shared memory when they are 16-byte aligned (n even), else read by the threads
+    static const bool plain = getenv("CSK_NORMS_PLAIN") != nullptr;  // A/B
+    const unsigned grid = static_cast<unsigned>((d + 31) / 32);
+    if (!plain && n % 2 == 0 && aligned16(At)) {
+        CSK_CHECK(raise_smem(ctx, reinterpret_cast<const void *>(k_row_norms_staged)));
+        k_row_norms_staged<<<grid, 32, kNormSmem, stream>>>(At, d, n, nsq);
+    } else {
+        k_row_norms_exact<<<grid, 32, 0, stream>>>(At, d, n, nsq);
+    }
     CSK_CUDA(ctx, cudaGetLastError());
     return CSK_OK;
 }

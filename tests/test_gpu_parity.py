@@ -49,6 +49,19 @@ def _check_sketch(csk, A, b, d, seed, **kw):
     return At, bt, nsq
 
 
+@pytest.mark.parametrize("d,n,offset", [(1, 2, 0), (31, 64, 0), (33, 130, 0), (70, 500, 0), (100, 2000, 0),
+                                        (65, 63, 0), (40, 7, 0), (50, 500, 1), (5, 1, 0), (3, 66, 0)])
+def test_row_norms_paths(csk, d, n, offset):
+    """S4 bit-exact on both norm kernels: the TMA-staged one (n even, 16-byte aligned rows: full
+    and partial 64-column stages, d not a multiple of 32) and the plain one (odd n, or A~ starting
+    8 bytes off a 16-byte boundary)."""
+    g = torch.Generator().manual_seed(d * 1000 + n)
+    flat = torch.randn(d * n + offset, generator=g, dtype=torch.float64)
+    A = flat[offset:].view(d, n)
+    nsq = csk.csk_row_norms(A.cuda()[0:d] if offset == 0 else flat.cuda()[offset:].view(d, n))
+    assert np.array_equal(_np(nsq), oracle.row_norms(A.numpy()))
+
+
 # ---------------------------------------------------------------- S1/S2
 @pytest.mark.parametrize("seed,m,d,off", [(0, 1000, 500, 0), (0, 20000, 2000, 0),
                                           (2**63 + 5, 123457, 40000, 0), (7, 5000, 3, 1234)])
