@@ -36,6 +36,11 @@
 
 #include "csk_internal.cuh"
 
+// 1: read the exchange pair the PTX-model way (an acquire fence after the poll, then a re-read)
+#ifndef CSK_STRICT_ACQUIRE
+#define CSK_STRICT_ACQUIRE 0
+#endif
+
 namespace csk {
 
 namespace {
@@ -1119,6 +1124,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                                 if (RESMODE) ld_relaxed_v4(lp, lc2, lmx, lsum);
                                 else ld_relaxed_v2(lp, lc2, lmx);
                             } while (lc2 < static_cast<unsigned long long>(p.Gr) && !watchdog());
+#if CSK_STRICT_ACQUIRE
+                            if (lc2 >= static_cast<unsigned long long>(p.Gr)) {  // see the single-GPU poll
+                                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                                if (RESMODE) ld_relaxed_v4(lp, lc2, lmx, lsum);
+                                else ld_relaxed_v2(lp, lc2, lmx);
+                            }
+#endif
                             unsigned long long h, l, hs = 0ull, ls = 0ull;
                             ll_pack(__longlong_as_double(static_cast<long long>(lmx)), tag, h, l);
                             if (RESMODE) ll_pack(__longlong_as_double(static_cast<long long>(lsum)), tag, hs, ls);
@@ -1148,11 +1160,26 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         }
                         timed_out = __any_sync(0xffffffffu, timed_out);
                         c = static_cast<unsigned long long>(G);
-                    } else do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
-                        if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
-                        else ld_relaxed_v2(pair, c, mx);
-                        if (c < static_cast<unsigned long long>(G) && watchdog()) break;
-                    } while (c < static_cast<unsigned long long>(G));
+                    } else {
+                        do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
+                            if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
+                            else ld_relaxed_v2(pair, c, mx);
+                            if (c < static_cast<unsigned long long>(G) && watchdog()) break;
+                        } while (c < static_cast<unsigned long long>(G));
+#if CSK_STRICT_ACQUIRE
+                        // the PTX-model form of the read (memory-model note):
+                        // the count seen by a relaxed poll plus an acquire fence synchronizes with
+                        // every CTA's red.release of the count, so a re-read of the pair after the
+                        // fence sees every CTA's red.max (and red.add of the sum) -- without relying
+                        // on the 16/32-byte poll being one L2-sector snapshot.  One fence and one
+                        // more L2 round trip per iteration; off by default (measured in DESIGN.md)
+                        if (c >= static_cast<unsigned long long>(G)) {
+                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                            if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
+                            else ld_relaxed_v2(pair, c, mx);
+                        }
+#endif
+                    }
                     if (timed_out) {
                         stop = -3;
                         mx = 0ull;
