@@ -56,6 +56,13 @@ def main():
                 done_spread = (done.max(1).values - done.min(1).values).mean().item()
                 print(f"   skew (ns, mean over 64 iterations): publish spread {spread:.0f}, last publish -> first "
                       f"spin exit {lastpub_to_done:.0f}, spin-exit spread {done_spread:.0f}")
+                late = (pub - pub.min(1, keepdim=True).values).mean(0)  # per CTA, ns after the first publish
+                order = late.argsort(descending=True)[:6].tolist()
+                q = [late[i * geoG // 4:(i + 1) * geoG // 4].mean().item() for i in range(4)]
+                print("   latest publishers (CTA: mean ns after the first): "
+                      + ", ".join(f"{i}: {late[i].item():.0f}" for i in order)
+                      + f" | mean lateness by CTA quarter: {q[0]:.0f} {q[1]:.0f} {q[2]:.0f} {q[3]:.0f}"
+                      + f" | median {late.median().item():.0f}")
             w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(15))
             w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(15) if c[16 + i])
             print(f"{nm} G={geo['num_ctas']} wpg={wpg} IT={r.iterations} {ms * 1e3 / it:.2f} us/it = "
