@@ -26,8 +26,17 @@ CSK_NO_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source o
     -o gpurun_out/${R}_sketch_csr_C5 python tools/csr_time.py 3 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_plan_hist -s 37 -c 1 \
     -o gpurun_out/${R}_plan_C5 python tools/plan_time.py > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_row_norms_exact -s 2 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_row_norms_staged -s 2 -c 1 \
     -o gpurun_out/${R}_norms_C5 python tools/csr_time.py 3 > /dev/null 2>&1
+# NVTX: only the kernels inside the csk_sketch / csk_solve_ex ranges are profiled (the ranges exist)
+timeout 300 ncu --nvtx --nvtx-include "csk_sketch/" --nvtx-include "csk_solve_ex/" --metrics gpu__time_duration.sum \
+    --csv python tools/run_solve_once.py C1 > gpurun_out/${R}_nvtx_ranges.csv 2>&1
+# the random-gather floor of C5's CSR access pattern, the norms and CSR kernel times, Table 1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_gather tools/microbench_gather.cu && \
+    timeout 300 ./tools/microbench_gather > gpurun_out/${R}_microbench_gather.txt 2>&1
+timeout 300 python tools/norms_time.py > gpurun_out/${R}_norms_time.txt 2>&1
+timeout 300 python tools/csr_time.py 5 > gpurun_out/${R}_csr_time.txt 2>&1
+timeout 1800 python tools/table1.py --trials 50 --json gpurun_out/${R}_table1.json > gpurun_out/${R}_table1.md 2>&1
 for rep in gpurun_out/${R}_*.ncu-rep; do
     [ -f "$rep" ] || continue
     b=$(basename "$rep" .ncu-rep)
