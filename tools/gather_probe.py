@@ -1,4 +1,5 @@
-"""Is the short-row sketch bound by random row gathers?  The same kernel (k_sketch_dense_wpb)
+"""Is the dense sketch bound by random row gathers?  The same kernel (k_sketch_dense_wpb for n <= 256,
+k_sketch_dense above: C3 and C4 shapes too)
 with a random map (the hash) and with a monotone map (bucket j = rows [j m/d, (j+1) m/d): the
 rows are read in address order).  python tools/gather_probe.py"""
 import os
@@ -11,8 +12,8 @@ import paper_2004_02480_b200 as csk  # noqa: E402
 
 ctx = csk.Context()
 csk.csk_ctx_set_timing(True, ctx=ctx)
-for m, n in [(700000, 50), (700000, 100), (700000, 150)]:
-    d = n * n
+for m, n, d in [(700000, 50, 2500), (700000, 100, 10000), (700000, 150, 22500), (100000, 500, 5000),
+                (1000000, 1000, 10000)]:
     A = torch.randn(m, n, dtype=torch.float64, device="cuda")
     b = torch.randn(m, dtype=torch.float64, device="cuda")
     h_rand, s_rand = csk.csk_hash(m, d, seed=3)
