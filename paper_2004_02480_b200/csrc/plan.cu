@@ -116,6 +116,8 @@ __device__ __forceinline__ void sort_segment(int32_t *perm, int32_t a, int32_t s
 }
 
 constexpr int kPlanThreads = 512;
+constexpr int kPlanDirtyCap = 1024;  // k_plan_hist: listed (bucket, CTA) groups per CTA
+constexpr int kPlanColPer = 8;       // k_plan_hist P2a, warp per bucket: CTAs per lane (G <= 256)
 __global__ void __launch_bounds__(kPlanThreads, 1)
 k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int32_t *h_in, const int8_t *sign_in,
              int32_t *count, int32_t *cursor, int32_t *offsets, int32_t *perm, int32_t *scratch, int32_t *ctot,
@@ -250,8 +252,9 @@ k_plan_fused(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int
 //       hist[c][j] (coalesced)
 //   P2  hist[c][j] := sum_{c' < c} hist[c'][j] (column prefix, one thread per bucket), bucket
 //       totals -> offsets by the multi-CTA scan of k_plan_fused
-//   P3  cursors in shared memory start at offsets[j] + hist[c][j]; each row takes a slot by a
-//       shared atomic; then every (bucket, CTA) group of >= 2 rows is insertion-sorted by row
+//   P3  cursors in shared memory start at offsets[j] + hist[c][j]; rows take slots chunk by
+//       chunk in row order (warp-ranked by __match_any_sync, one shared atomic per bucket per
+//       warp), and only the (bucket, CTA) groups two warps of one chunk claimed are sorted
 // Three grid barriers, no global atomics, no per-bucket sort pass.
 __global__ void __launch_bounds__(kPlanThreads, 1)
 k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int32_t *h_in, const int8_t *sign_in,
@@ -261,6 +264,8 @@ k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int3
     extern __shared__ int32_t sh[];  // [d]: histogram, then cursors
     __shared__ int32_t wsum[32];
     __shared__ int32_t sbase;
+    __shared__ int32_t ndirty;
+    __shared__ int32_t dirty[kPlanDirtyCap];  // buckets whose group needs the row-order sort
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
     const int64_t gtid = static_cast<int64_t>(c) * blockDim.x + tid;
@@ -293,7 +298,36 @@ k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int3
     int32_t *hc = hist + static_cast<int64_t>(c) * d;
     for (int64_t j = tid; j < d; j += kPlanThreads) hc[j] = sh[j];
     grid.sync();
-    // P2a: column prefix over the CTAs, bucket totals
+    // P2a: column prefix over the CTAs, bucket totals.  Few buckets (d <= threads / 32): a warp
+    // per bucket, lane l the CTAs [l per, (l+1) per) (one round of loads, a warp scan); else a
+    // thread per bucket walking the G CTAs with 16 loads in flight
+    if (static_cast<int64_t>(d) * 32 <= gthreads && G <= 32 * kPlanColPer) {
+        const int per = (G + 31) / 32;
+        for (int64_t j = gtid >> 5; j < d; j += gthreads >> 5) {
+            int32_t v[kPlanColPer];
+            int32_t run = 0;
+#pragma unroll
+            for (int u = 0; u < kPlanColPer; ++u) {
+                const int cq = lane * per + u;
+                v[u] = (u < per && cq < G) ? hist[static_cast<int64_t>(cq) * d + j] : 0;
+                run += v[u];
+            }
+            int32_t incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int32_t ex = incl - run;
+#pragma unroll
+            for (int u = 0; u < kPlanColPer; ++u) {
+                const int cq = lane * per + u;
+                if (u < per && cq < G) hist[static_cast<int64_t>(cq) * d + j] = ex;
+                ex += v[u];
+            }
+            if (lane == 31) count[j] = incl;
+        }
+    } else
     for (int64_t j = gtid; j < d; j += gthreads) {
         int32_t run = 0;
         for (int q0 = 0; q0 < G; q0 += 16) {  // 16 loads in flight, then the prefix and the stores
@@ -349,29 +383,43 @@ k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int3
     }
     if (gtid == 0) offsets[d] = m;
     grid.sync();
-    // P3: this CTA's slots, then its (bucket, CTA) groups of >= 2 rows sorted by row
+    // P3: this CTA's slots.  Rows are taken in chunks of kPlanThreads, in row order: inside a
+    // warp, rows of one bucket get consecutive slots in lane (= row) order (__match_any_sync
+    // ranks, one shared atomic per bucket per warp); chunks follow one another (a barrier), so
+    // only two warps of one chunk claiming the same bucket can land out of row order.  The claim
+    // detects that (its cursor moved since the chunk began) and lists the bucket; only the listed
+    // (bucket, CTA) groups are sorted afterwards.  (A full list falls back to sorting every group.)
     for (int64_t j = tid; j < d; j += kPlanThreads) sh[j] = offsets[j] + hc[j];
+    if (tid == 0) ndirty = 0;
     __syncthreads();
-    for (int32_t i = i0 + tid; i < i1; i += kPlanThreads) {
-        uint32_t neg;
-        const uint32_t h = bucket(i, neg);
-        const int32_t pos = atomicAdd(&sh[h], 1);
-        CSK_DCHECK(pos >= 0 && pos < m);
-        perm[pos] = static_cast<int32_t>(static_cast<uint32_t>(i) | (neg << 31));
-    }
-    __syncthreads();
-    for (int64_t j0 = tid; j0 < d; j0 += 8 * kPlanThreads) {
-        int32_t ga[8], ge[8];  // group bounds of 8 buckets (their loads in flight together)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int64_t j = j0 + static_cast<int64_t>(u) * kPlanThreads;
-            ga[u] = j < d ? offsets[j] + hc[j] : 0;
-            ge[u] = j < d ? sh[j] : 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int32_t base = i0; base < i1; base += kPlanThreads) {
+        const int32_t i = base + tid;
+        const bool valid = i < i1;
+        uint32_t neg = 0u, h = 0u;
+        if (valid) h = bucket(i, neg);
+        const unsigned same = __match_any_sync(0xffffffffu, valid ? h : (0x80000000u | static_cast<uint32_t>(lane)));
+        const int leader = __ffs(same) - 1;
+        int32_t start = 0;
+        if (valid && lane == leader) start = sh[h];
+        __syncthreads();  // every warp has read its cursors before any warp claims
+        int32_t pos = 0;
+        if (valid && lane == leader) {
+            pos = atomicAdd(&sh[h], __popc(same));
+            if (pos != start) {
+                const int q = atomicAdd(&ndirty, 1);
+                if (q < kPlanDirtyCap) dirty[q] = static_cast<int32_t>(h);
+            }
         }
-#pragma unroll 1
-        for (int u = 0; u < 8; ++u) {
-        const int32_t a = ga[u], e = ge[u];
-        for (int32_t t = a + 1; t < e; ++t) {  // insertion sort of the group (rows are distinct)
+        pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(same & lt);
+        if (valid) {
+            CSK_DCHECK(pos >= 0 && pos < m);
+            perm[pos] = static_cast<int32_t>(static_cast<uint32_t>(i) | (neg << 31));
+        }
+        __syncthreads();  // this chunk's claims are done before the next chunk reads its cursors
+    }
+    auto sort_group = [&](int32_t a, int32_t e) {  // insertion sort by row (rows are distinct)
+        for (int32_t t = a + 1; t < e; ++t) {
             const int32_t v = perm[t], key = v & 0x7fffffff;
             int32_t s = t - 1;
             while (s >= a && (perm[s] & 0x7fffffff) > key) {
@@ -380,6 +428,27 @@ k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int3
             }
             perm[s + 1] = v;
         }
+    };
+    if (ndirty <= kPlanDirtyCap) {
+        // the listed groups (a bucket may be listed more than once: the first to set the cursor's
+        // sign bit sorts it)
+        for (int q = tid; q < ndirty; q += kPlanThreads) {
+            const int32_t j = dirty[q];
+            const int32_t e = atomicOr(&sh[j], static_cast<int32_t>(0x80000000u));
+            if (e < 0) continue;
+            sort_group(offsets[j] + hc[j], e);
+        }
+    } else {
+        for (int64_t j0 = tid; j0 < d; j0 += 8 * kPlanThreads) {
+            int32_t ga[8], ge[8];  // group bounds of 8 buckets (their loads in flight together)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t j = j0 + static_cast<int64_t>(u) * kPlanThreads;
+                ga[u] = j < d ? offsets[j] + hc[j] : 0;
+                ge[u] = j < d ? sh[j] : 0;
+            }
+#pragma unroll 1
+            for (int u = 0; u < 8; ++u) sort_group(ga[u], ge[u]);
         }
     }
 }
@@ -416,7 +485,8 @@ csk_status_t build_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_
     static const bool no_hist = getenv("CSK_PLAN_ATOMIC") != nullptr;  // A/B: the global-atomic plan
     // histogram plan: the d counts fit in shared memory and the CTA groups stay small
     const size_t hist_smem = static_cast<size_t>(d) * 4;
-    if (!use_cub && !no_hist && hist_smem + 1024 <= static_cast<size_t>(ctx->max_smem_optin) && m <= 512 * d) {
+    if (!use_cub && !no_hist && hist_smem + 1024 + kPlanDirtyCap * 4 <= static_cast<size_t>(ctx->max_smem_optin) &&
+        m <= 512 * d) {
         int G = static_cast<int>((m + 255) / 256);
         if (G > ctx->num_sms) G = ctx->num_sms;
         if (G < 1) G = 1;
