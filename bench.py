@@ -444,9 +444,9 @@ def c5_extra(csk, ctx, cap=None):
         e[2].record()
         rep = csk.csk_solve_wait(ctx)
         torch.cuda.synchronize()
-        res = (e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), rep)
+        res = (e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), rep, csk.csk_last_kernel_ms("sketch", ctx=ctx))
         del At, bt, nsq
-    sk, sv, rep = res
+    sk, sv, rep, skk = res
     t = csk.csk_last_solve_tiers(ctx=ctx)
     G, rg = t["num_ctas"], 8 // max(t["group_warps"], 1)
     rows_cta = -(-d // G)
@@ -461,6 +461,11 @@ def c5_extra(csk, ctx, cap=None):
     return {"ms_per_step": round(sk + sv, 4), "sketch_ms": round(sk, 4), "solve_ms": round(sv, 4),
             "sketch_bytes": sk_bytes, "sketch_hbm_gbs": round(sk_bytes / (sk * 1e-3) / 1e9, 1),
             "sketch_hbm_frac_with_plan": round(sk_bytes / (sk * 1e-3) / 1e9 / peak, 4),
+            "sketch_kernel_ms": round(skk, 4),
+            "sketch_kernel_hbm_frac": round(sk_bytes / (skk * 1e-3) / 1e9 / peak, 4) if skk > 0 else None,
+            "sketch_kernel_note": "k_sketch_csr alone (libcsk events); its floor is the random row gather: "
+                                  "tools/microbench_gather.cu reads the same rows in the same order with "
+                                  "nothing folded in 0.57 ms (0.64 ms with the A~ writes), DESIGN.md section 6",
             "iterations": rep.iterations, "final_res": rep.final_res,
             "termination": ["converged", "max_iters", "stagnated"][rep.termination],
             "us_per_iteration": round(us_it, 3), "tiers": t,
