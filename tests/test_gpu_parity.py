@@ -88,6 +88,25 @@ def test_plan_bitexact(csk, m, d):
     assert np.array_equal(_np(offs), np.searchsorted(h[order], np.arange(d + 1), side="left"))
 
 
+@pytest.mark.parametrize("m,d,pattern", [(227328, 500, "mod32"), (227328, 500, "mod500"),
+                                         (150000, 3000, "runs"), (100000, 5000, "reverse")])
+def test_plan_explicit_map_collisions(csk, m, d, pattern):
+    """Explicit maps built to collide inside the histogram plan's 512-row chunks: h = i mod 32
+    (every warp of every chunk claims the same 32 buckets, so the list of colliding groups
+    overflows and the plan sorts every group), i mod d, runs of equal buckets and a descending
+    map -- the stable order (rows ascending inside a bucket) in every case."""
+    i = np.arange(m, dtype=np.int64)
+    h = {"mod32": i % 32, "mod500": i % d, "runs": (i // 37) % d, "reverse": (d - 1) - (i * d) // m}[pattern]
+    h = h.astype(np.int32)
+    s = np.where((i * 2654435761) % 7 < 3, -1, 1).astype(np.int8)
+    perm, offs = csk.csk_plan(m, d, h=torch.from_numpy(h).cuda(), sign=torch.from_numpy(s).cuda())
+    order = np.argsort(h, kind="stable")
+    want = order.astype(np.int64) | np.where(s[order] < 0, 1 << 31, 0)
+    got = _np(perm).astype(np.int64) & 0xFFFFFFFF
+    assert np.array_equal(got, want)
+    assert np.array_equal(_np(offs), np.searchsorted(h[order], np.arange(d + 1), side="left"))
+
+
 # ---------------------------------------------------------------- S3/S4
 @pytest.mark.parametrize("m,n,d", [(1000, 50, 500), (20000, 200, 2000), (3001, 17, 700),
                                    (999, 1, 10), (4000, 2500, 300), (5000, 64, 4999),
