@@ -136,6 +136,21 @@ def test_sketch_short_rows_unaligned(csk, n, lda):
     assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
 
 
+@pytest.mark.parametrize("m,n,lda,d", [(3000, 513, 514, 400), (2500, 777, 780, 300), (4000, 1000, 1000, 1999),
+                                       (1500, 300, 300, 100), (2000, 2600, 2600, 64)])
+def test_sketch_long_rows_padded(csk, m, n, lda, d):
+    """Long rows through the TMA ring kernel: odd n (the last column read past the bulk copy),
+    padded lda, a short last stage, several column chunks (n = 2600)."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    buf = torch.randn(m * lda, generator=g, dtype=torch.float64, device="cuda")
+    A = buf.view(m, lda)[:, :n]
+    b = torch.randn(m, generator=g, dtype=torch.float64, device="cuda")
+    At, bt, nsq = csk.csk_sketch(A, b, d, seed=21)
+    At_o, bt_o = oracle.sketch_dense(_np(A.contiguous()), _np(b), d, seed=21)
+    assert np.array_equal(_np(At), At_o) and np.array_equal(_np(bt), bt_o)
+    assert np.array_equal(_np(nsq), oracle.row_norms(At_o))
+
+
 @pytest.mark.parametrize("lda,shift", [(136, 0), (131, 0), (130, 1)])
 def test_sketch_padded_and_unaligned_lda(csk, lda, shift):
     """lda > n (even: TMA path), odd lda and an 8-byte-aligned A (plain-load path)."""
