@@ -72,6 +72,7 @@ struct LoopParams {
     int64_t *report;          // [0]=iterations, [1]=final_res bits, [2]=termination, [3]=last idx
     const double *bb;         // residual mode: ||b~||^2 (device scalar)
     int wpg;                  // warps per row group (1, 2, 4, 8)
+    int fuse_ts;              // full TMEM tier + shared-memory rows in one interleaved pass
     int rr;                   // rows per group held in registers (<= RRMAX)
     int rs;                   // rows per group held in shared memory
     int rt;                   // rows per group held in tensor memory (TM variants, <= 16)
@@ -401,6 +402,50 @@ __device__ __forceinline__ void tmem_block_wide(uint32_t taddr, const double (&x
     for (int j = 0; j < NB; ++j) acc[j] = lo[j] + hi[j];
 }
 
+// The full TMEM tier (16 rows) and up to RSM shared-memory rows in ONE pass: step j issues the
+// tcgen05.ld.x32 of TMEM rows j, j+1, then the step's six shared-memory (row, column pair) units
+// (LDS.128 + two FMAs each), and only then waits for the load and folds the two rows (two
+// column-half chains each, added) -- the TMEM load latency hides behind the shared-memory loads
+// and FMAs instead of being exposed after every load.  acc[0..15] = TMEM rows, acc[16 + i] =
+// shared-memory row i (i < rs; rows past rs re-read row rs-1 and are never written back), the rest
+// 0: one 32-row transposed tree follows.  Every row's partial has the order of the separate tier
+// passes (tmem_block_wide, smem_block), and the 32-row tree adds the lanes in the same bit order as
+// two 16-row trees, so the dot products are bit-identical to theirs.
+template <int RSM>
+__device__ __forceinline__ void tmem_smem_fused(uint32_t taddr, const double *arows, int tg, int rs, int TG,
+                                                 const double (&x)[8], double (&acc)[32]) {
+    static_assert(RSM * 4 <= 48, "six shared-memory units per TMEM row pair");
+    const double2 *a2 = reinterpret_cast<const double2 *>(arows) + tg;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kTmRowsDev; j += 2) {
+        uint32_t v[32];
+        tmem_ld32_async(taddr + 16u * j, v);
+#pragma unroll
+        for (int u = 3 * j; u < 3 * j + 6; ++u) {
+            const int i = u >> 2, qp = u & 3;
+            if (i < RSM) {
+                const int ii = i < rs ? i : rs - 1;
+                const double2 val = a2[(static_cast<size_t>(ii) * 4 + qp) * TG];
+                acc[16 + i] = __fma_rn(val.x, x[2 * qp], acc[16 + i]);
+                acc[16 + i] = __fma_rn(val.y, x[2 * qp + 1], acc[16 + i]);
+            }
+        }
+        tmem_wait_ld(v);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double lo = 0.0, hi = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                lo = __fma_rn(dbl_of(v[16 * h + 2 * q], v[16 * h + 2 * q + 1]), x[q], lo);
+                hi = __fma_rn(dbl_of(v[16 * h + 2 * q + 8], v[16 * h + 2 * q + 9]), x[q + 4], hi);
+            }
+            acc[j + h] = lo + hi;
+        }
+    }
+}
+
 // NB shared-memory rows (from i0, clamped to rs-1) folded against x: columns outer, rows inner.
 // Layout [row][q/2][thread][2]: a thread's columns c_q, c_{q+1} sit in one 16-byte word.
 template <int NB, int CB>
@@ -649,6 +694,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     const double fin_b2 = (TM == 1 && fast_fin && lane + 32 < ng) ? btl[lr0 + 32 + lane] : 0.0;
     const double fin_i2 = (TM == 1 && fast_fin && lane + 32 < ng) ? invl[lr0 + 32 + lane] : 0.0;
     const bool all_reg = rr == ng;  // every row of the group in registers: own partial by shuffle
+    const bool fuse_ts = p.fuse_ts != 0;  // (A/B: CSK_LOOP_FUSE_TS=0 takes the separate tier passes)
 
     int64_t k = 0, last = -1;
     int term = -1;
@@ -676,6 +722,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
     }
 #else
 #define LP(i)
+#endif
+#if CSK_PHASE_PROF && CSK_PROBE_GEMV
+#define LPG(i) LP(i)
+#define LPT(i)
+#else
+#define LPG(i)
+#define LPT(i) LP(i)
 #endif
     for (;; ++k) {
         // ---- S8 of iteration k-1, fused at the top of iteration k: x_q += lambda a_{i_{k-1}}[c_q]
@@ -731,6 +784,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         }
         // ---- S6 GEMV: register rows (transposed tree: row i ends in lanes [i LPR, (i+1) LPR)) ----
         double sreg;
+        // the full TMEM tier and the shared-memory rows in one interleaved pass (C4's layout)
+        const bool fused = TM == 1 && !ST && rt == kTmRowsDev && rs >= 1 && rs <= 12 && fuse_ts;
+        bool smem_done = false;  // the fused pass took the shared-memory rows
         {
             double acc[V];
 #pragma unroll
@@ -745,13 +801,23 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             const int i = lane / LPR;
             if ((lane % LPR) == 0 && i < rr && !(all_reg && wg == 0)) dotp[wg * RM + lr0 + i] = s;
         }
+        LPG(11)
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
         if constexpr (TM != 0) {
             // blocks of 8 / 4 / 2 rows (a block may run one row past rt, reading an unused row
             // of this thread's TMEM area that is never written back); a full wide tier (16 rows)
             // folds both blocks into one 16-row tree (one tree depth instead of two)
             int j0 = 0;
-            if (TM == 1 && rt == kTmRowsDev) {
+            if (fused) {
+                // full TMEM tier + the shared-memory rows in one interleaved pass, one 32-row tree
+                double acc32[32];
+                tmem_smem_fused<12>(tbase, arows, tg, rs, TG, x, acc32);
+                const double s = treduce<32>(acc32, lane);
+                if (lane < 16) dotp[wg * RM + lr0 + rr + lane] = s;
+                else if (lane - 16 < rs) dotp[wg * RM + lr0 + rr + rt + lane - 16] = s;
+                j0 = rt;
+                smem_done = true;
+            } else if (TM == 1 && rt == kTmRowsDev) {
                 double acc16[16];
                 tmem_block_wide<8, CB>(tbase, x, *reinterpret_cast<double(*)[8]>(&acc16[0]));
                 tmem_block_wide<8, CB>(tbase + 16u * 8, x, *reinterpret_cast<double(*)[8]>(&acc16[8]));
@@ -788,13 +854,14 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 }
             }
         }
+        LPG(12)
         // ---- S6 GEMV: shared-memory rows, blocks of 8, transposed tree ----
         {
             // blocks of 8 (a tail of <= 4 rows: a block of 4), columns outer so the block's rows
             // form independent fma chains; rows past rs re-read row rs-1 (never written back).
             // 9..12 rows with the TMEM tier: one 16-row tree over a block of 8 and a block of 4
-            int i0 = 0;
-            if (TM == 1 && rs > 8 && rs <= 12) {
+            int i0 = smem_done ? rs : 0;
+            if (!smem_done && TM == 1 && rs > 8 && rs <= 12) {
                 double acc16[16];
                 smem_block<8, CB>(arows, tg, 0, rs, TG, x, *reinterpret_cast<double(*)[8]>(&acc16[0]));
                 smem_block<4, CB>(arows, tg, 8, rs, TG, x, *reinterpret_cast<double(*)[4]>(&acc16[8]));
@@ -888,9 +955,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 }
             }
         }
+        LPG(13)
         // ---- S7 (group): r_i = b~_i - dot, score, lambda, key; group argmax -> cand[grp] ----
         if (WPG > 1) group_bar(1 + grp, TG);
         else __syncwarp();
+        LPG(14)
         if (wg == 0 || (split2 && wg == 1)) {
             unsigned long long bk = 0ull;
             double bl = 0.0, bs = -1.0, rr2 = 0.0;
@@ -1184,9 +1253,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         stop = -3;
                         mx = 0ull;
                     }
-                    // no acquire fence: A~, b~ are immutable and the slot is LL-validated; the
-                    // proxy fence orders this thread's generic view before its TMA reads
-                    fence_proxy_async_global();
+                    // no acquire fence: A~, b~ are immutable and the slot is LL-validated (a proxy
+                    // fence here would order only this thread's own accesses, not the owner's slot
+                    // store, so none is issued: a stale TMA copy of the slot fails its tags)
                     LP(3)
 #if CSK_PHASE_PROF
                     if (p.skew && lane == 0 && k >= 8 && k < 72) {
@@ -1217,7 +1286,7 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                                 oslot = p.slots_r[orank] + par_off + static_cast<size_t>(olc) * kSlotWords;
                                 orow = p.At_r[orank] + (wrow - p.dlo[orank]) * n;
                             }
-                            LP(11)
+                            LPT(11)
                             unsigned long long *sb = const_cast<unsigned long long *>(slotbuf);
                             sb[4] = reinterpret_cast<unsigned long long>(orow);
                             sb[7] = reinterpret_cast<unsigned long long>(oslot);
@@ -1226,11 +1295,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                                 // mbarrier (odd n: the row is read with plain loads in the update)
                                 const uint32_t rbytes = even ? static_cast<uint32_t>(n) * 8u : 0u;
                                 mbar_arrive_expect_tx(mbar, rbytes + 32u);
-                                LP(12)
+                                LPT(12)
                                 bulk_g2s(sb, oslot, 32u, mbar);
-                                LP(13)
+                                LPT(13)
                                 if (even) bulk_g2s(rowbuf, orow, rbytes, mbar);
-                                LP(14)
+                                LPT(14)
                             } else {
                                 // across GPUs: the slot by system-scope loads (LL-validated), the
                                 // row by plain loads from the peer's memory in the update
@@ -1292,6 +1361,9 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                 lam = ll_val(slotbuf[0], slotbuf[1]);
                 sc = ll_val(slotbuf[2], slotbuf[3]);
             } else if (!CLU) {  // the copy raced the owner's slot store: re-read until the tags match
+#if CSK_PHASE_PROF
+                if (prof) ph[15] += 1000;  // (per mille of the iterations, in the probe's per-iteration print)
+#endif
                 const unsigned long long *gs = reinterpret_cast<const unsigned long long *>(slotbuf[7]);
                 lam = ll_load(gs, tag, SYS);
                 sc = ll_load(gs + 2, tag, SYS);
@@ -1327,6 +1399,8 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         }
     }
 #undef LP
+#undef LPG
+#undef LPT
     if constexpr (ST) {  // drain the copies already issued for the iteration that never ran
         if (producer && SC > 0) {
             const uint32_t g0 = static_cast<uint32_t>(k + 1) * static_cast<uint32_t>(SC);
@@ -1514,6 +1588,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
             return fail(ctx, CSK_E_ARG, "csk_solve: group_warps must be 1, 2, 4 or 8");
         if (opts->group_warps > wpg) wpg = opts->group_warps;
     }
+    {  // A/B knob: force the group width (may go below the default: more columns per thread)
+        static const int fw = getenv("CSK_LOOP_WPG") ? atoi(getenv("CSK_LOOP_WPG")) : 0;
+        if (fw > 0 && fw <= kLW && (fw & (fw - 1)) == 0 && 32 * fw * 16 >= n) wpg = fw;
+    }
     if (32 * wpg * 16 < n) return fail(ctx, CSK_E_UNSUPPORTED, "csk_solve: n too large for the register GEMV");
     int cb = 1;
     while (32 * wpg * cb < n) cb *= 2;
@@ -1566,6 +1644,8 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
         if (allow_tm && ((flags & CSK_SOLVE_FORCE_TMEM) || g.rb - g.rr > 0)) {
             // narrow when every row past 8 register rows fits in TMEM (no shared-memory tier)
             tmk = (g.rb - kTmRegRowsNarrow <= kTmRows) ? 2 : 1;
+            static const int ftmk = getenv("CSK_LOOP_TMK") ? atoi(getenv("CSK_LOOP_TMK")) : 0;  // A/B knob
+            if (ftmk == 1 || ftmk == 2) tmk = ftmk;
             g.rr = reg_rows(tmk == 2 ? kTmRegRowsNarrow : kTmRegRowsWide);
             g.rt = (g.rb - g.rr) < kTmRows ? (g.rb - g.rr) : kTmRows;
             g.rs = smem_fit(g.rb - g.rr - g.rt);
@@ -1740,6 +1820,8 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.report = static_cast<int64_t *>(ctx->report.ptr);
     prm.bb = bb;
     prm.wpg = wpg;
+    static const int fuse_ts = getenv("CSK_LOOP_FUSE_TS") ? atoi(getenv("CSK_LOOP_FUSE_TS")) : 1;  // A/B knob
+    prm.fuse_ts = fuse_ts;
     prm.rr = rr;
     prm.rs = rs;
     prm.rt = rt;

@@ -5,6 +5,7 @@ Phases: 0 GEMV + group finalize, 1 B1 wait, 2 CTA argmax + publish, 3 spin, 4 TM
 slot load, 5 B2 wait, 6 row wait, 7 update.  w0 = warp 0 (exchange), w7 = last warp (RES test).
 """
 import os
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -16,11 +17,11 @@ import paper_2004_02480_b200 as csk  # noqa: E402
 from csk_synth import CONFIGS, make_config  # noqa: E402
 
 NAMES = ["gemv+final", "arrive(leader)", "combine+publish", "spin", "post", "B2", "rowwait", "upd", "fence",
-         "owner+tma", "stopchk", "owner", "sb+expect", "slotcp", "rowcp"]
+         "owner+tma", "stopchk", "owner", "sb+expect", "slotcp", "rowcp", "slot_reread_permille"]
 
 
 def main():
-    names = [a for a in sys.argv[1:] if a in CONFIGS] or ["C1", "C2", "C3"]
+    names = [a for a in sys.argv[1:] if a in CONFIGS or re.fullmatch(r"\d+x\d+", a)] or ["C1", "C2", "C3"]
     ctas = [0]
     wpgs = [0]
     for a in sys.argv[1:]:
@@ -29,10 +30,18 @@ def main():
         if a.startswith("--wpg="):
             wpgs = [int(v) for v in a.split("=")[1].split(",")]
     for nm in names:
-        cfg = CONFIGS[nm]
-        p = make_config(cfg, "cuda")
-        At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
-        cap = cfg.max_iters if nm != "C4" else 3000
+        if nm in CONFIGS:
+            cfg = CONFIGS[nm]
+            p = make_config(cfg, "cuda")
+            At, bt, nsq = csk.csk_sketch(p.A, p.b, cfg.d, seed=cfg.sketch_seed)
+            cap = cfg.max_iters if nm != "C4" else 3000
+        else:  # "DxN": a random A~ of that shape (b~ = A~ x*), 1500 iterations
+            d, n = (int(v) for v in nm.split("x"))
+            g = torch.Generator(device="cuda").manual_seed(d * 7919 + n)
+            At = torch.randn(d, n, dtype=torch.float64, device="cuda", generator=g)
+            xs = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+            bt, nsq, cap = At @ xs, (At * At).sum(1), 1500
+            p = type("P", (), {"x_star": xs})()
         for G, wpg in [(g, w) for g in ctas for w in wpgs]:
             csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, group_warps=wpg)
             ph = torch.zeros(32 + 64 * 2 * 160, dtype=torch.int64, device="cuda")
@@ -63,8 +72,8 @@ def main():
                       + ", ".join(f"{i}: {late[i].item():.0f}" for i in order)
                       + f" | mean lateness by CTA quarter: {q[0]:.0f} {q[1]:.0f} {q[2]:.0f} {q[3]:.0f}"
                       + f" | median {late.median().item():.0f}")
-            w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(15))
-            w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(15) if c[16 + i])
+            w0 = " ".join(f"{NAMES[i]}={c[i] / it:.0f}" for i in range(16))
+            w7 = " ".join(f"{NAMES[i]}={c[16 + i] / it:.0f}" for i in range(16) if c[16 + i])
             print(f"{nm} G={geo['num_ctas']} wpg={wpg} IT={r.iterations} {ms * 1e3 / it:.2f} us/it = "
                   f"{ms * 1e6 / it * 1.965:.0f} cyc/it | w0 cyc/it: {w0} | w7: {w7}", flush=True)
 
