@@ -73,6 +73,8 @@ struct LoopParams {
     const double *bb;         // residual mode: ||b~||^2 (device scalar)
     int wpg;                  // warps per row group (1, 2, 4, 8)
     int fuse_ts;              // full TMEM tier + shared-memory rows in one interleaved pass
+    int npoll;                // exchange polls in flight per CTA (1: one at a time)
+    int pdelay;               // cycles between their first issues
     int rr;                   // rows per group held in registers (<= RRMAX)
     int rs;                   // rows per group held in shared memory
     int rt;                   // rows per group held in tensor memory (TM variants, <= 16)
@@ -1230,11 +1232,57 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
                         timed_out = __any_sync(0xffffffffu, timed_out);
                         c = static_cast<unsigned long long>(G);
                     } else {
-                        do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
-                            if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
-                            else ld_relaxed_v2(pair, c, mx);
-                            if (c < static_cast<unsigned long long>(G) && watchdog()) break;
-                        } while (c < static_cast<unsigned long long>(G));
+                        if (TM == 0 && !CLU && p.npoll > 1) {  // (not built into the TMEM-tier or cluster kernels)
+                            // A/B knob CSK_LOOP_NPOLL: staggered polls, NP loads of the pair in
+                            // flight, issued ~pdelay cycles apart and each re-issued as soon as it
+                            // returns short of G (the count reaching G would be seen ~RT/NP after
+                            // it lands).  Measured SLOWER (C3 2.87 -> 3.05 / 3.52 us at NP = 2 / 4):
+                            // the extra reads of the one hot line delay the atomics on it.  The
+                            // default (one poll at a time) is the loop below.
+                            constexpr int NP = 4;
+                            unsigned long long pc[NP], pm[NP], ps[NP];
+                            const int np = p.npoll < NP ? p.npoll : NP;
+                            auto issue = [&](int i) {
+                                if (RESMODE) ld_relaxed_v4(pair, pc[i], pm[i], ps[i]);
+                                else ld_relaxed_v2(pair, pc[i], pm[i]);
+                            };
+#pragma unroll
+                            for (int i = 0; i < NP; ++i) {
+                                if (i < np) {
+                                    if (i > 0) {
+                                        const long long t0 = clock64();
+                                        while (clock64() - t0 < p.pdelay) {}
+                                    }
+                                    issue(i);
+                                }
+                            }
+                            bool got = false;
+                            while (!got) {
+#pragma unroll
+                                for (int i = 0; i < NP; ++i) {
+                                    if (!got && i < np) {
+                                        if (pc[i] >= static_cast<unsigned long long>(G)) {
+                                            c = pc[i];
+                                            mx = pm[i];
+                                            rsum = ps[i];
+                                            got = true;
+                                        } else {
+                                            issue(i);
+                                        }
+                                    }
+                                }
+                                if (!got && watchdog()) {
+                                    c = 0ull;
+                                    break;
+                                }
+                            }
+                        } else {
+                            do {  // relaxed polls (an acquire load would invalidate L1 on every poll)
+                                if (RESMODE) ld_relaxed_v4(pair, c, mx, rsum);
+                                else ld_relaxed_v2(pair, c, mx);
+                                if (c < static_cast<unsigned long long>(G) && watchdog()) break;
+                            } while (c < static_cast<unsigned long long>(G));
+                        }
 #if CSK_STRICT_ACQUIRE
                         // the PTX-model form of the read (memory-model note):
                         // the count seen by a relaxed poll plus an acquire fence synchronizes with
@@ -1822,6 +1870,10 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.wpg = wpg;
     static const int fuse_ts = getenv("CSK_LOOP_FUSE_TS") ? atoi(getenv("CSK_LOOP_FUSE_TS")) : 1;  // A/B knob
     prm.fuse_ts = fuse_ts;
+    static const int npoll = getenv("CSK_LOOP_NPOLL") ? atoi(getenv("CSK_LOOP_NPOLL")) : 1;  // A/B knobs
+    static const int pdelay = getenv("CSK_LOOP_PDELAY") ? atoi(getenv("CSK_LOOP_PDELAY")) : 150;
+    prm.npoll = npoll;
+    prm.pdelay = pdelay;
     prm.rr = rr;
     prm.rs = rs;
     prm.rt = rt;
