@@ -328,7 +328,9 @@ k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int3
             if (lane == 31) count[j] = incl;
         }
     } else
-    for (int64_t j = gtid; j < d; j += gthreads) {
+    // thread per bucket; consecutive warps of buckets go to consecutive CTAs (warp-major over the
+    // grid), so the d / 32 busy warps spread over every SM instead of filling the first few CTAs
+    for (int64_t j = ((static_cast<int64_t>(warp) * G + c) << 5) + lane; j < d; j += gthreads) {
         int32_t run = 0;
         for (int q0 = 0; q0 < G; q0 += 16) {  // 16 loads in flight, then the prefix and the stores
             int32_t v[16];
@@ -370,10 +372,12 @@ k_plan_hist(uint64_t seed, int64_t row_offset, int32_t m, uint32_t d, const int3
     __syncthreads();
     const int32_t local = wsum[warp] + incl - run;
     grid.sync();
-    if (tid == 0) {
+    if (warp == 0) {  // base of this CTA's slice: the totals of the CTAs before it (a warp sum)
         int32_t bsum = 0;
-        for (int q = 0; q < c; ++q) bsum += ctot[q];
-        sbase = bsum;
+        for (int q = lane; q < c; q += 32) bsum += ctot[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+        if (lane == 0) sbase = bsum;
     }
     __syncthreads();
     int32_t base = sbase + local;
@@ -489,6 +493,8 @@ csk_status_t build_plan(csk_ctx_t ctx, uint64_t seed, int64_t row_offset, int64_
         m <= 512 * d) {
         int G = static_cast<int>((m + 255) / 256);
         if (G > ctx->num_sms) G = ctx->num_sms;
+        static const int gcap = getenv("CSK_PLAN_G") ? atoi(getenv("CSK_PLAN_G")) : 0;  // A/B knob
+        if (gcap > 0 && G > gcap) G = gcap;
         if (G < 1) G = 1;
         CSK_CHECK(ensure(ctx, ctx->keys_in, static_cast<size_t>(d + 1) * 4 + 2 * static_cast<size_t>(ctx->num_sms) * 4 + 64));
         int32_t *count = static_cast<int32_t *>(ctx->keys_in.ptr);
