@@ -361,6 +361,30 @@ def test_solve_tmem_tier(csk, n, d, num_ctas, reg_rows, group_warps):
     assert np.array_equal(_np(g.idx_trace)[:n_same], o.idx_trace[:n_same])
 
 
+@pytest.mark.parametrize("n,rs", [(1000, 3), (1000, 5), (1000, 12), (999, 7)])
+def test_solve_fused_tmem_smem_pass(csk, n, rs):
+    """C4's layout (4 warps per group: 6 register rows, the full 16-row TMEM tier, rs shared-memory
+    rows per thread) runs the interleaved TMEM + shared-memory pass (loop.cu tmem_smem_fused) with
+    one 32-row tree: capped run with the oracle's i_k sequence and RES, lockstep with r_k."""
+    G = 16
+    d = G * 2 * (6 + 16 + rs)  # two 4-warp groups per CTA
+    m = max(4 * d, 8 * n)
+    p = make_dense(m, n, "gauss", 700 + n + rs, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, d, seed=rs)
+    cap = 300
+    g = csk.csk_solve(At, bt, nsq, x_star=p.x_star, max_iters=cap, num_ctas=G, tmem=True, trace=cap + 1,
+                      trace_x=True, trace_r=60)
+    t = csk.csk_last_solve_tiers()
+    assert (t["num_ctas"], t["group_warps"], t["reg_rows"], t["tmem_rows"], t["smem_rows"], t["ring_stages"]) == \
+        (G, 4, 6, 16, rs, 0), t
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(p.x_star), max_iters=cap,
+                     trace=cap + 1)
+    assert g.termination == o.termination == csk.MAX_ITERS
+    assert np.array_equal(_np(g.idx_trace), o.idx_trace)
+    assert abs(g.final_res - o.final_res) <= 1e-6 * o.final_res
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 60, g.r_trace)
+
+
 @pytest.mark.parametrize("n", [1, 3, 63, 64, 65, 129, 1023, 2047, 2048])
 def test_solve_ragged_n(csk, n):
     """Ragged widths around the 64-column lane groups and the n <= 2048 register limit.
