@@ -532,6 +532,8 @@ def mwrk_compare(csk, ctx, cfg, p, csk_ms, csk_it):
 
 
 def extras(csk, ctx, names, flush):
+    _, sm_max_mhz, _ = _peaks()
+    smem_gbs = 148 * SMEM_BYTES_PER_CLK_PER_SM * sm_max_mhz * 1e6 / 1e9
     res = {}
     for nm in names:
         cfg = CONFIGS[nm]
@@ -565,6 +567,13 @@ def extras(csk, ctx, names, flush):
                    "us_per_iteration": round(sv * 1e3 / max(rep.iterations, 1), 4),
                    "sketch_hbm_gbs": round(alg_bytes_sketch(cfg) / (sk * 1e-3) / 1e9, 1),
                    "loop_gbs": round(alg_bytes_iter(cfg) * rep.iterations / (sv * 1e-3) / 1e9, 1)}
+        # t_bw = the loop's bytes per iteration over the SMEM yardstick, beside t_iter
+        t_iter = sv * 1e3 / max(rep.iterations, 1)
+        t_bw = alg_bytes_iter(cfg) / (smem_gbs * 1e9) * 1e6
+        res[nm].update({"loop_t_bw_us": round(t_bw, 4), "loop_t_bw_frac": round(t_bw / t_iter, 4),
+                        "loop_floor_note": "t_iter's fixed part (grid exchange + winner-row fetch + update) is "
+                                           "~2.3-2.5 us on 148 CTAs (one row per CTA, profiles/r02_loop_scan.txt); "
+                                           "C1/C2 run one 16-CTA cluster (DSMEM exchange)"})
         del p, At
         torch.cuda.empty_cache()
     return res
