@@ -1,33 +1,36 @@
-// loop.cu -- S5..S8: the Algorithm 1 loop as ONE persistent kernel,
-// A~ held in REGISTERS (then shared memory, then re-read from L2/HBM), one flat
-// atomic exchange per iteration.
+// loop.cu -- S5..S8: the Algorithm 1 loop as ONE persistent kernel, A~ held
+// on chip (registers, then TMEM, then shared memory; rows past those re-read from L2/HBM
+// through a TMA ring), one flat atomic exchange per iteration.
 //
-// Grid: G cooperative CTAs (default: one per SM), 8 warps each, no clusters.  CTA c owns
-// the contiguous rows [d c/G, d (c+1)/G) of A~.  Its warps form RG = 8/WPG row groups of
-// WPG warps (TG = 32 WPG threads); group g owns a balanced contiguous slice of the CTA's
-// rows, and thread t of a group owns the columns c_q = t + TG q (q < CB), so every group
-// holds all n columns and keeps its own copy of x_k in registers (CB doubles per thread).
-// Row i of a group lives in
-//   i <  rr            : registers   (a[i][q], CB doubles per row per thread)
-//   rr <= i < rr + rs  : shared memory, [i][q][t] (a warp reads 32 consecutive doubles)
-//   otherwise          : re-read from L2/HBM every iteration (coalesced along c_q).
+// Grid: G cooperative CTAs (default: one per SM), 8 warps each (C1/C2-sized systems: one
+// 16-CTA cluster with a DSMEM exchange instead).  CTA c owns the contiguous rows
+// [d c/G, d (c+1)/G) of A~.  Its warps form RG = 8/WPG row groups of WPG warps (TG = 32 WPG
+// threads); group g owns a balanced contiguous slice of the CTA's rows, and thread t of a group
+// owns the columns c_q = t + TG q (q < CB), so every group holds all n columns and keeps its own
+// copy of x_k in registers (CB doubles per thread).  Row i of a group lives in
+//   i <  rr                 : registers   (a[i][q], CB doubles per row per thread)
+//   rr <= i < rr + rt       : TMEM (CB = 8: 16 TMEM columns per row in the thread's lane)
+//   ... < rr + rt + rs      : shared memory, [i][q/2][t][2] (16-byte words, conflict-free)
+//   otherwise               : streamed from L2/HBM every iteration (TMA ring, ST variants)
 //
 // Iteration k (no launch, no grid barrier beyond the exchange itself):
-//   S6  GEMV: thread partials sum_q fma(a[i][q], x_q) in q order; register rows reduce
-//       across the warp with a transposed shuffle tree (row i ends in a fixed lane group),
-//       other rows with a xor butterfly; warp partials of a row are added in warp order.
-//       Fixed order everywhere -> identical bits in every run.
-//   S5  RES_k = ||x_k - x*||^2 / ||x*||^2 from group 0's registers, in every CTA
+//   S6  GEMV: thread partials sum_q fma(a[i][q], x_q) in q order; rows reduce across the warp
+//       with a transposed shuffle tree (row i ends in a fixed lane group); a full TMEM tier and
+//       the shared-memory rows go through one interleaved pass and one 32-row tree (C4);
+//       warp partials of a row are added in warp order.  Fixed order everywhere -> identical
+//       bits in every run.
+//   S5  RES_k = ||x_k - x*||^2 / ||x*||^2 from the last group's registers, in every CTA
 //       (identical arithmetic -> every CTA takes the same stop decision, no communication).
 //   S7  score_i = r_i^2/nsq_i (masked rows never win).  A row's 64-bit key is
 //       (score bits >> (b-1)) << b | (2^b - 1 - i), b = bits(d+1): max key = max score,
 //       ties (equal in the kept 53-b mantissa bits) -> lowest row index (R-15).
 //       CTA argmax -> one red.max.u64 of the key + one red.release.add of an arrival
-//       counter on the same 16-byte pair; thread 0 spins on a 16-byte acquire load of
-//       {count, max} until all G CTAs arrived (3 rotating pairs, CTA 0 clears the next).
-//   S8  every CTA reads the winner's (lambda, score) slot, TMA-copies A~^(ik) into shared
-//       memory, and applies x_q += lambda a_ik[c_q] with the same fma in every copy, so all
-//       copies of x stay bit-identical.
+//       counter on the same 16-byte pair; warp 0 polls {count, max} with relaxed 16-byte loads
+//       until all G CTAs arrived (3 rotating pairs, CTA 0 clears the next; DESIGN.md section 6,
+//       memory-model note).
+//   S8  every CTA TMA-copies the winner's (lambda, score) slot and A~^(ik) into shared memory
+//       and applies x_q += lambda a_ik[c_q] with the same fma in every copy, so all copies of x
+//       stay bit-identical.
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
