@@ -62,6 +62,31 @@ def test_virtual_ranks_match_oracle(csk, P):
     assert abs(g.iterations - rep.iterations) <= max(1, 0.05 * o.iterations)
 
 
+def test_virtual_ranks_c4_layout(csk):
+    """The SYS kernel with C4's per-CTA layout (4-warp groups of 6 register + 16 TMEM + 12
+    shared-memory rows: the fused TMEM + shared-memory pass) in a 2-rank decomposition: the
+    oracle's i_k sequence, r_k within the lockstep bar, identical copies of x."""
+    from test_gpu_parity import _lockstep
+    P, n = 2, 1000
+    d = P * 74 * 68  # 74 CTAs per virtual rank, 68 rows each
+    g = torch.Generator(device="cuda").manual_seed(2468)
+    At = torch.randn(d, n, dtype=torch.float64, device="cuda", generator=g)
+    xs = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    bt = At @ xs
+    nsq = csk.csk_row_norms(At)
+    cap = 80
+    x, copies, rep, tr = csk.csk_solve_virtual_ranks(At, bt, nsq, P, x_star=xs, tol=1e-30, max_iters=cap,
+                                                     trace=cap + 1, trace_x=True, trace_r=20)
+    t = csk.csk_last_solve_tiers()
+    assert (t["group_warps"], t["reg_rows"], t["tmem_rows"], t["smem_rows"]) == (4, 6, 16, 12), t
+    assert all(torch.equal(copies[q], copies[0]) for q in range(P))
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x_star=_np(xs), tol=1e-30, max_iters=cap,
+                     trace=cap + 1)
+    assert rep.termination == o.termination == csk.MAX_ITERS
+    assert np.array_equal(_np(tr.idx_trace)[:cap], o.idx_trace[:cap])
+    _lockstep(At, bt, nsq, tr.x_trace, tr.idx_trace, 20, tr.r_trace)
+
+
 @pytest.mark.parametrize("P", [2, 4])
 def test_virtual_ranks_streamed_rows(csk, P):
     """Rows past the on-chip tiers (92 MB of A > what 148 SMs hold) stream through the TMA ring
