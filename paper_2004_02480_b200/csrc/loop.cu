@@ -235,6 +235,26 @@ __device__ __forceinline__ double treduce(double (&v)[V], int lane) {
     return v[0];
 }
 
+// One level (lane mask o, cnt rows still live) of treduce<V>: the same adds in the same order,
+// so a tree run level by level (interleaved with other work) gives treduce's bits.
+template <int V>
+__device__ __forceinline__ void treduce_level(double (&v)[V], int lane, int o, int cnt) {
+    if (cnt > 1) {
+        const int half = cnt >> 1;
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < V / 2; ++j) {
+            if (j < half) {
+                const double send = upper ? v[j] : v[j + half];
+                const double keep = upper ? v[j + half] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+    } else {
+        v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+}
+
 template <int N>
 struct Pow2Ceil {
     static constexpr int v = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
@@ -416,9 +436,10 @@ __device__ __forceinline__ void tmem_block_wide(uint32_t taddr, const double (&x
 // 0: one 32-row transposed tree follows.  Every row's partial has the order of the separate tier
 // passes (tmem_block_wide, smem_block), and the 32-row tree adds the lanes in the same bit order as
 // two 16-row trees, so the dot products are bit-identical to theirs.
-template <int RSM>
+template <int RSM, int VR = 1>
 __device__ __forceinline__ void tmem_smem_fused(uint32_t taddr, const double *arows, int tg, int rs, int TG,
-                                                 const double (&x)[8], double (&acc)[32]) {
+                                                 const double (&x)[8], double (&acc)[32],
+                                                 double *racc = nullptr) {
     static_assert(RSM * 4 <= 48, "six shared-memory units per TMEM row pair");
     const double2 *a2 = reinterpret_cast<const double2 *>(arows) + tg;
 #pragma unroll
@@ -435,6 +456,17 @@ __device__ __forceinline__ void tmem_smem_fused(uint32_t taddr, const double *ar
                 const double2 val = a2[(static_cast<size_t>(ii) * 4 + qp) * TG];
                 acc[16 + i] = __fma_rn(val.x, x[2 * qp], acc[16 + i]);
                 acc[16 + i] = __fma_rn(val.y, x[2 * qp + 1], acc[16 + i]);
+            }
+        }
+        if constexpr (VR > 1) {
+            // the register rows' tree, one level per step (levels o = 16, 8, 4, 2, 1)
+            if ((j >> 1) < 5) {
+                const int lvl = j >> 1;
+                int cnt = VR;
+#pragma unroll
+                for (int t = 0; t < 5; ++t)
+                    if (t < lvl && cnt > 1) cnt >>= 1;
+                treduce_level<VR>(*reinterpret_cast<double(*)[VR]>(racc), threadIdx.x & 31, 16 >> lvl, cnt);
             }
         }
         tmem_wait_ld(v);
@@ -792,19 +824,23 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         // the full TMEM tier and the shared-memory rows in one interleaved pass (C4's layout)
         const bool fused = TM == 1 && !ST && rt == kTmRowsDev && rs >= 1 && rs <= 12 && fuse_ts;
         bool smem_done = false;  // the fused pass took the shared-memory rows
+        double racc[V];  // register rows' partials (their tree runs inside the fused pass)
         {
-            double acc[V];
 #pragma unroll
-            for (int i = 0; i < V; ++i) acc[i] = 0.0;
+            for (int i = 0; i < V; ++i) racc[i] = 0.0;
 #pragma unroll
             for (int q = 0; q < CB; ++q) {
 #pragma unroll
-                for (int i = 0; i < RRMAX; ++i) acc[i] = __fma_rn(a[i][q], x[q], acc[i]);
+                for (int i = 0; i < RRMAX; ++i) racc[i] = __fma_rn(a[i][q], x[q], racc[i]);
             }
-            const double s = treduce<V>(acc, lane);
-            sreg = s;
-            const int i = lane / LPR;
-            if ((lane % LPR) == 0 && i < rr && !(all_reg && wg == 0)) dotp[wg * RM + lr0 + i] = s;
+            if (!(TM == 1 && fused)) {
+                const double s = treduce<V>(racc, lane);
+                sreg = s;
+                const int i = lane / LPR;
+                if ((lane % LPR) == 0 && i < rr && !(all_reg && wg == 0)) dotp[wg * RM + lr0 + i] = s;
+            } else {
+                sreg = 0.0;  // (TMEM rows present: the finalize reads dotp)
+            }
         }
         LPG(11)
         // ---- S6 GEMV: TMEM rows, blocks of 8 (two rows per tcgen05.ld), transposed tree ----
@@ -816,7 +852,11 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
             if (fused) {
                 // full TMEM tier + the shared-memory rows in one interleaved pass, one 32-row tree
                 double acc32[32];
-                tmem_smem_fused<12>(tbase, arows, tg, rs, TG, x, acc32);
+                tmem_smem_fused<12, V>(tbase, arows, tg, rs, TG, x, acc32, racc);
+                {  // the register rows' tree finished inside the pass: row i in lanes [i LPR, (i+1) LPR)
+                    const int i = lane / LPR;
+                    if ((lane % LPR) == 0 && i < rr) dotp[wg * RM + lr0 + i] = racc[0];
+                }
                 const double s = treduce<32>(acc32, lane);
                 if (lane < 16) dotp[wg * RM + lr0 + rr + lane] = s;
                 else if (lane - 16 < rs) dotp[wg * RM + lr0 + rr + rt + lane - 16] = s;
