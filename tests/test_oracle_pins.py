@@ -51,6 +51,17 @@ def test_hash_survey_vectors_seed0_d500():
     assert int(c2.max()) == int(rows["c2_max_bucket"][0])
 
 
+def test_hash_golden_file_matches_its_generator():
+    """The golden file's data lines are exactly what the committed big-int script prints."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gen_hash", os.path.join(GOLDEN, "gen_hash_seed0_d500.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    with open(os.path.join(GOLDEN, "hash_seed0_d500.txt")) as f:
+        data = [ln.rstrip("\n") for ln in f if ln.strip() and not ln.startswith("#")]
+    assert data == gen.golden_lines()
+
+
 def _mix(z):
     z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
     z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
