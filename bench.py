@@ -678,10 +678,11 @@ def run_reference(args):
     del p
     oracle.build()
     runs = max(3, min(args.steps, 5))
-    cb = _oracle_timed(cfg, A, b, xs, runs=runs, warmup=1)
+    warm = max(1, min(args.warmup, 5))  # the requested W untimed samples (capped at 5: ~3 s each)
+    cb = _oracle_timed(cfg, A, b, xs, runs=runs, warmup=warm)
     v = cb["value"]
     return {"metric": METRIC, "value": v, "unit": "ms", "n_gpus": 0,
-            "steps": runs, "warmup": 1, "ms_per_step": v,
+            "steps": runs, "warmup": warm, "ms_per_step": v,
             "higher_is_better": False, "impl": "reference", "dtype": "f64",
             "data": ("synthetic (torch Philox on the GPU, copied to the host: the same bytes as our arm; csk_synth.py)"
                      if on_gpu else "synthetic (torch Philox CPU stream; no GPU here, csk_synth.py)"),
@@ -690,7 +691,7 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "iterations": cb["iterations"], "vs_baseline": None,
             "note": f"each step = one pinned single-core oracle sample (median of {runs}); "
-                    "--steps K is clamped to 3..5 samples so the arm finishes in about a minute"}
+                    "--steps K is clamped to 3..5 samples and --warmup W to 1..5 so the arm finishes in about a minute"}
 
 
 def _sharded_roofline(dist, cfg, ws, it, kloop, ksk):
