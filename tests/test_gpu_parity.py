@@ -426,6 +426,35 @@ def test_solve_residual_mode(csk, num_ctas, cluster):
     _lockstep(At, bt, nsq, g2.x_trace, g2.idx_trace, 200, g2.r_trace)
 
 
+@pytest.mark.parametrize("m,n,d,kw,resmode", [
+    (6000, 40, 400, {}, False),                                   # one 16-CTA cluster (DSMEM exchange)
+    (6000, 40, 400, {"num_ctas": 148, "cluster_size": 1}, True),  # grid exchange, residual stop
+    (60000, 300, 3000, {}, False),                                # register rows on 148 CTAs
+    (40000, 1000, 2000, {"num_ctas": 16, "tmem": True}, False),   # TMEM + shared-memory tiers
+])
+def test_solve_warm_start(csk, m, n, d, kw, resmode):
+    """Algorithm 1 from an arbitrary x0 (INPUT ... x0; the loop P:61-64 is the same from any
+    start): the kernel takes x0 from x, and its trajectory follows the oracle's from the same x0 --
+    lockstep with r_k, the same i_k sequence and stop."""
+    p = make_dense(m, n, "gauss", 900 + n, "cuda")
+    At, bt, nsq = csk.csk_sketch(p.A, p.b, d, seed=11)
+    gen = torch.Generator().manual_seed(4242 + n)
+    x0 = (torch.randn(n, generator=gen, dtype=torch.float64) * 3.0).to("cuda")
+    xs = None if resmode else p.x_star
+    cap = 400
+    tol = 1e-8 if resmode else 1e-6
+    g = csk.csk_solve(At, bt, nsq, x0=x0, x_star=xs, tol=tol, max_iters=cap, trace=cap + 1, trace_x=True,
+                      trace_r=80, **kw)
+    assert torch.equal(g.x_trace[0], x0), "x_0 is not the given start"
+    o = oracle.solve(_np(At), _np(bt), oracle.row_norms(_np(At)), x0=_np(x0), x_star=None if xs is None else _np(xs),
+                     tol=tol, max_iters=cap, trace=cap + 1)
+    assert g.termination == o.termination
+    assert abs(g.iterations - o.iterations) <= max(1, 0.05 * o.iterations)
+    _lockstep(At, bt, nsq, g.x_trace, g.idx_trace, 80, g.r_trace)
+    k = min(g.iterations, o.iterations)
+    assert np.array_equal(_np(g.idx_trace)[:k], o.idx_trace[:k])
+
+
 def test_solve_edge_cases(csk):
     dev = "cuda"
     # A = I4, b = (4,3,2,1): exactly 4 steps, indices 0..3 (S:283)
