@@ -263,6 +263,23 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
         : "memory");
 }
 
+// The same copy with an L2 eviction priority (createpolicy, whole-line fraction 1.0): `keep`
+// marks the lines evict_last (they stay in the 126 MB L2 between loop iterations), otherwise
+// evict_first (a streamed row that will not be re-read before L2 has turned over).
+__device__ __forceinline__ void bulk_g2s_l2(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                            uint64_t *bar, bool keep) {
+    uint64_t pol;
+    if (keep)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // Streaming read-only 16-byte load that does not allocate in L1.  Deliberately not
 // `volatile`: the data is immutable for the kernel's lifetime, and a volatile asm
 // would pin the loads in program order and serialise them.

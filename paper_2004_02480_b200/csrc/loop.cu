@@ -100,6 +100,8 @@ struct LoopParams {
     int64_t dlo[kMaxRanks + 1];             // rank r owns the global rows [dlo[r], dlo[r+1])
     int RMr[kMaxRanks];                     // rank r's rows per CTA, ceil((dlo[r+1]-dlo[r]) / Gr)
     int st_rows, st_stages;                 // ST variants: rows per stream-ring stage, stages per row group
+    int st_rest_first;                      // ST: the chunks past st_pin are copied evict_first (1) or without a hint (0)
+    int st_pin;                             // ST: each group's first st_pin chunks are kept in L2 (evict_last), the rest evict_first; < 0: no hints
     unsigned long long rm_magic;            // P = 1: ceil(2^40 / RM) if (d-1) RM < 2^40 (row -> CTA by a multiply), else 0
     const double *At_r[kMaxRanks];          // rank r's rows of A~ (row dlo[r] first)
     const double *bt_r[kMaxRanks];
@@ -269,6 +271,12 @@ constexpr size_t kRowbufOff = 1664;
 struct LoopSmem {
     size_t ctl, mbar, slotbuf, cand, resp, btl, invl, dotp, xs, rowbuf, arows, ring, rbar, total;
 };
+// Streamed rows kept resident in L2 (copied evict_last; the other streamed rows evict_first): 96 MB of
+// the 126 MB L2 measured best on the B200 (C5 loop 88.5 -> 85.6 us/iteration, MWRK on C3 54.1 -> 50.5;
+// 128 MB and above falls back to the unhinted time), and only for ring chunks of at least 16 KB (with
+// 4.8-8 KB chunks the hinted copies measured 4-6 % slower).  profiles/r02_l2pin_ab.txt.
+constexpr int kLoopL2PinMB = 96;           // CSK_LOOP_L2PIN_MB overrides (0: no hints)
+constexpr int kLoopL2PinMinChunk = 16000;  // bytes; CSK_LOOP_L2PIN_MINCHUNK overrides
 // Bytes of one stream-ring stage: st_rows whole rows of A~ (a 128-B multiple)
 __host__ __device__ inline size_t st_stage_bytes(int64_t n, int st_rows) {
     return (static_cast<size_t>(st_rows) * static_cast<size_t>(n) * 8 + 127) & ~size_t(127);
@@ -603,7 +611,13 @@ __global__ void __launch_bounds__(kLT, 1) k_loop(const LoopParams p) {
         const int nr = min(SR, ng - s0 - c * SR);
         const uint32_t by = static_cast<uint32_t>(nr) * static_cast<uint32_t>(n) * 8u;
         mbar_arrive_expect_tx(rbar + 2 * st, by);
-        bulk_g2s(ring + st * st_stride, Ash + (r0 - dlo_r + lr0 + s0 + c * SR) * n, by, rbar + 2 * st);
+        if (p.st_pin < 0)
+            bulk_g2s(ring + st * st_stride, Ash + (r0 - dlo_r + lr0 + s0 + c * SR) * n, by, rbar + 2 * st);
+        else if (c < p.st_pin || p.st_rest_first)
+            bulk_g2s_l2(ring + st * st_stride, Ash + (r0 - dlo_r + lr0 + s0 + c * SR) * n, by, rbar + 2 * st,
+                        c < p.st_pin);
+        else
+            bulk_g2s(ring + st * st_stride, Ash + (r0 - dlo_r + lr0 + s0 + c * SR) * n, by, rbar + 2 * st);
     };
 
     if (tid == 0) {
@@ -1922,6 +1936,20 @@ csk_status_t run_loop(csk_ctx_t ctx, const double *At, const double *bt, const d
     prm.rt = rt;
     prm.st_rows = geo.st_rows;
     prm.st_stages = geo.st_stages;
+    // L2 residency of the streamed rows: the first CSK_LOOP_L2PIN_MB megabytes of them (split evenly
+    // over the row groups, whole ring chunks) are copied with evict_last, the rest with evict_first,
+    // so that part of A~ is served from L2 every iteration instead of from HBM.  0: no hints.
+    static const int l2pin_mb = getenv("CSK_LOOP_L2PIN_MB") ? atoi(getenv("CSK_LOOP_L2PIN_MB")) : kLoopL2PinMB;
+    static const int l2rest = getenv("CSK_LOOP_L2PIN_REST") ? atoi(getenv("CSK_LOOP_L2PIN_REST")) : 1;
+    prm.st_rest_first = l2rest;
+    prm.st_pin = -1;
+    static const int l2minchunk =
+        getenv("CSK_LOOP_L2PIN_MINCHUNK") ? atoi(getenv("CSK_LOOP_L2PIN_MINCHUNK")) : kLoopL2PinMinChunk;
+    if (geo.st_rows > 0 && l2pin_mb > 0 && static_cast<int64_t>(geo.st_rows) * n * 8 >= l2minchunk) {
+        const double chunk = static_cast<double>(geo.st_rows) * static_cast<double>(n) * 8.0;
+        const double groups = static_cast<double>(G) * static_cast<double>(rg);
+        prm.st_pin = static_cast<int>(static_cast<double>(l2pin_mb) * 1.0e6 / (chunk * groups));
+    }
     prm.key_bits = kb;
     prm.rows_max = rows_max;
     prm.trace_cap = opts ? opts->trace_cap : 0;
