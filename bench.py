@@ -472,7 +472,9 @@ def c5_extra(csk, ctx, cap=None):
             "streamed_rows_per_iteration": streamed_rows,
             "loop_streamed_hbm_gbs": round(gbs, 1), "loop_streamed_hbm_frac": round(gbs / peak, 4),
             "note": "time to RES <= 1e-6 on one GPU (second of two runs); rows past the on-chip tiers are "
-                    "re-read from HBM every iteration through the TMA stream ring"}
+                    "re-read every iteration through the TMA stream ring; 96 MB of them stay L2-resident "
+                    "(evict_last copies, the rest evict_first), so loop_streamed_hbm_gbs is algorithmic bytes per "
+                    "iteration time and may exceed the HBM copy peak"}
 
 
 def c4_uncapped(csk, ctx, cap=2_000_000):
